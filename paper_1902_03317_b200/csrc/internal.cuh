@@ -1,0 +1,158 @@
+// Internal helpers shared by the sm_100a kernels behind include/spten_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/spten_b200.h"
+
+// ---------------------------------------------------------------------------
+// Host side: context, errors, scratch.
+
+struct spt_ctx {
+  int device = 0;
+  int num_sms = 148;
+  size_t l2_bytes = 0;
+  // Sticky device error words (min entry index of the first failure), reset
+  // to all-ones. [0] tew_eq pattern mismatch, [1] tew_eq div-by-zero,
+  // [2] mttkrp unsorted input, [3] spare.
+  unsigned long long* d_err = nullptr;
+  // Growable scratch (sort temp storage, counts, ...).
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  // Decoupled look-back state: per-tile status words tagged with an epoch,
+  // a self-resetting tile-id counter and R-wide fp64 payloads.
+  uint32_t* d_status = nullptr;
+  size_t status_cap = 0;  // tiles
+  double* d_payload = nullptr;
+  size_t payload_cap = 0;  // doubles
+  unsigned long long* d_tile_ctr = nullptr;
+  uint32_t epoch = 0;
+  // Pinned host words for count read-back.
+  unsigned long long* h_pinned = nullptr;
+  // L2 flush buffer.
+  void* l2buf = nullptr;
+  size_t l2buf_bytes = 0;
+  uint64_t launches = 0;
+};
+
+namespace spt {
+
+int set_error(int status, const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+// Grow-only scratch; may synchronise the device when it grows.
+int ctx_scratch(spt_ctx* ctx, size_t bytes, void** out);
+// Look-back state sized for `tiles` tiles and `payload_doubles` doubles;
+// returns the epoch to pass to the kernel (never 0).
+int ctx_lookback(spt_ctx* ctx, size_t tiles, size_t payload_doubles, uint32_t* epoch);
+// Validate a descriptor (order range, nnz limit, non-null pointers when nnz>0).
+int check_coo(const spt_coo* t, const char* who, bool need_values = true);
+// Synchronise `stream` and decode the sticky error words.
+int sync_and_check(spt_ctx* ctx, cudaStream_t stream);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline unsigned grid_for(uint64_t work_items, unsigned block, unsigned max_blocks) {
+  uint64_t g = (work_items + block - 1) / block;
+  if (g == 0) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return static_cast<unsigned>(g);
+}
+
+#define SPT_CUDA(call)                                               \
+  do {                                                               \
+    cudaError_t _e = (call);                                         \
+    if (_e != cudaSuccess) return ::spt::cuda_status(_e, #call);     \
+  } while (0)
+
+#define SPT_LAUNCHED(ctx)                                                           \
+  do {                                                                              \
+    cudaError_t _e = cudaGetLastError();                                            \
+    if (_e != cudaSuccess) return ::spt::cuda_status(_e, "kernel launch");          \
+    (ctx)->launches++;                                                              \
+  } while (0)
+
+#define SPT_TRY(expr)              \
+  do {                             \
+    int _s = (expr);               \
+    if (_s != SPT_OK) return _s;   \
+  } while (0)
+
+// Internal entry points implemented in the other translation units.
+int sort_tuples(spt_ctx* ctx, const spt_coo* x, const uint32_t* mode_order, uint32_t* d_perm,
+                cudaStream_t stream);  // stable; d_perm receives the permutation
+int gather_coo(spt_ctx* ctx, spt_coo* x, const uint32_t* d_perm, cudaStream_t stream);
+
+}  // namespace spt
+
+// ---------------------------------------------------------------------------
+// Device side.
+
+namespace spt {
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// Streaming (evict-first) 128-bit loads/stores for data touched once.
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) { __stcs(p, v); }
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+  return __ldcs(reinterpret_cast<const unsigned int*>(p));
+}
+__device__ __forceinline__ void st_stream(uint32_t* p, uint32_t v) {
+  __stcs(reinterpret_cast<unsigned int*>(p), v);
+}
+
+// Acquire/release on a status word (gpu scope) for decoupled look-back.
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// Philox4x32-10 counter-based RNG (Salmon et al., SC'11).
+struct Philox {
+  static __host__ __device__ __forceinline__ uint4 round(uint4 c, uint2 k) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    uint32_t hi0 = __umulhi_compat(M0, c.x), lo0 = M0 * c.x;
+    uint32_t hi1 = __umulhi_compat(M1, c.z), lo1 = M1 * c.z;
+    return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  static __host__ __device__ __forceinline__ uint32_t __umulhi_compat(uint32_t a, uint32_t b) {
+    return static_cast<uint32_t>((static_cast<uint64_t>(a) * b) >> 32);
+  }
+  static __host__ __device__ __forceinline__ uint4 gen(uint64_t counter, uint64_t stream,
+                                                       uint64_t seed) {
+    uint4 c = make_uint4(static_cast<uint32_t>(counter), static_cast<uint32_t>(counter >> 32),
+                         static_cast<uint32_t>(stream), static_cast<uint32_t>(stream >> 32));
+    uint2 k = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+      c = round(c, k);
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    return c;
+  }
+};
+
+// 24-bit mantissa uniform in [0,1).
+__host__ __device__ __forceinline__ float u01(uint32_t r) {
+  return static_cast<float>(r >> 8) * (1.0f / 16777216.0f);
+}
+// 53-bit uniform in [0,1).
+__host__ __device__ __forceinline__ double u01d(uint32_t a, uint32_t b) {
+  return static_cast<double>((static_cast<uint64_t>(a) << 21) ^ (b >> 11)) *
+         (1.0 / 9007199254740992.0);
+}
+
+}  // namespace spt

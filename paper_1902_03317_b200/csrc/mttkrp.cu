@@ -1,0 +1,543 @@
+// K8 MTTKRP: out(i_n, r) = sum_m val_m * prod_{d != n, ascending} F_d(i_d(m), r).
+//
+// Reference: seq::mttkrp P/src/kernels_seq.cpp:153-174, par::mttkrp
+// P/src/kernels_par.cpp:275-337, mttkrp_row P/src/kernel_detail.hpp:176-188,
+// check_mttkrp_inputs P/src/kernel_detail.hpp:153-174.
+//
+// Segmented strategy (input sorted with the output mode leading, i.e. entries
+// of one output row are contiguous):
+//   * A CTA owns a tile of TILE=2048 consecutive entries, staged into shared
+//     memory with 128-bit loads. Tile ids are taken from a self-resetting
+//     atomic counter so predecessors are always resident (look-back safety).
+//   * Each warp splits into P = 32/G lane groups; a group owns a contiguous
+//     run of entries and each lane holds VEC consecutive columns (float4
+//     gathers: an R=32 factor row is one 128-byte line read by 8 lanes).
+//     Gathers for U=4 entries are issued before any is consumed.
+//   * Per-term products are formed in fp32 exactly as the reference does
+//     (val, then *= F_d for d ascending), so every term is bit-identical to
+//     seq's; accumulation is in fp64 and each output element is rounded
+//     once, which keeps the result within 1e-5 of an fp64 recomputation even
+//     for the heavy Zipf rows (a serial fp32 chain would not be).
+//   * Rows that start and end inside one group are written directly (plain
+//     128-bit stores, one writer per row, no atomics); the first/last run of
+//     each group goes to a shared-memory slot; the CTA folds the slots, writes
+//     the rows it completes and zero-fills every empty row in its range, so
+//     the output needs no memset and each element is written exactly once.
+//   * A row that continues across tiles is completed with a decoupled
+//     look-back over fp64 R-wide tile partials (status words tagged with a
+//     per-launch epoch, so no per-launch reset is needed). Tiles whose first
+//     row starts inside them never wait.
+//   * The kernel verifies the sortedness it relies on (free: it reads the
+//     mode index anyway) and reports violations through the context's
+//     error word.
+// Atomic strategy (any order): zero the output, then vector red.global.add
+// per term group -- the analogue of the reference's `omp atomic` strategy.
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kTile = 2048;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kFlagA = 1, kFlagP = 2, kFlagBoundary = 4;
+
+struct MttkrpParams {
+  const uint32_t* out_idx;
+  const uint32_t* oidx[SPT_MAX_ORDER - 1];
+  const float* ofac[SPT_MAX_ORDER - 1];
+  const float* val;
+  float* out;
+  uint64_t nnz;
+  uint32_t rows;   // I_n
+  uint32_t R;      // row stride of factors and output
+  uint32_t c0;     // first column handled by this launch
+  uint32_t ncols;  // columns handled (<= CB)
+  uint32_t ntiles;
+  uint32_t epoch;
+  uint32_t* status;
+  double* payA;  // [ntiles][CB]
+  double* payP;  // [ntiles][CB]
+  unsigned long long* tile_ctr;
+  unsigned long long* err;
+};
+
+template <int VEC>
+struct Vec;
+template <>
+struct Vec<4> {
+  static __device__ __forceinline__ void load(const float* p, float (&f)[4]) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    f[0] = v.x;
+    f[1] = v.y;
+    f[2] = v.z;
+    f[3] = v.w;
+  }
+  static __device__ __forceinline__ void store(float* p, const float (&f)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+  }
+};
+template <>
+struct Vec<1> {
+  static __device__ __forceinline__ void load(const float* p, float (&f)[1]) { f[0] = __ldg(p); }
+  static __device__ __forceinline__ void store(float* p, const float (&f)[1]) { *p = f[0]; }
+};
+
+// Zero rows [r0, r1) for this lane's columns.
+template <int VEC>
+__device__ __forceinline__ void zero_rows(float* out, uint32_t r0, uint32_t r1, uint32_t R,
+                                          uint32_t col, bool col_ok) {
+  if (!col_ok) return;
+  float z[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) z[k] = 0.0f;
+  for (uint32_t r = r0; r < r1; ++r) Vec<VEC>::store(out + (size_t)r * R + col, z);
+}
+
+template <int NM1, int G, int VEC>
+__global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
+  constexpr int P = 32 / G;            // groups per warp
+  constexpr int GROUPS = kWarps * P;   // groups per CTA
+  constexpr int EG = kTile / GROUPS;   // entries per group
+  constexpr int CB = G * VEC;          // columns per launch
+  constexpr int NSLOT = 2 * GROUPS;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_slot = reinterpret_cast<double*>(smem_raw);                 // [NSLOT][CB]
+  uint32_t* s_out = reinterpret_cast<uint32_t*>(s_slot + NSLOT * CB);  // [kTile]
+  float* s_val = reinterpret_cast<float*>(s_out + kTile);              // [kTile]
+  uint32_t* s_oidx = reinterpret_cast<uint32_t*>(s_val + kTile);       // [NM1][kTile]
+  __shared__ uint32_t s_slot_row[NSLOT];
+  __shared__ uint32_t s_tile, s_flag;
+  __shared__ uint32_t s_meta[4];
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    const unsigned long long t = atomicAdd(p.tile_ctr, 1ull);
+    if (t == p.ntiles - 1) atomicExch(p.tile_ctr, 0ull);  // last increment of this launch
+    s_tile = static_cast<uint32_t>(t);
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t t0 = (uint64_t)tile * kTile;
+  const int cnt = (p.nnz - t0 < (uint64_t)kTile) ? static_cast<int>(p.nnz - t0) : kTile;
+
+  // ---- stage the tile (mode index, values, other-mode indices) ----------
+  if (cnt == kTile) {
+    const int nv = kTile / 4;
+    for (int i = tid; i < nv; i += kThreads) {
+      reinterpret_cast<uint4*>(s_out)[i] = spt::ld_stream(reinterpret_cast<const uint4*>(p.out_idx + t0) + i);
+      reinterpret_cast<uint4*>(s_val)[i] =
+          spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0) + i);
+#pragma unroll
+      for (int j = 0; j < NM1; ++j)
+        reinterpret_cast<uint4*>(s_oidx + j * kTile)[i] =
+            spt::ld_stream(reinterpret_cast<const uint4*>(p.oidx[j] + t0) + i);
+    }
+  } else {
+    for (int i = tid; i < cnt; i += kThreads) {
+      s_out[i] = p.out_idx[t0 + i];
+      s_val[i] = p.val[t0 + i];
+#pragma unroll
+      for (int j = 0; j < NM1; ++j) s_oidx[j * kTile + i] = p.oidx[j][t0 + i];
+    }
+  }
+  for (int i = tid; i < NSLOT; i += kThreads) s_slot_row[i] = kNone;
+  __syncthreads();
+
+  // ---- per-group segmented accumulation ----------------------------------
+  const int warp = tid >> 5, lane = tid & 31;
+  const int group = warp * P + lane / G;
+  const int gl = lane % G;
+  const uint32_t lcol = gl * VEC;  // column within the block
+  const bool col_ok = lcol < p.ncols;
+  const uint32_t col = p.c0 + lcol;
+  const int e_begin = group * EG;
+  const int e_end = min(e_begin + EG, cnt);
+
+  uint32_t run_row = kNone;
+  bool first_run = true;
+  double acc[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) acc[k] = 0.0;
+
+  constexpr int kUnroll = (NM1 * VEC <= 12) ? 4 : 2;
+  for (int e = e_begin; e < e_end; e += kUnroll) {
+    float prod[kUnroll][VEC];
+    uint32_t rr[kUnroll];
+    // Issue every gather of the batch before consuming any.
+    float f[kUnroll][NM1][VEC];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int eu = e + u;
+      if (eu < e_end && col_ok) {
+#pragma unroll
+        for (int j = 0; j < NM1; ++j)
+          Vec<VEC>::load(p.ofac[j] + (size_t)s_oidx[j * kTile + eu] * p.R + col, f[u][j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NM1; ++j)
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) f[u][j][k] = 0.0f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int eu = e + u;
+      rr[u] = eu < e_end ? s_out[eu] : kNone;
+      const float v = eu < e_end ? s_val[eu] : 0.0f;
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        float t = v;  // row[r] = val; row[r] *= f_d[r] for d ascending
+#pragma unroll
+        for (int j = 0; j < NM1; ++j) t = __fmul_rn(t, f[u][j][k]);
+        prod[u][k] = t;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (rr[u] == kNone) continue;
+      const uint32_t row = rr[u];
+      if (row == run_row) {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[k] += (double)prod[u][k];
+      } else {
+        if (run_row != kNone) {
+          if (row < run_row) {
+            if (gl == 0) atomicMin(p.err + 2, (unsigned long long)(t0 + e + u));
+          }
+          if (first_run) {
+            const int slot = 2 * group;
+            if (gl == 0) s_slot_row[slot] = run_row;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) s_slot[slot * CB + lcol + k] = acc[k];
+            first_run = false;
+          } else if (col_ok) {
+            float o[VEC];
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) o[k] = (float)acc[k];
+            Vec<VEC>::store(p.out + (size_t)run_row * p.R + col, o);
+          }
+          if (row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
+        }
+        run_row = row;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[k] = (double)prod[u][k];
+      }
+    }
+  }
+  if (run_row != kNone) {
+    const int slot = 2 * group + (first_run ? 0 : 1);
+    if (gl == 0) s_slot_row[slot] = run_row;
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) s_slot[slot * CB + lcol + k] = acc[k];
+  }
+  __syncthreads();
+
+  // ---- CTA fold of the group boundary slots -------------------------------
+  const uint32_t head_row = s_out[0];
+  const uint32_t tail_row = s_out[cnt - 1];
+  if (tid == 0) {
+    const uint32_t prev_row = tile > 0 ? p.out_idx[t0 - 1] : kNone;
+    const uint32_t next_row = (tile + 1 < p.ntiles) ? p.out_idx[t0 + cnt] : kNone;
+    if (prev_row != kNone && prev_row > head_row) atomicMin(p.err + 2, (unsigned long long)t0);
+    if (next_row != kNone && next_row < tail_row)
+      atomicMin(p.err + 2, (unsigned long long)(t0 + cnt));
+    s_meta[0] = prev_row == head_row ? 1u : 0u;  // continues from previous tile
+    s_meta[1] = next_row == tail_row ? 1u : 0u;  // continues into next tile
+    s_meta[2] = next_row;
+  }
+  double head_acc = 0.0, tail_acc = 0.0;
+  const int c = tid;  // one thread per column of the block for the fold
+  if (c < CB) {
+    const bool cok = static_cast<uint32_t>(c) < p.ncols;
+    uint32_t cur_row = kNone;
+    int cur_group = -1;
+    double cur = 0.0;
+    for (int s = 0; s < NSLOT; ++s) {
+      const uint32_t r = s_slot_row[s];
+      if (r == kNone) continue;
+      const double v = s_slot[s * CB + c];
+      if (r == cur_row) {
+        cur += v;
+      } else {
+        if (cur_row != kNone) {
+          if (cur_row == head_row) head_acc = cur;
+          else if (cur_row == tail_row) tail_acc = cur;
+          else if (cok) p.out[(size_t)cur_row * p.R + p.c0 + c] = (float)cur;
+          if ((s >> 1) != cur_group && r > cur_row + 1 && cok)
+            for (uint32_t z = cur_row + 1; z < r; ++z) p.out[(size_t)z * p.R + p.c0 + c] = 0.0f;
+        }
+        cur_row = r;
+        cur = v;
+      }
+      cur_group = s >> 1;
+    }
+    if (cur_row != kNone) {
+      if (cur_row == head_row) head_acc = cur;
+      else tail_acc = cur;  // cur_row == tail_row
+    }
+  }
+  __syncthreads();
+  const bool cont_prev = s_meta[0] != 0;
+  const bool cont_next = s_meta[1] != 0;
+  const uint32_t next_row = s_meta[2];
+  const bool boundary = head_row != tail_row;
+
+  // ---- inter-tile zero fill ------------------------------------------------
+  if (c < CB && static_cast<uint32_t>(c) < p.ncols) {
+    if (tile == 0)
+      for (uint32_t z = 0; z < head_row; ++z) p.out[(size_t)z * p.R + p.c0 + c] = 0.0f;
+    const uint32_t stop = next_row == kNone ? p.rows : next_row;
+    for (uint32_t z = tail_row + 1; z < stop; ++z) p.out[(size_t)z * p.R + p.c0 + c] = 0.0f;
+  }
+
+  // ---- decoupled look-back for rows spanning tiles ------------------------
+  double carry = 0.0;
+  const uint32_t tag = p.epoch << 3;
+  if (cont_next && (boundary || !cont_prev)) {
+    // Inclusive partial of the tail row is known without predecessors.
+    if (c < CB) {
+      p.payP[(size_t)tile * CB + c] = boundary ? tail_acc : head_acc;
+      __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) spt::st_release(p.status + tile, tag | kFlagP);
+  } else if (cont_next) {
+    // Single-row tile continuing both ways: publish the aggregate first.
+    if (c < CB) {
+      p.payA[(size_t)tile * CB + c] = head_acc;
+      __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) spt::st_release(p.status + tile, tag | kFlagA);
+  }
+  if (cont_prev) {
+    uint32_t j = tile - 1;
+    while (true) {
+      if (tid == 0) {
+        uint32_t s;
+        do {
+          s = spt::ld_acquire(p.status + j);
+        } while ((s >> 3) != p.epoch || (s & 3u) == 0);
+        s_flag = s;
+      }
+      __syncthreads();
+      const uint32_t s = s_flag;
+      const double* pay = (s & kFlagP) ? p.payP : p.payA;
+      if (c < CB) carry += spt::ld_cg(pay + (size_t)j * CB + c);
+      __syncthreads();
+      if ((s & kFlagP) || (s & kFlagBoundary) || j == 0) break;
+      --j;
+    }
+    if (cont_next && !boundary) {
+      if (c < CB) {
+        p.payP[(size_t)tile * CB + c] = carry + head_acc;
+        __threadfence();
+      }
+      __syncthreads();
+      if (tid == 0) spt::st_release(p.status + tile, tag | kFlagP);
+    }
+  }
+
+  // ---- rows completed by this tile ------------------------------------------
+  if (c < CB && static_cast<uint32_t>(c) < p.ncols) {
+    if (boundary || !cont_next) p.out[(size_t)head_row * p.R + p.c0 + c] = (float)(carry + head_acc);
+    if (boundary && !cont_next) p.out[(size_t)tail_row * p.R + p.c0 + c] = (float)tail_acc;
+  }
+}
+
+template <int NM1, int G, int VEC>
+__global__ void __launch_bounds__(kThreads) mttkrp_atomic_kernel(MttkrpParams p) {
+  constexpr int P = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const uint32_t lcol = gl * VEC;
+  if (lcol >= p.ncols) return;
+  const uint32_t col = p.c0 + lcol;
+  const uint64_t gid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / G;
+  const uint64_t ngroups = (uint64_t)gridDim.x * blockDim.x / G;
+  (void)P;
+  for (uint64_t m = gid; m < p.nnz; m += ngroups) {
+    float f[NM1][VEC];
+#pragma unroll
+    for (int j = 0; j < NM1; ++j) Vec<VEC>::load(p.ofac[j] + (size_t)p.oidx[j][m] * p.R + col, f[j]);
+    const float v = p.val[m];
+    float* o = p.out + (size_t)p.out_idx[m] * p.R + col;
+    float t[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      t[k] = v;
+#pragma unroll
+      for (int j = 0; j < NM1; ++j) t[k] = __fmul_rn(t[k], f[j][k]);
+    }
+    if constexpr (VEC == 4) {
+      atomicAdd(reinterpret_cast<float4*>(o), make_float4(t[0], t[1], t[2], t[3]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) atomicAdd(o + k, t[k]);
+    }
+  }
+}
+
+template <int G, int VEC>
+size_t seg_smem(int nm1) {
+  constexpr int GROUPS = kWarps * (32 / G);
+  constexpr int CB = G * VEC;
+  return (size_t)2 * GROUPS * CB * sizeof(double) + (size_t)kTile * (2 + nm1) * sizeof(uint32_t);
+}
+
+using KernelFn = void (*)(MttkrpParams);
+
+template <int G, int VEC>
+KernelFn pick_seg(int nm1) {
+  switch (nm1) {
+    case 1: return mttkrp_seg_kernel<1, G, VEC>;
+    case 2: return mttkrp_seg_kernel<2, G, VEC>;
+    case 3: return mttkrp_seg_kernel<3, G, VEC>;
+    case 4: return mttkrp_seg_kernel<4, G, VEC>;
+    case 5: return mttkrp_seg_kernel<5, G, VEC>;
+    case 6: return mttkrp_seg_kernel<6, G, VEC>;
+    default: return mttkrp_seg_kernel<7, G, VEC>;
+  }
+}
+
+template <int G, int VEC>
+KernelFn pick_atomic(int nm1) {
+  switch (nm1) {
+    case 1: return mttkrp_atomic_kernel<1, G, VEC>;
+    case 2: return mttkrp_atomic_kernel<2, G, VEC>;
+    case 3: return mttkrp_atomic_kernel<3, G, VEC>;
+    case 4: return mttkrp_atomic_kernel<4, G, VEC>;
+    case 5: return mttkrp_atomic_kernel<5, G, VEC>;
+    case 6: return mttkrp_atomic_kernel<6, G, VEC>;
+    default: return mttkrp_atomic_kernel<7, G, VEC>;
+  }
+}
+
+struct Variant {
+  int G, VEC;
+  KernelFn seg, atomic;
+  size_t smem;
+};
+
+// Column blocking: float4 lanes when R % 4 == 0 (G = smallest power of two
+// with G*4 >= R, at most 32 -> 128 columns per launch), scalar lanes otherwise
+// (32 columns per launch).
+Variant choose_variant(uint32_t R, int nm1) {
+  if (R % 4 == 0) {
+    const uint32_t q = R / 4;
+    if (q <= 2) return {2, 4, pick_seg<2, 4>(nm1), pick_atomic<2, 4>(nm1), seg_smem<2, 4>(nm1)};
+    if (q <= 4) return {4, 4, pick_seg<4, 4>(nm1), pick_atomic<4, 4>(nm1), seg_smem<4, 4>(nm1)};
+    if (q <= 8) return {8, 4, pick_seg<8, 4>(nm1), pick_atomic<8, 4>(nm1), seg_smem<8, 4>(nm1)};
+    if (q <= 16)
+      return {16, 4, pick_seg<16, 4>(nm1), pick_atomic<16, 4>(nm1), seg_smem<16, 4>(nm1)};
+    return {32, 4, pick_seg<32, 4>(nm1), pick_atomic<32, 4>(nm1), seg_smem<32, 4>(nm1)};
+  }
+  return {32, 1, pick_seg<32, 1>(nm1), pick_atomic<32, 1>(nm1), seg_smem<32, 1>(nm1)};
+}
+
+}  // namespace
+
+extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors,
+                              const uint64_t* rows, const uint64_t* cols, uint32_t mode,
+                              float* d_out, int strategy, unsigned flags, void* stream) {
+  if (!ctx) return spt::set_error(SPT_EINVAL, "mttkrp: null context");
+  SPT_TRY(spt::check_coo(x, "mttkrp"));
+  const uint32_t N = x->order;
+  // P/src/kernel_detail.hpp:157-173
+  if (N < 2) return spt::set_error(SPT_EINVAL, "mttkrp: input must have order >= 2");
+  if (mode >= N) return spt::set_error(SPT_EINVAL, "mttkrp: mode out of range");
+  if (!x->coalesced) return spt::set_error(SPT_EINVAL, "mttkrp: tensor must be coalesced");
+  if (!d_factors || !rows || !cols)
+    return spt::set_error(SPT_EINVAL, "mttkrp: need one factor matrix per mode");
+  uint64_t R = 0;
+  for (uint32_t d = 0; d < N; ++d) {
+    if (d == mode) continue;
+    if (R == 0) R = cols[d];
+    if (cols[d] != R)
+      return spt::set_error(SPT_EINVAL, "mttkrp: factor matrices must share the column count");
+    if (rows[d] != x->dims[d])
+      return spt::set_error(SPT_EINVAL, "mttkrp: factor rows must match the mode dimension");
+  }
+  if (R == 0) return spt::set_error(SPT_EINVAL, "mttkrp: factor rank must be >= 1");
+  if (R > 0xFFFFFFFFull) return spt::set_error(SPT_EOVERFLOW, "mttkrp: rank too large");
+  for (uint32_t d = 0; d < N; ++d)
+    if (d != mode && !d_factors[d] && x->dims[d] > 0)
+      return spt::set_error(SPT_EINVAL, "mttkrp: null factor for mode %u", d);
+  const uint32_t I = x->dims[mode];
+  if (I > 0 && !d_out) return spt::set_error(SPT_EINVAL, "mttkrp: null output");
+  cudaStream_t st = spt::as_stream(stream);
+  if (I == 0) return SPT_OK;
+  if (x->nnz == 0) {
+    SPT_CUDA(cudaMemsetAsync(d_out, 0, (size_t)I * R * sizeof(float), st));
+    return SPT_OK;
+  }
+
+  const int nm1 = static_cast<int>(N) - 1;
+  Variant v = choose_variant(static_cast<uint32_t>(R), nm1);
+  bool aligned = true;
+  for (uint32_t d = 0; d < N; ++d)
+    if (d != mode && !spt::aligned16(d_factors[d])) aligned = false;
+  if (!spt::aligned16(d_out)) aligned = false;
+  if (v.VEC == 4 && !aligned) v = {32, 1, pick_seg<32, 1>(nm1), pick_atomic<32, 1>(nm1), seg_smem<32, 1>(nm1)};
+  const uint32_t CB = v.G * v.VEC;
+
+  if (strategy == SPT_MTTKRP_AUTO)
+    strategy = (x->has_sort_order && static_cast<uint32_t>(x->sort_order[0]) == mode)
+                   ? SPT_MTTKRP_SEGMENTED
+                   : SPT_MTTKRP_ATOMIC;
+  if (strategy != SPT_MTTKRP_SEGMENTED && strategy != SPT_MTTKRP_ATOMIC)
+    return spt::set_error(SPT_EINVAL, "mttkrp: unknown strategy %d", strategy);
+
+  MttkrpParams p{};
+  p.out_idx = x->idx[mode];
+  int j = 0;
+  for (uint32_t d = 0; d < N; ++d) {
+    if (d == mode) continue;
+    p.oidx[j] = x->idx[d];
+    p.ofac[j] = d_factors[d];
+    ++j;
+  }
+  p.val = x->val;
+  p.out = d_out;
+  p.nnz = x->nnz;
+  p.rows = I;
+  p.R = static_cast<uint32_t>(R);
+  p.err = ctx->d_err;
+  p.tile_ctr = ctx->d_tile_ctr;
+
+  if (strategy == SPT_MTTKRP_ATOMIC) {
+    SPT_CUDA(cudaMemsetAsync(d_out, 0, (size_t)I * R * sizeof(float), st));
+    ctx->launches++;
+    const unsigned grid = spt::grid_for(x->nnz * v.G, kThreads, ctx->num_sms * 16);
+    for (uint32_t c0 = 0; c0 < R; c0 += CB) {
+      p.c0 = c0;
+      p.ncols = static_cast<uint32_t>(std::min<uint64_t>(CB, R - c0));
+      v.atomic<<<grid, kThreads, 0, st>>>(p);
+      SPT_LAUNCHED(ctx);
+    }
+    return SPT_OK;
+  }
+
+  const uint64_t ntiles = (x->nnz + kTile - 1) / kTile;
+  p.ntiles = static_cast<uint32_t>(ntiles);
+  SPT_CUDA(cudaFuncSetAttribute(v.seg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(v.smem)));
+  for (uint32_t c0 = 0; c0 < R; c0 += CB) {
+    uint32_t epoch;
+    SPT_TRY(spt::ctx_lookback(ctx, ntiles, 2 * ntiles * CB, &epoch));
+    p.status = ctx->d_status;
+    p.payA = ctx->d_payload;
+    p.payP = ctx->d_payload + ntiles * CB;
+    p.epoch = epoch;
+    p.c0 = c0;
+    p.ncols = static_cast<uint32_t>(std::min<uint64_t>(CB, R - c0));
+    v.seg<<<static_cast<unsigned>(ntiles), kThreads, v.smem, st>>>(p);
+    SPT_LAUNCHED(ctx);
+  }
+  if (flags & SPT_FLAG_ASYNC) return SPT_OK;
+  return spt::sync_and_check(ctx, st);
+}

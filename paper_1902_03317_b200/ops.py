@@ -1,0 +1,291 @@
+"""Host-side mirror of the reference's kernel entry points, on device tensors.
+
+Same names, argument meaning and error behaviour as `spten::seq` / `spten::par`
+(P/include/spten/kernels_seq.hpp:18-71, P/include/spten/kernels_par.hpp:305-346)
+and the tensor helpers (P/include/spten/tensor.hpp:147-165); every call goes
+through the C-ABI (include/spten_b200.h) to the sm_100a kernels. There is no
+CPU path: without the built extension these functions raise.
+
+Flop accounting mirrors spten::flops (P/src/flop_counter.cpp:8-15): each op
+records the sequential reference's count (P/src/kernels_seq.cpp:37, 51, 65,
+99, 144, 172).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import (ADD, DIV, MUL, SUB, SCALAR_ADD, SCALAR_MUL, MTTKRP_AUTO, MTTKRP_ATOMIC,
+                   MTTKRP_SEGMENTED, InvalidArgument, check)
+from .coo import DeviceCOO, FiberIndex, ptr
+
+__all__ = [
+    "ADD", "SUB", "MUL", "DIV", "SCALAR_ADD", "SCALAR_MUL", "MTTKRP_AUTO", "MTTKRP_ATOMIC",
+    "MTTKRP_SEGMENTED", "flops", "ascending_order", "mode_last_order", "ts", "tew_eq", "tew",
+    "ttv", "ttm", "mttkrp", "sort_lexicographic", "coalesce", "build_fiber_index",
+]
+
+
+class _Flops:
+    """spten::flops::{reset,count,record} (P/include/spten/flop_counter.hpp:8-14)."""
+
+    def __init__(self):
+        self._n = 0
+
+    def reset(self) -> None:
+        self._n = 0
+
+    def count(self) -> int:
+        return self._n
+
+    def record(self, n: int) -> None:
+        self._n += int(n)
+
+
+flops = _Flops()
+
+
+def ascending_order(n: int) -> list:
+    """P/src/tensor.cpp:11-15"""
+    return list(range(n))
+
+
+def mode_last_order(n: int, mode: int) -> list:
+    """P/src/tensor.cpp:17-24"""
+    return [d for d in range(n) if d != mode] + [mode]
+
+
+def _ctx(t: DeviceCOO | torch.Tensor):
+    dev = t.device if isinstance(t, DeviceCOO) else t.device
+    if dev.type != "cuda":
+        raise InvalidArgument("spten_b200 ops need CUDA tensors (no CPU fallback)")
+    return _lib.Context.get(dev.index if dev.index is not None else 0)
+
+
+def _stream(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _flags(sync: bool) -> int:
+    return 0 if sync else _lib.SPT_FLAG_ASYNC
+
+
+# ---------------------------------------------------------------------------
+# TS (P/src/kernels_seq.cpp:55-67)
+
+
+def ts(x: DeviceCOO, s: float, op: int, out: Optional[DeviceCOO] = None,
+       sync: bool = True) -> DeviceCOO:
+    ctx = _ctx(x)
+    z = out if out is not None else DeviceCOO.empty(x.dims, x.nnz, x.device)
+    xd, zd = x.descriptor(), z.descriptor()
+    check(_lib.load().spt_ts_f32(ctx.handle, ctypes.byref(xd), float(s), int(op),
+                                 ctypes.byref(zd), _flags(sync), _stream(x.device)))
+    z.adopt(zd)
+    flops.record(x.nnz)
+    return z
+
+
+# ---------------------------------------------------------------------------
+# TEW-eq (P/src/kernels_seq.cpp:11-39)
+
+
+def tew_eq(x: DeviceCOO, y: DeviceCOO, op: int, out: Optional[DeviceCOO] = None,
+           sync: bool = True) -> DeviceCOO:
+    ctx = _ctx(x)
+    z = out if out is not None else DeviceCOO.empty(x.dims, x.nnz, x.device)
+    xd, yd, zd = x.descriptor(), y.descriptor(), z.descriptor()
+    check(_lib.load().spt_tew_eq_f32(ctx.handle, ctypes.byref(xd), ctypes.byref(yd), int(op),
+                                     ctypes.byref(zd), _flags(sync), _stream(x.device)))
+    z.adopt(zd)
+    flops.record(x.nnz)
+    return z
+
+
+# ---------------------------------------------------------------------------
+# Preprocessing (P/src/tensor.cpp:54-120)
+
+
+def sort_lexicographic(t: DeviceCOO, mode_order: Sequence[int], sync: bool = True) -> None:
+    """In-place stable lexicographic sort; sets t.sort_order (P/src/tensor.cpp:54-64)."""
+    ctx = _ctx(t)
+    mo = list(mode_order)
+    if len(mo) != t.order:
+        raise InvalidArgument("sort_lexicographic: mode order has wrong length")
+    if sorted(mo) != list(range(t.order)):
+        raise InvalidArgument("sort_lexicographic: mode order is not a permutation")
+    arr = (ctypes.c_uint32 * t.order)(*mo)
+    d = t.descriptor()
+    check(_lib.load().spt_sort_f32(ctx.handle, ctypes.byref(d), arr, _flags(sync),
+                                   _stream(t.device)))
+    t.sort_order = mo
+
+
+def coalesce(t: DeviceCOO) -> DeviceCOO:
+    """Merge duplicate tuples by summation in storage order (P/src/tensor.cpp:66-90).
+    Like the reference, an unsorted input is sorted (on a copy) ascending first."""
+    ctx = _ctx(t)
+    src = t
+    if t.sort_order is None:
+        src = t.clone()
+        sort_lexicographic(src, ascending_order(t.order))
+    z = DeviceCOO.empty(t.dims, t.nnz, t.device)
+    sd, zd = src.descriptor(), z.descriptor()
+    n = ctypes.c_uint64(0)
+    check(_lib.load().spt_coalesce_f32(ctx.handle, ctypes.byref(sd), ctypes.byref(zd),
+                                       ctypes.byref(n), None, 0, _stream(t.device)))
+    return z.adopt(zd, int(n.value))
+
+
+def build_fiber_index(t: DeviceCOO, mode: int) -> FiberIndex:
+    """P/src/tensor.cpp:92-120; fptr as device u32 offsets."""
+    ctx = _ctx(t)
+    if mode >= t.order:
+        raise InvalidArgument("build_fiber_index: mode out of range")
+    if t.sort_order is None or t.sort_order[-1] != mode:
+        raise InvalidArgument(
+            "build_fiber_index: tensor must be sorted with the target mode as the last key")
+    fptr = torch.empty(t.nnz + 1, dtype=torch.int32, device=t.device)
+    n = ctypes.c_uint64(0)
+    d = t.descriptor()
+    check(_lib.load().spt_fiber_index(ctx.handle, ctypes.byref(d), int(mode), fptr.data_ptr(),
+                                      ctypes.byref(n), None, 0, _stream(t.device)))
+    nf = int(n.value)
+    return FiberIndex(mode, nf, fptr[: nf + 1])
+
+
+# ---------------------------------------------------------------------------
+# TEW (P/src/kernels_seq.cpp:41-53, P/src/kernel_detail.hpp:36-102)
+
+
+def tew(x: DeviceCOO, y: DeviceCOO, op: int, out: Optional[DeviceCOO] = None) -> DeviceCOO:
+    """General elementwise op by sorted merge. Like the reference, sorts both
+    operands ascending *in place* unless they already share a sort order."""
+    ctx = _ctx(x)
+    if op == DIV:
+        raise InvalidArgument(
+            "tew: div is not defined for mismatched patterns (unmatched entries divide by zero)")
+    if x.order != y.order:
+        raise InvalidArgument("tew: tensors must have the same order")
+    if not (x.coalesced and y.coalesced):
+        raise InvalidArgument("tew: both inputs must be coalesced")
+    if not (x.sort_order is not None and y.sort_order is not None
+            and list(x.sort_order) == list(y.sort_order)):
+        order = ascending_order(x.order)
+        sort_lexicographic(x, order)
+        sort_lexicographic(y, order)
+    cap = x.nnz + y.nnz if op != MUL else min(x.nnz, y.nnz)
+    dims = [max(a, b) for a, b in zip(x.dims, y.dims)]
+    z = out if out is not None else DeviceCOO.empty(dims, max(cap, 0), x.device)
+    xd, yd, zd = x.descriptor(), y.descriptor(), z.descriptor()
+    n = ctypes.c_uint64(0)
+    check(_lib.load().spt_tew_f32(ctx.handle, ctypes.byref(xd), ctypes.byref(yd), int(op),
+                                  ctypes.byref(zd), cap, ctypes.byref(n), None, 0,
+                                  _stream(x.device)))
+    nz = int(n.value)
+    z.adopt(zd, nz)
+    # matches + sub negations (P/src/kernel_detail.hpp:55-83)
+    flops.record({ADD: x.nnz + y.nnz - nz, SUB: y.nnz, MUL: nz}[op])
+    return z
+
+
+# ---------------------------------------------------------------------------
+# TTV / TTM (P/src/kernels_seq.cpp:69-151)
+
+
+def _precheck(x: DeviceCOO, mode: int, kernel: str) -> None:
+    # P/src/kernel_detail.hpp:110-115
+    if x.order < 2:
+        raise InvalidArgument(f"{kernel}: input must have order >= 2")
+    if mode >= x.order:
+        raise InvalidArgument(f"{kernel}: mode out of range")
+    if not x.coalesced:
+        raise InvalidArgument(f"{kernel}: tensor must be coalesced")
+    if x.sort_order is None or x.sort_order[-1] != mode:
+        raise InvalidArgument(f"{kernel}: tensor must be sorted with the target mode last")
+
+
+def _fiber_checks(x: DeviceCOO, mode: int, fib: FiberIndex, kernel: str) -> None:
+    # P/src/kernel_detail.hpp:106-119
+    _precheck(x, mode, kernel)
+    if fib.mode != mode or fib.fptr.numel() != fib.nfibs + 1:
+        raise InvalidArgument(f"{kernel}: fiber index does not match the tensor")
+
+
+def ttv(x: DeviceCOO, v: torch.Tensor, mode: int, fib: Optional[FiberIndex] = None,
+        out: Optional[DeviceCOO] = None) -> DeviceCOO:
+    ctx = _ctx(x)
+    if fib is None:
+        _precheck(x, mode, "ttv")
+        fib = build_fiber_index(x, mode)
+    _fiber_checks(x, mode, fib, "ttv")
+    dims = [e for d, e in enumerate(x.dims) if d != mode]
+    z = out if out is not None else DeviceCOO.empty(dims, fib.nfibs, x.device)
+    xd, zd = x.descriptor(), z.descriptor()
+    check(_lib.load().spt_ttv_f32(ctx.handle, ctypes.byref(xd), ptr(v), v.numel(), int(mode),
+                                  fib.fptr.data_ptr(), fib.nfibs, ctypes.byref(zd), 0,
+                                  _stream(x.device)))
+    z.adopt(zd)
+    flops.record(2 * x.nnz)
+    return z
+
+
+def ttm(x: DeviceCOO, u: torch.Tensor, mode: int, fib: Optional[FiberIndex] = None,
+        out: Optional[DeviceCOO] = None) -> DeviceCOO:
+    ctx = _ctx(x)
+    if u.dim() != 2:
+        raise InvalidArgument("ttm: u must be a matrix")
+    if fib is None:
+        _precheck(x, mode, "ttm")
+        fib = build_fiber_index(x, mode)
+    _fiber_checks(x, mode, fib, "ttm")
+    R = int(u.shape[1])
+    dims = list(x.dims)
+    dims[mode] = R
+    z = out if out is not None else DeviceCOO.empty(dims, fib.nfibs * R, x.device)
+    xd, zd = x.descriptor(), z.descriptor()
+    check(_lib.load().spt_ttm_f32(ctx.handle, ctypes.byref(xd), ptr(u), int(u.shape[0]), R,
+                                  int(mode), fib.fptr.data_ptr(), fib.nfibs, ctypes.byref(zd), 0,
+                                  _stream(x.device)))
+    z.adopt(zd)
+    flops.record(2 * R * x.nnz)
+    return z
+
+
+# ---------------------------------------------------------------------------
+# MTTKRP (P/src/kernels_seq.cpp:153-174, P/src/kernels_par.cpp:275-337)
+
+
+def mttkrp(x: DeviceCOO, factors: Sequence[Optional[torch.Tensor]], mode: int,
+           strategy: int = MTTKRP_AUTO, out: Optional[torch.Tensor] = None,
+           sync: bool = True) -> torch.Tensor:
+    """Returns the dims[mode] x R row-major fp32 result on the device.
+    factors[mode] is ignored (may be None), as in the reference."""
+    ctx = _ctx(x)
+    N = x.order
+    if len(factors) != N:
+        raise InvalidArgument("mttkrp: need one factor matrix per mode")
+    fp = (ctypes.c_void_p * N)()
+    rows = (ctypes.c_uint64 * N)()
+    cols = (ctypes.c_uint64 * N)()
+    R = 0
+    for d, f in enumerate(factors):
+        if d == mode or f is None:
+            continue
+        if f.dim() != 2 or f.dtype != torch.float32 or not f.is_contiguous():
+            raise InvalidArgument("mttkrp: factors must be contiguous 2-D float32 tensors")
+        fp[d] = ptr(f)
+        rows[d] = int(f.shape[0])
+        cols[d] = int(f.shape[1])
+        R = R or int(f.shape[1])
+    I = x.dims[mode] if mode < N else 0
+    if out is None:
+        out = torch.empty((I, max(R, 1) if R else 0), dtype=torch.float32, device=x.device)
+    xd = x.descriptor()
+    check(_lib.load().spt_mttkrp_f32(ctx.handle, ctypes.byref(xd), fp, rows, cols, int(mode),
+                                     ptr(out), int(strategy), _flags(sync), _stream(x.device)))
+    flops.record(x.nnz * N * R)
+    return out
