@@ -55,8 +55,7 @@ int ctx_lookback(spt_ctx* ctx, size_t tiles, size_t payload_doubles, uint32_t* e
     size_t cap = tiles + tiles / 4 + 64;
     SPT_CUDA(cudaMalloc(&ctx->d_status, cap * sizeof(uint32_t)));
     SPT_CUDA(cudaMemset(ctx->d_status, 0, cap * sizeof(uint32_t)));
-    ctx->status_cap = cap;
-    ctx->epoch = 0;  // all words are epoch 0 now
+    ctx->status_cap = cap;  // fresh words are epoch 0, which is never issued
   }
   if (payload_doubles > ctx->payload_cap) {
     if (ctx->d_payload) {
@@ -73,9 +72,27 @@ int ctx_lookback(spt_ctx* ctx, size_t tiles, size_t payload_doubles, uint32_t* e
   if (ctx->epoch == 0) {
     SPT_CUDA(cudaDeviceSynchronize());
     SPT_CUDA(cudaMemset(ctx->d_status, 0, ctx->status_cap * sizeof(uint32_t)));
+    if (ctx->d_status64)
+      SPT_CUDA(cudaMemset(ctx->d_status64, 0, ctx->status64_cap * sizeof(unsigned long long)));
     ctx->epoch = 1;
   }
   *epoch = ctx->epoch;
+  return SPT_OK;
+}
+
+int ctx_status64(spt_ctx* ctx, size_t tiles, unsigned long long** out) {
+  if (tiles > ctx->status64_cap) {
+    if (ctx->d_status64) {
+      SPT_CUDA(cudaDeviceSynchronize());
+      SPT_CUDA(cudaFree(ctx->d_status64));
+      ctx->d_status64 = nullptr;
+    }
+    size_t cap = tiles + tiles / 4 + 64;
+    SPT_CUDA(cudaMalloc(&ctx->d_status64, cap * sizeof(unsigned long long)));
+    SPT_CUDA(cudaMemset(ctx->d_status64, 0, cap * sizeof(unsigned long long)));
+    ctx->status64_cap = cap;
+  }
+  *out = ctx->d_status64;
   return SPT_OK;
 }
 
@@ -191,6 +208,7 @@ void spt_ctx_destroy(spt_ctx* c) {
   cudaFree(c->scratch);
   cudaFree(c->d_status);
   cudaFree(c->d_payload);
+  cudaFree(c->d_status64);
   cudaFree(c->l2buf);
   cudaFreeHost(c->h_pinned);
   delete c;

@@ -32,6 +32,9 @@ struct spt_ctx {
   size_t payload_cap = 0;  // doubles
   unsigned long long* d_tile_ctr = nullptr;
   uint32_t epoch = 0;
+  // 64-bit look-back words (epoch | flag | u32 count) for count scans.
+  unsigned long long* d_status64 = nullptr;
+  size_t status64_cap = 0;
   // Pinned host words for count read-back.
   unsigned long long* h_pinned = nullptr;
   // L2 flush buffer.
@@ -49,6 +52,9 @@ int ctx_scratch(spt_ctx* ctx, size_t bytes, void** out);
 // Look-back state sized for `tiles` tiles and `payload_doubles` doubles;
 // returns the epoch to pass to the kernel (never 0).
 int ctx_lookback(spt_ctx* ctx, size_t tiles, size_t payload_doubles, uint32_t* epoch);
+// 64-bit status words for `tiles` tiles (zeroed on growth); use with an epoch
+// from ctx_lookback.
+int ctx_status64(spt_ctx* ctx, size_t tiles, unsigned long long** out);
 // Validate a descriptor (order range, nnz limit, non-null pointers when nnz>0).
 int check_coo(const spt_coo* t, const char* who, bool need_values = true);
 // Synchronise `stream` and decode the sticky error words.
@@ -118,6 +124,14 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 // Philox4x32-10 counter-based RNG (Salmon et al., SC'11).
 struct Philox {
@@ -135,7 +149,6 @@ struct Philox {
     uint4 c = make_uint4(static_cast<uint32_t>(counter), static_cast<uint32_t>(counter >> 32),
                          static_cast<uint32_t>(stream), static_cast<uint32_t>(stream >> 32));
     uint2 k = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
-#pragma unroll
     for (int i = 0; i < 10; ++i) {
       c = round(c, k);
       k.x += 0x9E3779B9u;

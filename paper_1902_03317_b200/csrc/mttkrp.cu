@@ -62,7 +62,40 @@ struct MttkrpParams {
   double* payP;  // [ntiles][CB]
   unsigned long long* tile_ctr;
   unsigned long long* err;
+  // TTM (FIBER=true): output rows are fibers of an x sorted with `mode` last.
+  const uint32_t* fptr;
+  const uint32_t* tile_fiber;
+  const uint32_t* hidx[SPT_MAX_ORDER];  // x.indices[d] for the output index tuples
+  uint32_t* zidx[SPT_MAX_ORDER];        // z.indices[d]
+  uint32_t N;
+  uint32_t mode;
 };
+
+// TTM output index tuples of fiber `row` for `ncol` columns starting at col:
+// z.indices[d][row*R + r] = head index of the fiber (d != mode) or r
+// (P/src/kernels_seq.cpp:128-138).
+template <int NCOL>
+__device__ __forceinline__ void ttm_emit_idx(const MttkrpParams& p, uint32_t head,
+                                             uint32_t row, uint32_t col) {
+  const size_t base = (size_t)row * p.R + col;
+  for (uint32_t d = 0; d < p.N; ++d) {
+    uint32_t w[NCOL];
+    if (d == p.mode) {
+#pragma unroll
+      for (int k = 0; k < NCOL; ++k) w[k] = col + k;
+    } else {
+      const uint32_t h = p.hidx[d][head];
+#pragma unroll
+      for (int k = 0; k < NCOL; ++k) w[k] = h;
+    }
+    if constexpr (NCOL == 4) {
+      *reinterpret_cast<uint4*>(p.zidx[d] + base) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NCOL; ++k) p.zidx[d][base + k] = w[k];
+    }
+  }
+}
 
 template <int VEC>
 struct Vec;
@@ -96,7 +129,7 @@ __device__ __forceinline__ void zero_rows(float* out, uint32_t r0, uint32_t r1, 
   for (uint32_t r = r0; r < r1; ++r) Vec<VEC>::store(out + (size_t)r * R + col, z);
 }
 
-template <int NM1, int G, int VEC>
+template <int NM1, int G, int VEC, bool FIBER>
 __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
   constexpr int P = 32 / G;            // groups per warp
   constexpr int GROUPS = kWarps * P;   // groups per CTA
@@ -109,6 +142,7 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
   uint32_t* s_out = reinterpret_cast<uint32_t*>(s_slot + NSLOT * CB);  // [kTile]
   float* s_val = reinterpret_cast<float*>(s_out + kTile);              // [kTile]
   uint32_t* s_oidx = reinterpret_cast<uint32_t*>(s_val + kTile);       // [NM1][kTile]
+  uint32_t* s_fptr = s_oidx + NM1 * kTile;                             // FIBER: [kTile+2]
   __shared__ uint32_t s_slot_row[NSLOT];
   __shared__ uint32_t s_tile, s_flag;
   __shared__ uint32_t s_meta[4];
@@ -125,10 +159,19 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
   const int cnt = (p.nnz - t0 < (uint64_t)kTile) ? static_cast<int>(p.nnz - t0) : kTile;
 
   // ---- stage the tile (mode index, values, other-mode indices) ----------
+  uint32_t f_lo = 0, nstage = 0;
+  if constexpr (FIBER) {
+    f_lo = p.tile_fiber[tile];
+    const uint32_t f_end = (tile + 1 < p.ntiles) ? p.tile_fiber[tile + 1] + 1 : p.rows;
+    nstage = f_end - f_lo + 1;
+    for (uint32_t i = tid; i < nstage; i += kThreads) s_fptr[i] = p.fptr[f_lo + i];
+  }
   if (cnt == kTile) {
     const int nv = kTile / 4;
     for (int i = tid; i < nv; i += kThreads) {
-      reinterpret_cast<uint4*>(s_out)[i] = spt::ld_stream(reinterpret_cast<const uint4*>(p.out_idx + t0) + i);
+      if constexpr (!FIBER)
+        reinterpret_cast<uint4*>(s_out)[i] =
+            spt::ld_stream(reinterpret_cast<const uint4*>(p.out_idx + t0) + i);
       reinterpret_cast<uint4*>(s_val)[i] =
           spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0) + i);
 #pragma unroll
@@ -138,7 +181,7 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
     }
   } else {
     for (int i = tid; i < cnt; i += kThreads) {
-      s_out[i] = p.out_idx[t0 + i];
+      if constexpr (!FIBER) s_out[i] = p.out_idx[t0 + i];
       s_val[i] = p.val[t0 + i];
 #pragma unroll
       for (int j = 0; j < NM1; ++j) s_oidx[j * kTile + i] = p.oidx[j][t0 + i];
@@ -146,6 +189,25 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
   }
   for (int i = tid; i < NSLOT; i += kThreads) s_slot_row[i] = kNone;
   __syncthreads();
+  if constexpr (FIBER) {
+    // Output row of each entry = its fiber id (search once, then walk).
+    const int per = kTile / kThreads;
+    const int e0 = tid * per;
+    if (e0 < cnt) {
+      const uint64_t m0 = t0 + e0;
+      int lo = 0, hi = static_cast<int>(nstage) - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_fptr[mid] <= m0) lo = mid;
+        else hi = mid - 1;
+      }
+      for (int i = 0; i < per && e0 + i < cnt; ++i) {
+        while (lo + 1 < static_cast<int>(nstage) && s_fptr[lo + 1] <= m0 + i) ++lo;
+        s_out[e0 + i] = f_lo + lo;
+      }
+    }
+    __syncthreads();
+  }
 
   // ---- per-group segmented accumulation ----------------------------------
   const int warp = tid >> 5, lane = tid & 31;
@@ -219,6 +281,7 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
 #pragma unroll
             for (int k = 0; k < VEC; ++k) o[k] = (float)acc[k];
             Vec<VEC>::store(p.out + (size_t)run_row * p.R + col, o);
+            if constexpr (FIBER) ttm_emit_idx<VEC>(p, s_fptr[run_row - f_lo], run_row, col);
           }
           if (row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
         }
@@ -240,8 +303,16 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
   const uint32_t head_row = s_out[0];
   const uint32_t tail_row = s_out[cnt - 1];
   if (tid == 0) {
-    const uint32_t prev_row = tile > 0 ? p.out_idx[t0 - 1] : kNone;
-    const uint32_t next_row = (tile + 1 < p.ntiles) ? p.out_idx[t0 + cnt] : kNone;
+    uint32_t prev_row, next_row;
+    if constexpr (FIBER) {
+      // Rows are fiber ids: contiguous, every fiber non-empty.
+      prev_row = tile > 0 ? (s_fptr[0] < t0 ? f_lo : f_lo - 1) : kNone;
+      next_row = kNone;
+      if (tile + 1 < p.ntiles) next_row = s_fptr[tail_row - f_lo + 1] > t0 + cnt ? tail_row : tail_row + 1;
+    } else {
+      prev_row = tile > 0 ? p.out_idx[t0 - 1] : kNone;
+      next_row = (tile + 1 < p.ntiles) ? p.out_idx[t0 + cnt] : kNone;
+    }
     if (prev_row != kNone && prev_row > head_row) atomicMin(p.err + 2, (unsigned long long)t0);
     if (next_row != kNone && next_row < tail_row)
       atomicMin(p.err + 2, (unsigned long long)(t0 + cnt));
@@ -266,7 +337,10 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
         if (cur_row != kNone) {
           if (cur_row == head_row) head_acc = cur;
           else if (cur_row == tail_row) tail_acc = cur;
-          else if (cok) p.out[(size_t)cur_row * p.R + p.c0 + c] = (float)cur;
+          else if (cok) {
+            p.out[(size_t)cur_row * p.R + p.c0 + c] = (float)cur;
+            if constexpr (FIBER) ttm_emit_idx<1>(p, s_fptr[cur_row - f_lo], cur_row, p.c0 + c);
+          }
           if ((s >> 1) != cur_group && r > cur_row + 1 && cok)
             for (uint32_t z = cur_row + 1; z < r; ++z) p.out[(size_t)z * p.R + p.c0 + c] = 0.0f;
         }
@@ -344,8 +418,17 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
 
   // ---- rows completed by this tile ------------------------------------------
   if (c < CB && static_cast<uint32_t>(c) < p.ncols) {
-    if (boundary || !cont_next) p.out[(size_t)head_row * p.R + p.c0 + c] = (float)(carry + head_acc);
-    if (boundary && !cont_next) p.out[(size_t)tail_row * p.R + p.c0 + c] = (float)tail_acc;
+    if (boundary || !cont_next) {
+      p.out[(size_t)head_row * p.R + p.c0 + c] = (float)(carry + head_acc);
+      if constexpr (FIBER) {
+        // The head of the tile's first fiber may lie in an earlier tile.
+        ttm_emit_idx<1>(p, s_fptr[head_row - f_lo], head_row, p.c0 + c);
+      }
+    }
+    if (boundary && !cont_next) {
+      p.out[(size_t)tail_row * p.R + p.c0 + c] = (float)tail_acc;
+      if constexpr (FIBER) ttm_emit_idx<1>(p, s_fptr[tail_row - f_lo], tail_row, p.c0 + c);
+    }
   }
 }
 
@@ -389,18 +472,24 @@ size_t seg_smem(int nm1) {
   return (size_t)2 * GROUPS * CB * sizeof(double) + (size_t)kTile * (2 + nm1) * sizeof(uint32_t);
 }
 
+// TTM: same kernel with fiber rows and one "other" mode (the contracted one).
+template <int G, int VEC>
+size_t ttm_smem() {
+  return seg_smem<G, VEC>(1) + (size_t)(kTile + 2) * sizeof(uint32_t);
+}
+
 using KernelFn = void (*)(MttkrpParams);
 
 template <int G, int VEC>
 KernelFn pick_seg(int nm1) {
   switch (nm1) {
-    case 1: return mttkrp_seg_kernel<1, G, VEC>;
-    case 2: return mttkrp_seg_kernel<2, G, VEC>;
-    case 3: return mttkrp_seg_kernel<3, G, VEC>;
-    case 4: return mttkrp_seg_kernel<4, G, VEC>;
-    case 5: return mttkrp_seg_kernel<5, G, VEC>;
-    case 6: return mttkrp_seg_kernel<6, G, VEC>;
-    default: return mttkrp_seg_kernel<7, G, VEC>;
+    case 1: return mttkrp_seg_kernel<1, G, VEC, false>;
+    case 2: return mttkrp_seg_kernel<2, G, VEC, false>;
+    case 3: return mttkrp_seg_kernel<3, G, VEC, false>;
+    case 4: return mttkrp_seg_kernel<4, G, VEC, false>;
+    case 5: return mttkrp_seg_kernel<5, G, VEC, false>;
+    case 6: return mttkrp_seg_kernel<6, G, VEC, false>;
+    default: return mttkrp_seg_kernel<7, G, VEC, false>;
   }
 }
 
@@ -439,7 +528,113 @@ Variant choose_variant(uint32_t R, int nm1) {
   return {32, 1, pick_seg<32, 1>(nm1), pick_atomic<32, 1>(nm1), seg_smem<32, 1>(nm1)};
 }
 
+struct TtmVariant {
+  int G, VEC;
+  KernelFn fn;
+  size_t smem;
+};
+
+TtmVariant choose_ttm(uint32_t R, bool aligned) {
+  if (R % 4 == 0 && aligned) {
+    const uint32_t q = R / 4;
+    if (q <= 2) return {2, 4, mttkrp_seg_kernel<1, 2, 4, true>, ttm_smem<2, 4>()};
+    if (q <= 4) return {4, 4, mttkrp_seg_kernel<1, 4, 4, true>, ttm_smem<4, 4>()};
+    if (q <= 8) return {8, 4, mttkrp_seg_kernel<1, 8, 4, true>, ttm_smem<8, 4>()};
+    if (q <= 16) return {16, 4, mttkrp_seg_kernel<1, 16, 4, true>, ttm_smem<16, 4>()};
+    return {32, 4, mttkrp_seg_kernel<1, 32, 4, true>, ttm_smem<32, 4>()};
+  }
+  return {32, 1, mttkrp_seg_kernel<1, 32, 1, true>, ttm_smem<32, 1>()};
+}
+
 }  // namespace
+
+namespace spt {
+int build_tile_fiber_map(spt_ctx* ctx, const uint32_t* d_fptr, uint32_t nfibs, uint32_t tile,
+                         uint32_t* d_map, cudaStream_t st);
+int check_fiber_inputs(const spt_coo* x, uint32_t mode, const uint32_t* d_fptr, uint64_t nfibs,
+                       const char* k);
+}  // namespace spt
+
+// K7 TTM (P/src/kernels_seq.cpp:108-151, P/src/kernels_par.cpp:224-273,
+// ttm_fiber P/src/kernel_detail.hpp:132-140): the segmented kernel above with
+// output rows = fibers of x (sorted with `mode` last), the contracted mode's
+// index gathering rows of U, and an epilogue that writes the R output entries
+// of each fiber (value row + N index rows) with vector stores. Tensor cores are
+// deliberately not used: the op is gather/scatter-bound (1 mul-add per
+// 8 bytes gathered), and the output COO write dominates.
+extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uint64_t u_rows,
+                           uint64_t u_cols, uint32_t mode, const uint32_t* d_fptr, uint64_t nfibs,
+                           spt_coo* z, unsigned flags, void* stream) {
+  if (!ctx) return spt::set_error(SPT_EINVAL, "ttm: null context");
+  SPT_TRY(spt::check_fiber_inputs(x, mode, d_fptr, nfibs, "ttm"));
+  if (u_rows != x->dims[mode])
+    return spt::set_error(SPT_EINVAL, "ttm: matrix rows must match the mode dimension");
+  if (u_cols == 0) return spt::set_error(SPT_EINVAL, "ttm: matrix must have at least one column");
+  if (u_cols > 0xFFFFFFFFull || nfibs * u_cols >= (1ull << 32))
+    return spt::set_error(SPT_EOVERFLOW, "ttm: output nnz %llu exceeds the u32 device range",
+                          (unsigned long long)(nfibs * u_cols));
+  if (!z) return spt::set_error(SPT_EINVAL, "ttm: null output");
+  const uint32_t N = x->order;
+  const uint32_t R = static_cast<uint32_t>(u_cols);
+  z->order = N;
+  z->nnz = nfibs * R;
+  for (uint32_t d = 0; d < SPT_MAX_ORDER; ++d) {
+    z->dims[d] = d < N ? (d == mode ? R : x->dims[d]) : 0;
+    z->sort_order[d] = x->sort_order[d];
+  }
+  z->has_sort_order = 1;
+  z->coalesced = 1;
+  if (nfibs == 0) return SPT_OK;
+  for (uint32_t d = 0; d < N; ++d)
+    if (!z->idx[d]) return spt::set_error(SPT_EINVAL, "ttm: null output index array");
+  if (!z->val || !d_u) return spt::set_error(SPT_EINVAL, "ttm: null matrix or output values");
+  cudaStream_t st = spt::as_stream(stream);
+
+  bool aligned = spt::aligned16(d_u) && spt::aligned16(z->val);
+  for (uint32_t d = 0; d < N; ++d) aligned = aligned && spt::aligned16(z->idx[d]);
+  const TtmVariant v = choose_ttm(R, aligned);
+  const uint32_t CB = v.G * v.VEC;
+  const uint64_t ntiles = (x->nnz + kTile - 1) / kTile;
+  uint32_t* map;
+  SPT_TRY(spt::ctx_scratch(ctx, ntiles * sizeof(uint32_t), reinterpret_cast<void**>(&map)));
+  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), kTile, map, st));
+
+  MttkrpParams p{};
+  p.oidx[0] = x->idx[mode];
+  p.ofac[0] = d_u;
+  p.val = x->val;
+  p.out = z->val;
+  p.nnz = x->nnz;
+  p.rows = static_cast<uint32_t>(nfibs);
+  p.R = R;
+  p.err = ctx->d_err;
+  p.tile_ctr = ctx->d_tile_ctr;
+  p.ntiles = static_cast<uint32_t>(ntiles);
+  p.fptr = d_fptr;
+  p.tile_fiber = map;
+  for (uint32_t d = 0; d < N; ++d) {
+    p.hidx[d] = x->idx[d];
+    p.zidx[d] = z->idx[d];
+  }
+  p.N = N;
+  p.mode = mode;
+  SPT_CUDA(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(v.smem)));
+  for (uint32_t c0 = 0; c0 < R; c0 += CB) {
+    uint32_t epoch;
+    SPT_TRY(spt::ctx_lookback(ctx, ntiles, 2 * ntiles * CB, &epoch));
+    p.status = ctx->d_status;
+    p.payA = ctx->d_payload;
+    p.payP = ctx->d_payload + ntiles * CB;
+    p.epoch = epoch;
+    p.c0 = c0;
+    p.ncols = std::min<uint32_t>(CB, R - c0);
+    v.fn<<<static_cast<unsigned>(ntiles), kThreads, v.smem, st>>>(p);
+    SPT_LAUNCHED(ctx);
+  }
+  (void)flags;
+  return SPT_OK;
+}
 
 extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors,
                               const uint64_t* rows, const uint64_t* cols, uint32_t mode,

@@ -1,0 +1,328 @@
+// K6 TTV: one output entry per fiber, value = sum over the fiber of val*v[k].
+//
+// Reference: seq::ttv P/src/kernels_seq.cpp:69-101, par::ttv
+// P/src/kernels_par.cpp:179-216, ttv_fiber_value P/src/kernel_detail.hpp:121-128,
+// check_fiber_kernel_inputs P/src/kernel_detail.hpp:106-119, drop_mode :142-149.
+//
+// x is sorted with `mode` last, so a fiber is a contiguous entry range
+// [fptr[f], fptr[f+1]). The kernel is nnz-balanced, not fiber-balanced: a CTA
+// owns 2048 consecutive entries (256 threads x 8, blocked), forms each term
+// val*v[k] in fp32 (bit-identical to the reference's term), and reduces the
+// terms by fiber with a block-wide segmented scan in fp64 (cub::BlockScan over
+// (head-flag, sum) pairs). Fibers that cross a tile boundary are completed by
+// the tile holding their last entry, using the same epoch-tagged decoupled
+// look-back as MTTKRP (scalar fp64 payloads). The fiber index enters as the
+// u32 offsets plus a per-tile "first fiber" map built by a streaming pass
+// over fptr, so no tile ever binary-searches global memory. Output index
+// tuples are written by the tile holding the fiber head (gathered from the
+// head entry, P/src/kernels_seq.cpp:89-94).
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kEPT = 8;
+constexpr int kTile = kThreads * kEPT;
+constexpr uint32_t kFlagA = 1, kFlagP = 2;
+
+struct SegPair {
+  int head;
+  double v;
+};
+struct SegOp {
+  __device__ __forceinline__ SegPair operator()(const SegPair& a, const SegPair& b) const {
+    return {a.head | b.head, b.head ? b.v : a.v + b.v};
+  }
+};
+
+struct TtvParams {
+  const uint32_t* kidx;  // x.indices[mode]
+  const float* val;
+  const float* v;
+  const uint32_t* fptr;
+  const uint32_t* tile_fiber;
+  const uint32_t* hidx[SPT_MAX_ORDER - 1];  // x.indices[d], d != mode ascending
+  uint32_t* zidx[SPT_MAX_ORDER - 1];
+  float* zval;
+  uint64_t nnz;
+  uint32_t nfibs;
+  uint32_t ntiles;
+  uint32_t epoch;
+  uint32_t* status;
+  double* payA;
+  double* payP;
+  unsigned long long* tile_ctr;
+};
+
+template <int NO>
+__global__ void __launch_bounds__(kThreads) ttv_kernel(TtvParams p) {
+  using Scan = cub::BlockScan<SegPair, kThreads>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t s_fptr[kTile + 2];
+  __shared__ uint32_t s_tile;
+  __shared__ int s_meta[3];
+  __shared__ double s_carry;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    const unsigned long long t = atomicAdd(p.tile_ctr, 1ull);
+    if (t == p.ntiles - 1) atomicExch(p.tile_ctr, 0ull);
+    s_tile = static_cast<uint32_t>(t);
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t t0 = (uint64_t)tile * kTile;
+  const int cnt = (p.nnz - t0 < (uint64_t)kTile) ? static_cast<int>(p.nnz - t0) : kTile;
+  const uint32_t f_lo = p.tile_fiber[tile];
+  const uint32_t f_end = (tile + 1 < p.ntiles) ? p.tile_fiber[tile + 1] + 1 : p.nfibs;
+  const uint32_t nstage = f_end - f_lo + 1;  // fptr[f_lo .. f_end]
+  for (uint32_t i = tid; i < nstage; i += kThreads) s_fptr[i] = p.fptr[f_lo + i];
+
+  // Terms (fp32, as the reference forms them), blocked: entries tid*8 .. +7.
+  const int e0 = tid * kEPT;
+  float val[kEPT];
+  uint32_t kk[kEPT];
+  if (cnt == kTile) {
+    const uint4 k0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0));
+    const uint4 k1 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0) + 1);
+    const uint4 v0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0 + e0));
+    const uint4 v1 = spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0 + e0) + 1);
+    kk[0] = k0.x, kk[1] = k0.y, kk[2] = k0.z, kk[3] = k0.w;
+    kk[4] = k1.x, kk[5] = k1.y, kk[6] = k1.z, kk[7] = k1.w;
+    val[0] = __uint_as_float(v0.x), val[1] = __uint_as_float(v0.y);
+    val[2] = __uint_as_float(v0.z), val[3] = __uint_as_float(v0.w);
+    val[4] = __uint_as_float(v1.x), val[5] = __uint_as_float(v1.y);
+    val[6] = __uint_as_float(v1.z), val[7] = __uint_as_float(v1.w);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kEPT; ++i) {
+      const bool ok = e0 + i < cnt;
+      kk[i] = ok ? p.kidx[t0 + e0 + i] : 0;
+      val[i] = ok ? p.val[t0 + e0 + i] : 0.0f;
+    }
+  }
+  float term[kEPT];
+#pragma unroll
+  for (int i = 0; i < kEPT; ++i) term[i] = (e0 + i < cnt) ? __fmul_rn(val[i], __ldg(p.v + kk[i])) : 0.0f;
+  __syncthreads();
+
+  // Local fiber of each item: binary search once, then walk.
+  int lf[kEPT];
+  bool head[kEPT];
+  {
+    const uint64_t m0 = t0 + e0;
+    int lo = 0, hi = static_cast<int>(nstage) - 1;  // largest j with s_fptr[j] <= m0
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_fptr[mid] <= m0) lo = mid;
+      else hi = mid - 1;
+    }
+    int j = lo;
+#pragma unroll
+    for (int i = 0; i < kEPT; ++i) {
+      const uint64_t m = m0 + i;
+      while (j + 1 < static_cast<int>(nstage) && s_fptr[j + 1] <= m) ++j;
+      lf[i] = j;
+      head[i] = (e0 + i < cnt) && s_fptr[j] == m;
+    }
+  }
+  SegPair agg{0, 0.0};
+#pragma unroll
+  for (int i = 0; i < kEPT; ++i) {
+    if (e0 + i >= cnt) break;
+    if (head[i]) agg = {1, (double)term[i]};
+    else agg.v += (double)term[i];
+  }
+  SegPair excl, block_agg;
+  Scan(scan_tmp).ExclusiveScan(agg, excl, SegOp(), block_agg);
+  if (tid == 0) excl = {0, 0.0};
+
+  if (tid == 0) {
+    const bool cont_prev = s_fptr[0] < t0;
+    // fiber of the last entry
+    const uint64_t ml = t0 + cnt - 1;
+    int lo = 0, hi = static_cast<int>(nstage) - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_fptr[mid] <= ml) lo = mid;
+      else hi = mid - 1;
+    }
+    s_meta[0] = cont_prev;
+    s_meta[1] = s_fptr[lo + 1] > ml + 1;  // last fiber continues into the next tile
+    s_meta[2] = lo;                        // local id of the last fiber
+  }
+  __syncthreads();
+  const bool cont_prev = s_meta[0], cont_next = s_meta[1];
+  const bool single = s_meta[2] == 0;
+  const uint32_t tag = p.epoch << 3;
+
+  // Publish the tail partial for successors (only when one needs it).
+  if (cont_next && tid == 0) {
+    if (!single || !cont_prev) {
+      p.payP[tile] = block_agg.v;
+      __threadfence();
+      spt::st_release(p.status + tile, tag | kFlagP);
+    } else {
+      p.payA[tile] = block_agg.v;
+      __threadfence();
+      spt::st_release(p.status + tile, tag | kFlagA);
+    }
+  }
+  // Look-back for the first fiber's carry-in (thread 0 walks, scalar payload).
+  if (tid == 0) {
+    double carry = 0.0;
+    if (cont_prev) {
+      uint32_t j = tile - 1;
+      while (true) {
+        uint32_t s;
+        do {
+          s = spt::ld_acquire(p.status + j);
+        } while ((s >> 3) != p.epoch || (s & 3u) == 0);
+        carry += spt::ld_cg(((s & kFlagP) ? p.payP : p.payA) + j);
+        if ((s & kFlagP) || j == 0) break;
+        --j;
+      }
+      if (cont_next && single) {
+        p.payP[tile] = carry + block_agg.v;
+        __threadfence();
+        spt::st_release(p.status + tile, tag | kFlagP);
+      }
+    }
+    s_carry = carry;
+  }
+  __syncthreads();
+  const double carry = s_carry;
+
+  // Emit fibers that end in this tile; heads write the index tuple.
+  double run = excl.v;
+#pragma unroll
+  for (int i = 0; i < kEPT; ++i) {
+    const int e = e0 + i;
+    if (e >= cnt) break;
+    const uint64_t m = t0 + e;
+    run = head[i] ? (double)term[i] : run + (double)term[i];
+    const uint32_t f = f_lo + lf[i];
+    if (head[i]) {
+#pragma unroll
+      for (int d = 0; d < NO; ++d) p.zidx[d][f] = p.hidx[d][m];
+    }
+    const bool fiber_end_here = s_fptr[lf[i] + 1] == m + 1;
+    if (fiber_end_here) p.zval[f] = (float)(run + (lf[i] == 0 ? carry : 0.0));
+  }
+}
+
+// map[t] = fiber containing entry t*tile (fptr is non-decreasing, every fiber
+// non-empty); one thread per fiber, streaming over fptr.
+__global__ void tile_fiber_kernel(const uint32_t* fptr, uint32_t nfibs, uint32_t tile,
+                                  uint32_t* map) {
+  uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (; f < nfibs; f += stride) {
+    const uint32_t a = (fptr[f] + tile - 1) / tile, b = (fptr[f + 1] + tile - 1) / tile;
+    for (uint32_t t = a; t < b; ++t) map[t] = f;
+  }
+}
+
+}  // namespace
+
+namespace spt {
+
+int build_tile_fiber_map(spt_ctx* ctx, const uint32_t* d_fptr, uint32_t nfibs, uint32_t tile,
+                         uint32_t* d_map, cudaStream_t st) {
+  tile_fiber_kernel<<<grid_for(nfibs, 256, ctx->num_sms * 16), 256, 0, st>>>(d_fptr, nfibs, tile,
+                                                                            d_map);
+  SPT_LAUNCHED(ctx);
+  return SPT_OK;
+}
+
+int check_fiber_inputs(const spt_coo* x, uint32_t mode, const uint32_t* d_fptr, uint64_t nfibs,
+                       const char* k) {
+  SPT_TRY(check_coo(x, k));
+  // P/src/kernel_detail.hpp:110-118
+  if (x->order < 2) return set_error(SPT_EINVAL, "%s: input must have order >= 2", k);
+  if (mode >= x->order) return set_error(SPT_EINVAL, "%s: mode out of range", k);
+  if (!x->coalesced) return set_error(SPT_EINVAL, "%s: tensor must be coalesced", k);
+  if (!x->has_sort_order || static_cast<uint32_t>(x->sort_order[x->order - 1]) != mode)
+    return set_error(SPT_EINVAL, "%s: tensor must be sorted with the target mode last", k);
+  if (!d_fptr || nfibs > x->nnz || (x->nnz > 0 && nfibs == 0))
+    return set_error(SPT_EINVAL, "%s: fiber index does not match the tensor", k);
+  return SPT_OK;
+}
+
+}  // namespace spt
+
+extern "C" int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uint64_t v_len,
+                           uint32_t mode, const uint32_t* d_fptr, uint64_t nfibs, spt_coo* z,
+                           unsigned flags, void* stream) {
+  if (!ctx) return spt::set_error(SPT_EINVAL, "ttv: null context");
+  SPT_TRY(spt::check_fiber_inputs(x, mode, d_fptr, nfibs, "ttv"));
+  if (v_len != x->dims[mode])
+    return spt::set_error(SPT_EINVAL, "ttv: vector length must match the mode dimension");
+  if (!z) return spt::set_error(SPT_EINVAL, "ttv: null output");
+  const uint32_t N = x->order;
+  // Output metadata: dims without `mode`, sort order drop_mode(...), coalesced.
+  z->order = N - 1;
+  z->nnz = nfibs;
+  uint32_t dz = 0;
+  for (uint32_t d = 0; d < N; ++d)
+    if (d != mode) z->dims[dz++] = x->dims[d];
+  for (uint32_t d = dz; d < SPT_MAX_ORDER; ++d) z->dims[d] = 0;
+  uint32_t k = 0;
+  for (uint32_t j = 0; j < N; ++j) {
+    const uint32_t d = x->sort_order[j];
+    if (d != mode) z->sort_order[k++] = d < mode ? d : d - 1;
+  }
+  z->has_sort_order = 1;
+  z->coalesced = 1;
+  if (nfibs == 0) return SPT_OK;
+  for (uint32_t d = 0; d < N - 1; ++d)
+    if (!z->idx[d]) return spt::set_error(SPT_EINVAL, "ttv: null output index array");
+  if (!z->val || !d_v) return spt::set_error(SPT_EINVAL, "ttv: null vector or output values");
+
+  cudaStream_t st = spt::as_stream(stream);
+  const uint64_t ntiles = (x->nnz + kTile - 1) / kTile;
+  uint32_t* map;
+  SPT_TRY(spt::ctx_scratch(ctx, ntiles * sizeof(uint32_t), reinterpret_cast<void**>(&map)));
+  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), kTile, map, st));
+  uint32_t epoch;
+  SPT_TRY(spt::ctx_lookback(ctx, ntiles, 2 * ntiles, &epoch));
+  TtvParams p{};
+  p.kidx = x->idx[mode];
+  p.val = x->val;
+  p.v = d_v;
+  p.fptr = d_fptr;
+  p.tile_fiber = map;
+  uint32_t j = 0;
+  for (uint32_t d = 0; d < N; ++d) {
+    if (d == mode) continue;
+    p.hidx[j] = x->idx[d];
+    p.zidx[j] = z->idx[j];
+    ++j;
+  }
+  p.zval = z->val;
+  p.nnz = x->nnz;
+  p.nfibs = static_cast<uint32_t>(nfibs);
+  p.ntiles = static_cast<uint32_t>(ntiles);
+  p.epoch = epoch;
+  p.status = ctx->d_status;
+  p.payA = ctx->d_payload;
+  p.payP = ctx->d_payload + ntiles;
+  p.tile_ctr = ctx->d_tile_ctr;
+  const bool aligned = spt::aligned16(x->idx[mode]) && spt::aligned16(x->val);
+  if (!aligned) return spt::set_error(SPT_EINVAL, "ttv: index/value arrays must be 16-byte aligned");
+  const unsigned grid = static_cast<unsigned>(ntiles);
+  switch (N - 1) {
+    case 1: ttv_kernel<1><<<grid, kThreads, 0, st>>>(p); break;
+    case 2: ttv_kernel<2><<<grid, kThreads, 0, st>>>(p); break;
+    case 3: ttv_kernel<3><<<grid, kThreads, 0, st>>>(p); break;
+    case 4: ttv_kernel<4><<<grid, kThreads, 0, st>>>(p); break;
+    case 5: ttv_kernel<5><<<grid, kThreads, 0, st>>>(p); break;
+    case 6: ttv_kernel<6><<<grid, kThreads, 0, st>>>(p); break;
+    default: ttv_kernel<7><<<grid, kThreads, 0, st>>>(p); break;
+  }
+  SPT_LAUNCHED(ctx);
+  (void)flags;
+  return SPT_OK;
+}
