@@ -288,7 +288,7 @@ extern "C" int spt_tew_f32(spt_ctx* ctx, const spt_coo* x, const spt_coo* y, int
   if (total == 0) {
     SPT_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
   } else {
-    for (uint32_t d = 0; d < N; ++d)
+    for (uint32_t d = 0; d < N && need; ++d)
       if (!z->idx[d]) return spt::set_error(SPT_EINVAL, "tew: null output index array");
     if (!z->val && need) return spt::set_error(SPT_EINVAL, "tew: null output values");
     MergeParams p{};

@@ -161,6 +161,21 @@ def build_fiber_index(t: DeviceCOO, mode: int) -> FiberIndex:
 # TEW (P/src/kernels_seq.cpp:41-53, P/src/kernel_detail.hpp:36-102)
 
 
+def tew_device(x: DeviceCOO, y: DeviceCOO, op: int, out: DeviceCOO,
+               d_count: torch.Tensor) -> DeviceCOO:
+    """Stream-ordered TEW for the device-resident path: x and y must already
+    share a sort order; `out` has capacity nnz_x+nnz_y (mul: min); the output
+    count lands in d_count (int64 CUDA scalar) without a host sync."""
+    ctx = _ctx(x)
+    cap = out.nnz
+    xd, yd, zd = x.descriptor(), y.descriptor(), out.descriptor()
+    check(_lib.load().spt_tew_f32(ctx.handle, ctypes.byref(xd), ctypes.byref(yd), int(op),
+                                  ctypes.byref(zd), cap, None, d_count.data_ptr(),
+                                  _lib.SPT_FLAG_ASYNC, _stream(x.device)))
+    out.adopt(zd)
+    return out
+
+
 def tew(x: DeviceCOO, y: DeviceCOO, op: int, out: Optional[DeviceCOO] = None) -> DeviceCOO:
     """General elementwise op by sorted merge. Like the reference, sorts both
     operands ascending *in place* unless they already share a sort order."""
