@@ -12,7 +12,11 @@ import os
 import threading
 
 MAX_ORDER = 8
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspten_b200.so")
+# SPT_LIB_PATH selects an alternative build of the same library (tuning
+# experiments); it is never a different implementation.
+LIB_PATH = os.environ.get(
+    "SPT_LIB_PATH",
+    os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspten_b200.so"))
 
 # spt_status -> reference exception types (P/src/kernel_detail.hpp:38-44,
 # P/src/kernels_seq.cpp:32-34). Named after the C++ exceptions.

@@ -41,6 +41,8 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTile = 2048;
+constexpr int kTileP = kTile + kTile / 8;  // padded per-entry smem arrays
+__device__ __forceinline__ int sw(int e) { return e + ((e >> 5) << 2); }
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kFlagA = 1, kFlagP = 2, kFlagBoundary = 4;
 
@@ -129,20 +131,32 @@ __device__ __forceinline__ void zero_rows(float* out, uint32_t r0, uint32_t r1, 
   for (uint32_t r = r0; r < r1; ++r) Vec<VEC>::store(out + (size_t)r * R + col, z);
 }
 
+#ifndef SPT_MTTKRP_UNROLL
+#define SPT_MTTKRP_UNROLL 4
+#endif
+#ifndef SPT_MTTKRP_MINB
+#define SPT_MTTKRP_MINB 3  // <= 85 registers: 3 CTAs (24 warps) per SM
+#endif
+
 template <int NM1, int G, int VEC, bool FIBER>
-__global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
+__global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(MttkrpParams p) {
   constexpr int P = 32 / G;            // groups per warp
   constexpr int GROUPS = kWarps * P;   // groups per CTA
   constexpr int EG = kTile / GROUPS;   // entries per group
   constexpr int CB = G * VEC;          // columns per launch
-  constexpr int NSLOT = 2 * GROUPS;
+  constexpr int NSLOT = 2 * kWarps;  // warp head/tail partials
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_slot = reinterpret_cast<double*>(smem_raw);                 // [NSLOT][CB]
-  uint32_t* s_out = reinterpret_cast<uint32_t*>(s_slot + NSLOT * CB);  // [kTile]
-  float* s_val = reinterpret_cast<float*>(s_out + kTile);              // [kTile]
-  uint32_t* s_oidx = reinterpret_cast<uint32_t*>(s_val + kTile);       // [NM1][kTile]
-  uint32_t* s_fptr = s_oidx + NM1 * kTile;                             // FIBER: [kTile+2]
+  // Per-entry arrays use the padded layout sw(e) (16 B of padding every 32
+  // entries) so the P groups of a warp, which read entries EG apart, hit
+  // distinct banks; 16-byte chunks stay aligned for the vector staging.
+  uint32_t* s_out = reinterpret_cast<uint32_t*>(s_slot + NSLOT * CB);  // [kTileP]
+  float* s_val = reinterpret_cast<float*>(s_out + kTileP);             // [kTileP]
+  uint32_t* s_oidx = reinterpret_cast<uint32_t*>(s_val + kTileP);      // [NM1][kTileP]
+  uint32_t* s_fptr = s_oidx + NM1 * kTileP;                            // FIBER: [kTile+2]
+  double* s_gslot = reinterpret_cast<double*>(s_fptr + (FIBER ? kTile + 4 : 0));  // [GROUPS*2][CB]
+  __shared__ uint32_t s_grow[2 * GROUPS];
   __shared__ uint32_t s_slot_row[NSLOT];
   __shared__ uint32_t s_tile, s_flag;
   __shared__ uint32_t s_meta[4];
@@ -170,21 +184,21 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
     const int nv = kTile / 4;
     for (int i = tid; i < nv; i += kThreads) {
       if constexpr (!FIBER)
-        reinterpret_cast<uint4*>(s_out)[i] =
+        reinterpret_cast<uint4*>(s_out)[i + (i >> 3)] =
             spt::ld_stream(reinterpret_cast<const uint4*>(p.out_idx + t0) + i);
-      reinterpret_cast<uint4*>(s_val)[i] =
+      reinterpret_cast<uint4*>(s_val)[i + (i >> 3)] =
           spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0) + i);
 #pragma unroll
       for (int j = 0; j < NM1; ++j)
-        reinterpret_cast<uint4*>(s_oidx + j * kTile)[i] =
+        reinterpret_cast<uint4*>(s_oidx + j * kTileP)[i + (i >> 3)] =
             spt::ld_stream(reinterpret_cast<const uint4*>(p.oidx[j] + t0) + i);
     }
   } else {
     for (int i = tid; i < cnt; i += kThreads) {
-      if constexpr (!FIBER) s_out[i] = p.out_idx[t0 + i];
-      s_val[i] = p.val[t0 + i];
+      if constexpr (!FIBER) s_out[sw(i)] = p.out_idx[t0 + i];
+      s_val[sw(i)] = p.val[t0 + i];
 #pragma unroll
-      for (int j = 0; j < NM1; ++j) s_oidx[j * kTile + i] = p.oidx[j][t0 + i];
+      for (int j = 0; j < NM1; ++j) s_oidx[j * kTileP + sw(i)] = p.oidx[j][t0 + i];
     }
   }
   for (int i = tid; i < NSLOT; i += kThreads) s_slot_row[i] = kNone;
@@ -203,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
       }
       for (int i = 0; i < per && e0 + i < cnt; ++i) {
         while (lo + 1 < static_cast<int>(nstage) && s_fptr[lo + 1] <= m0 + i) ++lo;
-        s_out[e0 + i] = f_lo + lo;
+        s_out[sw(e0 + i)] = f_lo + lo;
       }
     }
     __syncthreads();
@@ -221,11 +235,26 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
 
   uint32_t run_row = kNone;
   bool first_run = true;
+  // Group results go to this warp's slots: [2*gw] = first run, [2*gw+1] = last
+  // run (if distinct). acc: fp64 total of the open run; a32: fp32 partial of
+  // the open run within the current batch (<= kUnroll terms), spilled into acc
+  // once per batch.
+  const int gw = lane / G;  // group within the warp
+  double* my_gslot = s_gslot + (size_t)warp * (2 * P) * CB;
+  uint32_t* my_grow = s_grow + warp * (2 * P);
+  if (gl == 0) {
+    my_grow[2 * gw] = kNone;
+    my_grow[2 * gw + 1] = kNone;
+  }
   double acc[VEC];
+  float a32[VEC];
 #pragma unroll
-  for (int k = 0; k < VEC; ++k) acc[k] = 0.0;
+  for (int k = 0; k < VEC; ++k) {
+    acc[k] = 0.0;
+    a32[k] = 0.0f;
+  }
 
-  constexpr int kUnroll = (NM1 * VEC <= 12) ? 4 : 2;
+  constexpr int kUnroll = (NM1 * VEC <= 12) ? SPT_MTTKRP_UNROLL : 2;
   for (int e = e_begin; e < e_end; e += kUnroll) {
     float prod[kUnroll][VEC];
     uint32_t rr[kUnroll];
@@ -237,7 +266,7 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
       if (eu < e_end && col_ok) {
 #pragma unroll
         for (int j = 0; j < NM1; ++j)
-          Vec<VEC>::load(p.ofac[j] + (size_t)s_oidx[j * kTile + eu] * p.R + col, f[u][j]);
+          Vec<VEC>::load(p.ofac[j] + (size_t)s_oidx[j * kTileP + sw(eu)] * p.R + col, f[u][j]);
       } else {
 #pragma unroll
         for (int j = 0; j < NM1; ++j)
@@ -248,8 +277,8 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int eu = e + u;
-      rr[u] = eu < e_end ? s_out[eu] : kNone;
-      const float v = eu < e_end ? s_val[eu] : 0.0f;
+      rr[u] = eu < e_end ? s_out[sw(eu)] : kNone;
+      const float v = eu < e_end ? s_val[sw(eu)] : 0.0f;
 #pragma unroll
       for (int k = 0; k < VEC; ++k) {
         float t = v;  // row[r] = val; row[r] *= f_d[r] for d ascending
@@ -264,17 +293,18 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
       const uint32_t row = rr[u];
       if (row == run_row) {
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) acc[k] += (double)prod[u][k];
+        for (int k = 0; k < VEC; ++k) a32[k] += prod[u][k];
       } else {
         if (run_row != kNone) {
           if (row < run_row) {
             if (gl == 0) atomicMin(p.err + 2, (unsigned long long)(t0 + e + u));
           }
-          if (first_run) {
-            const int slot = 2 * group;
-            if (gl == 0) s_slot_row[slot] = run_row;
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) s_slot[slot * CB + lcol + k] = acc[k];
+          for (int k = 0; k < VEC; ++k) acc[k] += (double)a32[k];
+          if (first_run) {
+            if (gl == 0) my_grow[2 * gw] = run_row;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) my_gslot[(2 * gw) * CB + lcol + k] = acc[k];
             first_run = false;
           } else if (col_ok) {
             float o[VEC];
@@ -287,21 +317,98 @@ __global__ void __launch_bounds__(kThreads) mttkrp_seg_kernel(MttkrpParams p) {
         }
         run_row = row;
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) acc[k] = (double)prod[u][k];
+        for (int k = 0; k < VEC; ++k) {
+          acc[k] = 0.0;
+          a32[k] = prod[u][k];
+        }
       }
+    }
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      acc[k] += (double)a32[k];
+      a32[k] = 0.0f;
     }
   }
   if (run_row != kNone) {
-    const int slot = 2 * group + (first_run ? 0 : 1);
-    if (gl == 0) s_slot_row[slot] = run_row;
+    const int sl = 2 * gw + (first_run ? 0 : 1);
+    if (gl == 0) my_grow[sl] = run_row;
 #pragma unroll
-    for (int k = 0; k < VEC; ++k) s_slot[slot * CB + lcol + k] = acc[k];
+    for (int k = 0; k < VEC; ++k) my_gslot[sl * CB + lcol + k] = acc[k];
+  }
+  __syncwarp();
+
+  // ---- warp fold of the P groups' boundary runs (every lane group walks the
+  // warp's 2P slots, in parallel across warps): rows complete inside the warp
+  // are written here, the warp's first and last row go to two CTA slots.
+  {
+    uint32_t w_cur = kNone, h_row = kNone;
+    int cur_g = -1;
+    double w_acc[VEC], h_acc[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) w_acc[k] = h_acc[k] = 0.0;
+    const bool writer = gw == 0 && col_ok;
+#pragma unroll 1
+    for (int g = 0; g < P; ++g) {
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int sl = 2 * g + it;
+        const uint32_t row = my_grow[sl];
+        if (row == kNone) continue;
+        double v[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) v[k] = my_gslot[sl * CB + lcol + k];
+        if (row == w_cur) {
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) w_acc[k] += v[k];
+        } else {
+          if (w_cur != kNone) {
+            if (h_row == kNone) {
+              h_row = w_cur;
+#pragma unroll
+              for (int k = 0; k < VEC; ++k) h_acc[k] = w_acc[k];
+            } else if (writer) {
+              float o[VEC];
+#pragma unroll
+              for (int k = 0; k < VEC; ++k) o[k] = (float)w_acc[k];
+              Vec<VEC>::store(p.out + (size_t)w_cur * p.R + col, o);
+              if constexpr (FIBER) ttm_emit_idx<VEC>(p, s_fptr[w_cur - f_lo], w_cur, col);
+            }
+            if (g != cur_g && row > w_cur + 1 && writer)
+              zero_rows<VEC>(p.out, w_cur + 1, row, p.R, col, true);
+          }
+          w_cur = row;
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) w_acc[k] = v[k];
+        }
+        cur_g = g;
+      }
+    }
+    // slots: [2w] = warp head row, [2w+1] = warp tail row (if distinct)
+    uint32_t t_row = kNone;
+    if (h_row == kNone) {
+      h_row = w_cur;
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) h_acc[k] = w_acc[k];
+    } else {
+      t_row = w_cur;
+    }
+    if (gw == 0) {
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        s_slot[(2 * warp) * CB + lcol + k] = h_acc[k];
+        s_slot[(2 * warp + 1) * CB + lcol + k] = w_acc[k];
+      }
+      if (lane == 0) {
+        s_slot_row[2 * warp] = h_row;
+        s_slot_row[2 * warp + 1] = t_row;
+      }
+    }
   }
   __syncthreads();
 
   // ---- CTA fold of the group boundary slots -------------------------------
   const uint32_t head_row = s_out[0];
-  const uint32_t tail_row = s_out[cnt - 1];
+  const uint32_t tail_row = s_out[sw(cnt - 1)];
   if (tid == 0) {
     uint32_t prev_row, next_row;
     if constexpr (FIBER) {
@@ -469,13 +576,14 @@ template <int G, int VEC>
 size_t seg_smem(int nm1) {
   constexpr int GROUPS = kWarps * (32 / G);
   constexpr int CB = G * VEC;
-  return (size_t)2 * GROUPS * CB * sizeof(double) + (size_t)kTile * (2 + nm1) * sizeof(uint32_t);
+  return (size_t)2 * kWarps * CB * sizeof(double) + (size_t)kTileP * (2 + nm1) * sizeof(uint32_t) +
+         (size_t)2 * GROUPS * CB * sizeof(double);
 }
 
 // TTM: same kernel with fiber rows and one "other" mode (the contracted one).
 template <int G, int VEC>
 size_t ttm_smem() {
-  return seg_smem<G, VEC>(1) + (size_t)(kTile + 2) * sizeof(uint32_t);
+  return seg_smem<G, VEC>(1) + (size_t)(kTile + 4) * sizeof(uint32_t);
 }
 
 using KernelFn = void (*)(MttkrpParams);
