@@ -120,6 +120,17 @@ struct Vec<1> {
   static __device__ __forceinline__ void store(float* p, const float (&f)[1]) { *p = f[0]; }
 };
 
+template <int U>
+__device__ __forceinline__ void ld_batch(const uint32_t* p, uint32_t (&o)[U]) {
+  if constexpr (U == 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+  } else {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    o[0] = v.x, o[1] = v.y;
+  }
+}
+
 // Zero rows [r0, r1) for this lane's columns.
 template <int VEC>
 __device__ __forceinline__ void zero_rows(float* out, uint32_t r0, uint32_t r1, uint32_t R,
@@ -254,10 +265,19 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
     a32[k] = 0.0f;
   }
 
-  constexpr int kUnroll = (NM1 * VEC <= 12) ? SPT_MTTKRP_UNROLL : 2;
+  constexpr int kUnroll = (NM1 * VEC <= 12) ? 4 : 2;
   for (int e = e_begin; e < e_end; e += kUnroll) {
     float prod[kUnroll][VEC];
-    uint32_t rr[kUnroll];
+    uint32_t rr[kUnroll], ix[NM1][kUnroll];
+    float vv[kUnroll];
+    // One vector LDS per array for the whole batch (batches are 16-byte
+    // aligned in the padded layout and never straddle a pad).
+    ld_batch<kUnroll>(s_out + sw(e), rr);
+    ld_batch<kUnroll>(reinterpret_cast<const uint32_t*>(s_val) + sw(e),
+                      reinterpret_cast<uint32_t(&)[kUnroll]>(vv));
+#pragma unroll
+    for (int j = 0; j < NM1; ++j) ld_batch<kUnroll>(s_oidx + j * kTileP + sw(e), ix[j]);
+    const bool full = e + kUnroll <= e_end;
     // Issue every gather of the batch before consuming any.
     float f[kUnroll][NM1][VEC];
 #pragma unroll
@@ -266,26 +286,38 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
       if (eu < e_end && col_ok) {
 #pragma unroll
         for (int j = 0; j < NM1; ++j)
-          Vec<VEC>::load(p.ofac[j] + (size_t)s_oidx[j * kTileP + sw(eu)] * p.R + col, f[u][j]);
+          Vec<VEC>::load(p.ofac[j] + (size_t)ix[j][u] * p.R + col, f[u][j]);
       } else {
 #pragma unroll
         for (int j = 0; j < NM1; ++j)
 #pragma unroll
           for (int k = 0; k < VEC; ++k) f[u][j][k] = 0.0f;
       }
+      if (eu >= e_end) rr[u] = kNone;
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int eu = e + u;
-      rr[u] = eu < e_end ? s_out[sw(eu)] : kNone;
-      const float v = eu < e_end ? s_val[sw(eu)] : 0.0f;
 #pragma unroll
       for (int k = 0; k < VEC; ++k) {
-        float t = v;  // row[r] = val; row[r] *= f_d[r] for d ascending
+        float t = vv[u];  // row[r] = val; row[r] *= f_d[r] for d ascending
 #pragma unroll
         for (int j = 0; j < NM1; ++j) t = __fmul_rn(t, f[u][j][k]);
         prod[u][k] = t;
       }
+    }
+    // Fast path: the whole batch continues the open run (the common case).
+    bool same = full && rr[0] == run_row;
+#pragma unroll
+    for (int u = 1; u < kUnroll; ++u) same = same && rr[u] == run_row;
+    if (same) {
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        float s = prod[0][k];
+#pragma unroll
+        for (int u = 1; u < kUnroll; ++u) s += prod[u][k];
+        acc[k] += (double)s;
+      }
+      continue;
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
