@@ -132,6 +132,144 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
 __device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Relaxed polling loads (no L1 invalidation per poll, unlike ld.acquire).
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Warp-parallel decoupled look-back over epoch-tagged u32 status words
+// (word = epoch << 3 | flags, flags & 3 == 1: aggregate A, == 2: inclusive P).
+// Called by one full warp for tile `tile` > 0. Polls (never blocks on) the 32
+// nearest predecessors at a time and returns n such that the chain of tiles
+// [tile-n, tile-1] ends in a P at tile-n with only A's nearer: the caller sums
+// payload[tile-n .. tile-1]. Tiles further back than the first P are never
+// waited for, so predecessors that publish nothing (their row did not
+// continue) cannot stall it.
+__device__ __forceinline__ uint32_t lookback_chain(const uint32_t* status, uint32_t tile,
+                                                   uint32_t epoch) {
+  const unsigned lane = threadIdx.x & 31u;
+  uint32_t base = 0;  // predecessors already known to be A
+  while (true) {
+    const int64_t j = (int64_t)tile - 1 - base - lane;
+    uint32_t flag = 2;  // before tile 0: behave as a terminating P
+    if (j >= 0) {
+      const uint32_t s = ld_relaxed(status + j);
+      flag = ((s >> 3) == epoch) ? (s & 3u) : 0u;
+    }
+    const unsigned ready = __ballot_sync(0xffffffffu, flag != 0);
+    const unsigned isP = __ballot_sync(0xffffffffu, flag == 2);
+    // length of the ready prefix (lanes 0..k-1 all published)
+    const int prefix = (~ready) ? __ffs(~ready) - 1 : 32;
+    const unsigned pmask = isP & (prefix == 32 ? 0xffffffffu : ((1u << prefix) - 1));
+    if (pmask) {
+      __threadfence();  // acquire: payloads written before the flags are visible
+      return base + __ffs(pmask);  // includes the P tile
+    }
+    if (prefix == 32) base += 32;  // all A: slide the window
+    else __nanosleep(32);
+  }
+}
+
+// Same over 64-bit words (epoch << 34 | flag << 32 | u32 count): returns the
+// exclusive prefix count for `tile` (sum of A counts up to and including the
+// nearest P's inclusive count). One full warp; result valid in all lanes.
+__device__ __forceinline__ unsigned long long lookback_count64(const unsigned long long* status,
+                                                               uint32_t tile, uint32_t epoch) {
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned long long acc = 0;
+  uint32_t base = 0;
+  while (true) {
+    const int64_t j = (int64_t)tile - 1 - base - lane;
+    uint32_t flag = 2, cnt = 0;
+    if (j >= 0) {
+      // relaxed: the count lives in the flag word itself, no payload to order
+      const unsigned long long w = ld_relaxed64(status + j);
+      flag = ((w >> 34) == epoch) ? (uint32_t)((w >> 32) & 3u) : 0u;
+      cnt = (uint32_t)w;
+    }
+    const unsigned ready = __ballot_sync(0xffffffffu, flag != 0);
+    const unsigned isP = __ballot_sync(0xffffffffu, flag == 2);
+    const int prefix = (~ready) ? __ffs(~ready) - 1 : 32;
+    const unsigned pmask = isP & (prefix == 32 ? 0xffffffffu : ((1u << prefix) - 1));
+    const int upto = pmask ? __ffs(pmask) : (prefix == 32 ? 32 : 0);
+    unsigned long long v = (lane < (unsigned)upto) ? cnt : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    acc += v;
+    if (pmask) return acc;
+    if (prefix == 32) base += 32;
+    else __nanosleep(32);
+  }
+}
+
+// CTA-wide variant of lookback_count64: all NT threads poll NT predecessors
+// per round trip. When hundreds of tiles are in flight, the tiles between a
+// tile and the nearest inclusive prefix are mostly still in their own
+// look-back (A only), so a 32-wide window needed several sequential round
+// trips; NT-wide needs one. Must be called by every thread of the CTA.
+struct LookbackSmem {
+  uint32_t ready[32], isp[32];
+  unsigned long long sum;
+};
+template <int NT>
+__device__ __forceinline__ unsigned long long lookback_count64_block(
+    const unsigned long long* status, uint32_t tile, uint32_t epoch, LookbackSmem& sm) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned long long acc = 0;
+  uint32_t base = 0;
+  while (true) {
+    const int64_t j = (int64_t)tile - 1 - base - tid;
+    uint32_t flag = 2, cnt = 0;
+    if (j >= 0) {
+      const unsigned long long w = ld_relaxed64(status + j);
+      flag = ((w >> 34) == epoch) ? (uint32_t)((w >> 32) & 3u) : 0u;
+      cnt = (uint32_t)w;
+    }
+    const unsigned r = __ballot_sync(0xffffffffu, flag != 0);
+    const unsigned q = __ballot_sync(0xffffffffu, flag == 2);
+    if (lane == 0) {
+      sm.ready[warp] = r;
+      sm.isp[warp] = q;
+    }
+    if (tid == 0) sm.sum = 0;
+    __syncthreads();
+    int prefix = 0, upto = -1;  // upto: index past the nearest P inside the ready prefix
+    for (int w = 0; w < NW; ++w) {
+      const unsigned rw = sm.ready[w];
+      const int pw = (~rw) ? __ffs(~rw) - 1 : 32;
+      const unsigned pm = sm.isp[w] & (pw == 32 ? 0xffffffffu : ((1u << pw) - 1));
+      if (pm) {
+        upto = prefix + __ffs(pm);
+        break;
+      }
+      prefix += pw;
+      if (pw < 32) break;
+    }
+    const bool slide = upto < 0 && prefix == NT;
+    const int take = upto >= 0 ? upto : (slide ? NT : 0);
+    unsigned long long v = (tid < take) ? cnt : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && v) atomicAdd(&sm.sum, v);
+    __syncthreads();
+    acc += sm.sum;
+    __syncthreads();
+    if (upto >= 0) return acc;
+    if (slide) base += NT;
+    else __nanosleep(32);
+  }
+}
 
 // Philox4x32-10 counter-based RNG (Salmon et al., SC'11).
 struct Philox {

@@ -528,22 +528,19 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
     if (tid == 0) spt::st_release(p.status + tile, tag | kFlagA);
   }
   if (cont_prev) {
-    uint32_t j = tile - 1;
-    while (true) {
-      if (tid == 0) {
-        uint32_t s;
-        do {
-          s = spt::ld_acquire(p.status + j);
-        } while ((s >> 3) != p.epoch || (s & 3u) == 0);
-        s_flag = s;
+    // Warp 0 finds the chain [tile-n, tile-1] (A's ending in a P) 32 tiles per
+    // poll; then every column thread sums the chain's payloads.
+    if (warp == 0) {
+      const uint32_t n = spt::lookback_chain(p.status, tile, p.epoch);
+      if (lane == 0) s_flag = n;
+    }
+    __syncthreads();
+    const uint32_t n = s_flag;
+    if (c < CB) {
+      for (uint32_t q = 1; q <= n && q <= tile; ++q) {
+        const uint32_t j = tile - q;
+        carry += spt::ld_cg((q == n ? p.payP : p.payA) + (size_t)j * CB + c);
       }
-      __syncthreads();
-      const uint32_t s = s_flag;
-      const double* pay = (s & kFlagP) ? p.payP : p.payA;
-      if (c < CB) carry += spt::ld_cg(pay + (size_t)j * CB + c);
-      __syncthreads();
-      if ((s & kFlagP) || (s & kFlagBoundary) || j == 0) break;
-      --j;
     }
     if (cont_next && !boundary) {
       if (c < CB) {

@@ -28,6 +28,11 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kIPT = 8;
 constexpr int kTile = kThreads * kIPT;
+// Key arrays in shared memory get one pad word per 32 entries: the threads'
+// merge-path positions advance ~4 entries apart, which would otherwise fold
+// onto 8 banks.
+constexpr int kTP = kTile + kTile / 32;
+__device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
 constexpr unsigned long long kFlagA = 1, kFlagP = 2;
 
 struct MergeParams {
@@ -45,7 +50,20 @@ struct MergeParams {
   unsigned long long* status;
   unsigned long long* tile_ctr;
   unsigned long long* total;  // device: output count
+  // Packed-key path: position k of the sort order occupies bits
+  // [shift[k], shift[k] + width) of a u64 key (sort-order significance).
+  uint32_t shift[SPT_MAX_ORDER];
+  uint32_t mask[SPT_MAX_ORDER];
 };
+
+template <int N>
+__device__ __forceinline__ unsigned long long pack_g(const uint32_t* const* idx, const MergeParams& p,
+                                                     uint64_t m) {
+  unsigned long long k = 0;
+#pragma unroll
+  for (int q = 0; q < N; ++q) k |= (unsigned long long)idx[q][m] << p.shift[q];
+  return k;
+}
 
 template <int N>
 __device__ __forceinline__ int cmp_g(const MergeParams& p, uint64_t i, uint64_t j) {
@@ -57,29 +75,40 @@ __device__ __forceinline__ int cmp_g(const MergeParams& p, uint64_t i, uint64_t 
   return 0;
 }
 
-// Tile boundaries on the merge path (x-first on ties).
+// Tile boundaries on the merge path (x-first on ties): split[t] = number of x
+// items among the first t*kTile merged items = the first m in [lo, hi) where
+// x[m] <= y[diag-1-m] fails. One warp per diagonal runs a 33-ary search (32
+// probes per round trip, ~5 rounds for 10M) instead of a 24-step binary one.
 template <int N>
 __global__ void partition_kernel(MergeParams p, uint32_t* split) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > p.ntiles) return;
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31u;
+  if (t > p.ntiles) return;  // warp-uniform
   const uint64_t total = p.nx + p.ny;
   const uint64_t diag = std::min<uint64_t>((uint64_t)t * kTile, total);
   uint64_t lo = diag > p.ny ? diag - p.ny : 0;
   uint64_t hi = std::min<uint64_t>(diag, p.nx);
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    // take x[mid] before y[diag-1-mid] iff x[mid] <= y[diag-1-mid]
-    if (cmp_g<N>(p, mid, diag - 1 - mid) <= 0) lo = mid + 1;
-    else hi = mid;
+  while (hi - lo > 32) {
+    const uint64_t span = hi - lo;
+    const uint64_t m = lo + (span * (lane + 1)) / 33;
+    const bool pred = cmp_g<N>(p, m, diag - 1 - m) <= 0;
+    const int ntrue = __popc(__ballot_sync(0xffffffffu, pred));
+    const uint64_t m_last = __shfl_sync(0xffffffffu, m, ntrue > 0 ? ntrue - 1 : 0);
+    const uint64_t m_first_false = __shfl_sync(0xffffffffu, m, ntrue < 32 ? ntrue : 31);
+    if (ntrue > 0) lo = m_last + 1;
+    if (ntrue < 32) hi = m_first_false;
   }
-  split[t] = static_cast<uint32_t>(lo);
+  const uint64_t m = lo + lane;
+  const bool pred = m < hi && cmp_g<N>(p, m, diag - 1 - m) <= 0;
+  const int ntrue = __popc(__ballot_sync(0xffffffffu, pred));
+  if (lane == 0) split[t] = static_cast<uint32_t>(lo + ntrue);
 }
 
 template <int N>
 __device__ __forceinline__ int cmp_s(const uint32_t* sx, int i, const uint32_t* sy, int j) {
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    const uint32_t a = sx[k * kTile + i], b = sy[k * kTile + j];
+    const uint32_t a = sx[k * kTP + pad(i)], b = sy[k * kTP + pad(j)];
     if (a != b) return a < b ? -1 : 1;
   }
   return 0;
@@ -93,11 +122,15 @@ template <int N>
 __global__ void __launch_bounds__(kThreads) merge_kernel(MergeParams p) {
   using Scan = cub::BlockScan<uint32_t, kThreads>;
   extern __shared__ __align__(16) uint32_t smem[];
-  uint32_t* sx = smem;              // [N][kTile]
-  uint32_t* sy = smem + N * kTile;  // [N][kTile]
+  uint32_t* sx = smem;              // [N][kTP] keys (padded)
+  uint32_t* sy = smem + N * kTP;    // [N][kTP]
+  float* sxv = reinterpret_cast<float*>(sy + N * kTP);  // [kTP] values
+  float* syv = sxv + kTP;                               // [kTP]
+  uint32_t* s_obuf = reinterpret_cast<uint32_t*>(syv + kTP);  // [kTile] output staging
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_base;
+  __shared__ spt::LookbackSmem s_lb;
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -113,12 +146,16 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(MergeParams p) {
   const uint64_t a0 = p.split[tile], a1 = p.split[tile + 1];
   const uint64_t b0 = d0 - a0, b1 = d1 - a1;
   const int nxt = static_cast<int>(a1 - a0), nyt = static_cast<int>(b1 - b0);
-  for (int i = tid; i < nxt; i += kThreads)
+  for (int i = tid; i < nxt; i += kThreads) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) sx[k * kTile + i] = p.xi[k][a0 + i];
-  for (int j = tid; j < nyt; j += kThreads)
+    for (int k = 0; k < N; ++k) sx[k * kTP + pad(i)] = spt::ld_stream(p.xi[k] + a0 + i);
+    sxv[pad(i)] = __ldcs(p.xv + a0 + i);
+  }
+  for (int j = tid; j < nyt; j += kThreads) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) sy[k * kTile + j] = p.yi[k][b0 + j];
+    for (int k = 0; k < N; ++k) sy[k * kTP + pad(j)] = spt::ld_stream(p.yi[k] + b0 + j);
+    syv[pad(j)] = __ldcs(p.yv + b0 + j);
+  }
   __syncthreads();
 
   // Thread-local merge path split.
@@ -168,69 +205,259 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(MergeParams p) {
   uint32_t excl, tile_total;
   Scan(scan_tmp).ExclusiveSum(cnt, excl, tile_total);
 
-  // Decoupled look-back over tile counts: word = epoch<<34 | flag<<32 | count.
-  if (tid == 0) {
+  // Decoupled look-back over tile counts (word = epoch<<34 | flag<<32 | count),
+  // warp-parallel: 32 predecessors per poll.
+  // Decoupled look-back over the tile counts. The count travels inside the
+  // status word itself, so publication is a relaxed store (no MEMBAR) and
+  // polling is relaxed (no L1 invalidation).
+  if (tid < 32) {
     const unsigned long long tag = (unsigned long long)p.epoch << 34;
     unsigned long long base = 0;
     if (tile == 0) {
-      spt::st_release64(p.status + tile, tag | (kFlagP << 32) | tile_total);
+      if (tid == 0) spt::st_relaxed64(p.status + tile, tag | (kFlagP << 32) | tile_total);
     } else {
-      spt::st_release64(p.status + tile, tag | (kFlagA << 32) | tile_total);
-      uint32_t t = tile - 1;
-      while (true) {
-        unsigned long long w;
-        do {
-          w = spt::ld_acquire64(p.status + t);
-        } while ((w >> 34) != p.epoch || ((w >> 32) & 3ull) == 0);
-        base += w & 0xFFFFFFFFull;
-        if (((w >> 32) & 3ull) == kFlagP || t == 0) break;
-        --t;
-      }
-      spt::st_release64(p.status + tile, tag | (kFlagP << 32) | (base + tile_total));
+      if (tid == 0) spt::st_relaxed64(p.status + tile, tag | (kFlagA << 32) | tile_total);
+      base = spt::lookback_count64(p.status, tile, p.epoch);
+      if (tid == 0)
+        spt::st_relaxed64(p.status + tile, tag | (kFlagP << 32) | (base + tile_total));
     }
-    s_base = base;
-    if (tile == p.ntiles - 1) *p.total = base + tile_total;
+    if (tid == 0) {
+      s_base = base;
+      if (tile == p.ntiles - 1) *p.total = base + tile_total;
+    }
   }
   __syncthreads();
-  uint64_t pos = s_base + excl;
 
+  // Emission: every emitted item gets a tile-local slot; each of the N index
+  // arrays and the value array is assembled in shared memory and written out
+  // with fully coalesced stores (the thread-strided direct scatter would cost
+  // one 32-byte sector transaction per 4-byte element).
+  int lslot[kIPT];
+  uint32_t vbits[kIPT];
+  {
+    int lp = static_cast<int>(excl);
 #pragma unroll
-  for (int k = 0; k < kIPT; ++k) {
-    if (src[k] == 0) continue;
-    const bool m = matched[k];
-    if (src[k] == 1) {
-      if (p.op == SPT_MUL && !m) continue;
-      const uint64_t gx = a0 + li[k];
-      float v = __ldg(p.xv + gx);
-      if (m) {
-        // the matching y is the next y in merge order: global b0 + (#y consumed)
-        // recomputed from the tuple position: y index = number of y items before
-        // this x item in merge order.
-        const uint64_t gy = b0 + (static_cast<uint64_t>(dg + k) - li[k]);
-        v = apply(p.op, v, __ldg(p.yv + gy));
+    for (int k = 0; k < kIPT; ++k) {
+      lslot[k] = -1;
+      vbits[k] = 0;
+      if (src[k] == 0) continue;
+      const bool m = matched[k];
+      if (src[k] == 1) {
+        if (p.op == SPT_MUL && !m) continue;
+        float v = sxv[pad(li[k])];
+        if (m) {
+          // the matching y is the next y in merge order: local index = number of
+          // y items before this x item = (dg + k) - li[k]; it may sit just past
+          // this tile's y run.
+          const int yl = dg + k - li[k];
+          v = apply(p.op, v, yl < nyt ? syv[pad(yl)] : __ldg(p.yv + b0 + yl));
+        }
+        vbits[k] = __float_as_uint(v);
+      } else {
+        if (p.op == SPT_MUL || m) continue;
+        const float yv = syv[pad(li[k])];
+        vbits[k] = __float_as_uint(p.op == SPT_SUB ? -yv : yv);
       }
+      lslot[k] = lp++;
+    }
+  }
+  const uint64_t base = s_base;
+#pragma unroll 1
+  for (int q = 0; q <= N; ++q) {
 #pragma unroll
-      for (int q = 0; q < N; ++q) p.zi[q][pos] = sx[q * kTile + li[k]];
-      p.zv[pos] = v;
-      ++pos;
-    } else {
-      if (p.op == SPT_MUL || m) continue;
-      const uint64_t gy = b0 + li[k];
-      const float yv = __ldg(p.yv + gy);
+    for (int k = 0; k < kIPT; ++k) {
+      if (lslot[k] < 0) continue;
+      uint32_t w;
+      if (q == N) w = vbits[k];
+      else w = (src[k] == 1 ? sx : sy)[q * kTP + pad(li[k])];
+      s_obuf[lslot[k]] = w;
+    }
+    __syncthreads();
+    uint32_t* dst = q == N ? reinterpret_cast<uint32_t*>(p.zv) : p.zi[q];
+    for (uint32_t o = tid; o < tile_total; o += kThreads) spt::st_stream(dst + base + o, s_obuf[o]);
+    __syncthreads();
+  }
+}
+
+// Packed-key variant (sum of per-mode index widths <= 64 bits, e.g. C2's
+// 3 x 14 bits): every comparison is one u64 compare on a key staged once per
+// entry; indices are unpacked from the key on emission. u64 smem arrays get
+// one pad element per 16 so the ~4-apart merge positions of a half-warp hit
+// distinct banks.
+constexpr int kTP64 = kTile + kTile / 16;
+__device__ __forceinline__ int pad64(int i) { return i + (i >> 4); }
+
+template <int N>
+__device__ __forceinline__ void stage_side(const uint32_t* const* idx, const float* val,
+                                           uint64_t a0, int n, const uint32_t* shift,
+                                           unsigned long long* sk, float* sv, int tid) {
+  constexpr int R = kTile / kThreads;
+  uint32_t t[R][N];
+  float v[R];
 #pragma unroll
-      for (int q = 0; q < N; ++q) p.zi[q][pos] = sy[q * kTile + li[k]];
-      p.zv[pos] = p.op == SPT_SUB ? -yv : yv;
-      ++pos;
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + r * kThreads;
+    if (i < n) {
+#pragma unroll
+      for (int q = 0; q < N; ++q) t[r][q] = spt::ld_stream(idx[q] + a0 + i);
+      v[r] = __ldcs(val + a0 + i);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + r * kThreads;
+    if (i < n) {
+      unsigned long long k = 0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) k |= (unsigned long long)t[r][q] << shift[q];
+      sk[pad64(i)] = k;
+      sv[pad(i)] = v[r];
     }
   }
 }
 
 template <int N>
+__global__ void __launch_bounds__(kThreads, 4) merge64_kernel(MergeParams p) {
+  using Scan = cub::BlockScan<uint32_t, kThreads>;
+  extern __shared__ __align__(16) unsigned long long smem64[];
+  unsigned long long* sx = smem64;            // [kTP64]
+  unsigned long long* sy = smem64 + kTP64;    // [kTP64]
+  float* sxv = reinterpret_cast<float*>(sy + kTP64);          // [kTP]
+  float* syv = sxv + kTP;                                     // [kTP]
+  // Output staging aliases the x keys: they are dead once the merge is done
+  // (the Scan's barriers separate the last read from the first write).
+  uint32_t* s_obuf = reinterpret_cast<uint32_t*>(sx);  // [kTile]
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_base;
+  __shared__ spt::LookbackSmem s_lb;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    const unsigned long long t = atomicAdd(p.tile_ctr, 1ull);
+    if (t == p.ntiles - 1) atomicExch(p.tile_ctr, 0ull);
+    s_tile = static_cast<uint32_t>(t);
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t total = p.nx + p.ny;
+  const uint64_t d0 = (uint64_t)tile * kTile;
+  const uint64_t d1 = std::min<uint64_t>(d0 + kTile, total);
+  const uint64_t a0 = p.split[tile], a1 = p.split[tile + 1];
+  const uint64_t b0 = d0 - a0, b1 = d1 - a1;
+  const int nxt = static_cast<int>(a1 - a0), nyt = static_cast<int>(b1 - b0);
+  // Stage both runs with every global load of a side in flight at once (one
+  // round trip per side instead of one per loop iteration).
+  // The neighbours just outside the tile (for match tests at the edges),
+  // loaded together with the staging loads.
+  const unsigned long long y_after =
+      (b0 + nyt < p.ny) ? pack_g<N>(p.yi, p, b0 + nyt) : ~0ull;
+  const unsigned long long x_before = (a0 > 0) ? pack_g<N>(p.xi, p, a0 - 1) : ~0ull;
+  stage_side<N>(p.xi, p.xv, a0, nxt, p.shift, sx, sxv, tid);
+  stage_side<N>(p.yi, p.yv, b0, nyt, p.shift, sy, syv, tid);
+  __syncthreads();
+
+  const int len = nxt + nyt;
+  const int dg = std::min(tid * kIPT, len);
+  int lo = std::max(0, dg - nyt), hi = std::min(dg, nxt);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sx[pad64(mid)] <= sy[pad64(dg - 1 - mid)]) lo = mid + 1;
+    else hi = mid;
+  }
+  int i = lo, j = dg - lo;
+  unsigned long long kx = i < nxt ? sx[pad64(i)] : ~0ull;
+  unsigned long long ky = j < nyt ? sy[pad64(j)] : ~0ull;
+  unsigned long long key[kIPT];
+  uint32_t vbits[kIPT];
+  bool emit[kIPT];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int k = 0; k < kIPT; ++k) {
+    emit[k] = false;
+    key[k] = 0;
+    vbits[k] = 0;
+    if (dg + k >= len) continue;
+    const bool take_x = j >= nyt || (i < nxt && kx <= ky);
+    if (take_x) {
+      const unsigned long long ny_key = j < nyt ? ky : y_after;  // next y in merge order
+      const bool m = kx == ny_key;
+      float v = sxv[pad(i)];
+      if (m) v = apply(p.op, v, j < nyt ? syv[pad(j)] : __ldg(p.yv + b0 + j));
+      emit[k] = (p.op != SPT_MUL) || m;
+      key[k] = kx;
+      vbits[k] = __float_as_uint(v);
+      ++i;
+      kx = i < nxt ? sx[pad64(i)] : ~0ull;
+    } else {
+      const unsigned long long px = i > 0 ? sx[pad64(i - 1)] : x_before;  // previous x
+      const bool m = px == ky;
+      const float yv = syv[pad(j)];
+      emit[k] = (p.op != SPT_MUL) && !m;
+      key[k] = ky;
+      vbits[k] = __float_as_uint(p.op == SPT_SUB ? -yv : yv);
+      ++j;
+      ky = j < nyt ? sy[pad64(j)] : ~0ull;
+    }
+    cnt += emit[k] ? 1u : 0u;
+  }
+  uint32_t excl, tile_total;
+  Scan(scan_tmp).ExclusiveSum(cnt, excl, tile_total);
+  // Decoupled look-back over the tile counts. The count travels inside the
+  // status word itself, so publication is a relaxed store (no MEMBAR) and
+  // polling is relaxed (no L1 invalidation).
+  if (tid < 32) {
+    const unsigned long long tag = (unsigned long long)p.epoch << 34;
+    unsigned long long base = 0;
+    if (tile == 0) {
+      if (tid == 0) spt::st_relaxed64(p.status + tile, tag | (kFlagP << 32) | tile_total);
+    } else {
+      if (tid == 0) spt::st_relaxed64(p.status + tile, tag | (kFlagA << 32) | tile_total);
+      base = spt::lookback_count64(p.status, tile, p.epoch);
+      if (tid == 0)
+        spt::st_relaxed64(p.status + tile, tag | (kFlagP << 32) | (base + tile_total));
+    }
+    if (tid == 0) {
+      s_base = base;
+      if (tile == p.ntiles - 1) *p.total = base + tile_total;
+    }
+  }
+  __syncthreads();
+  const uint64_t base = s_base;
+#pragma unroll 1
+  for (int q = 0; q <= N; ++q) {
+    int lp = static_cast<int>(excl);
+#pragma unroll
+    for (int k = 0; k < kIPT; ++k) {
+      if (!emit[k]) continue;
+      s_obuf[lp++] = q == N ? vbits[k] : (uint32_t)((key[k] >> p.shift[q]) & p.mask[q]);
+    }
+    __syncthreads();
+    uint32_t* dst = q == N ? reinterpret_cast<uint32_t*>(p.zv) : p.zi[q];
+    for (uint32_t o = tid; o < tile_total; o += kThreads) spt::st_stream(dst + base + o, s_obuf[o]);
+    __syncthreads();
+  }
+}
+
+template <int N>
+int launch64(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
+  const uint32_t nt = p.ntiles;
+  partition_kernel<N><<<(nt + 1 + 7) / 8, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
+  SPT_LAUNCHED(ctx);
+  const size_t smem = (size_t)2 * kTP64 * 8 + (size_t)2 * kTP * 4;
+  SPT_CUDA(cudaFuncSetAttribute(merge64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  merge64_kernel<N><<<nt, kThreads, smem, st>>>(p);
+  SPT_LAUNCHED(ctx);
+  return SPT_OK;
+}
+
+template <int N>
 int launch(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
   const uint32_t nt = p.ntiles;
-  partition_kernel<N><<<(nt + 1 + 255) / 256, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
+  partition_kernel<N><<<(nt + 1 + 7) / 8, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
   SPT_LAUNCHED(ctx);
-  const size_t smem = (size_t)2 * N * kTile * sizeof(uint32_t);
+  const size_t smem = (size_t)(2 * N + 2) * kTP * sizeof(uint32_t) + kTile * sizeof(uint32_t);
   SPT_CUDA(cudaFuncSetAttribute(merge_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   merge_kernel<N><<<nt, kThreads, smem, st>>>(p);
@@ -312,8 +539,35 @@ extern "C" int spt_tew_f32(spt_ctx* ctx, const spt_coo* x, const spt_coo* y, int
     SPT_TRY(spt::ctx_lookback(ctx, 1, 1, &epoch));
     SPT_TRY(spt::ctx_status64(ctx, ntiles, &p.status));
     p.epoch = epoch;
-    // An empty side makes every key lookup on it invalid; give it a dummy.
-    switch (N) {
+    // Packed u64 keys when the per-mode index widths fit (sort order = key
+    // significance; indices are < dims as validate() requires).
+    uint32_t width[SPT_MAX_ORDER], bits = 0;
+    for (uint32_t k = 0; k < N; ++k) {
+      const uint32_t d = x->sort_order[k];
+      const uint32_t ext = std::max(x->dims[d], y->dims[d]);
+      uint32_t w = 0;
+      while (w < 32 && (1ull << w) < ext) ++w;
+      width[k] = w;
+      bits += w;
+    }
+    if (bits <= 64) {
+      uint32_t sh = 0;
+      for (int k = static_cast<int>(N) - 1; k >= 0; --k) {
+        p.shift[k] = sh;
+        p.mask[k] = width[k] >= 32 ? 0xFFFFFFFFu : ((1u << width[k]) - 1u);
+        sh += width[k];
+      }
+      switch (N) {
+        case 1: SPT_TRY(launch64<1>(ctx, p, st)); break;
+        case 2: SPT_TRY(launch64<2>(ctx, p, st)); break;
+        case 3: SPT_TRY(launch64<3>(ctx, p, st)); break;
+        case 4: SPT_TRY(launch64<4>(ctx, p, st)); break;
+        case 5: SPT_TRY(launch64<5>(ctx, p, st)); break;
+        case 6: SPT_TRY(launch64<6>(ctx, p, st)); break;
+        case 7: SPT_TRY(launch64<7>(ctx, p, st)); break;
+        default: SPT_TRY(launch64<8>(ctx, p, st)); break;
+      }
+    } else switch (N) {
       case 1: SPT_TRY(launch<1>(ctx, p, st)); break;
       case 2: SPT_TRY(launch<2>(ctx, p, st)); break;
       case 3: SPT_TRY(launch<3>(ctx, p, st)); break;

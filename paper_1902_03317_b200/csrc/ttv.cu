@@ -170,27 +170,23 @@ __global__ void __launch_bounds__(kThreads) ttv_kernel(TtvParams p) {
       spt::st_release(p.status + tile, tag | kFlagA);
     }
   }
-  // Look-back for the first fiber's carry-in (thread 0 walks, scalar payload).
-  if (tid == 0) {
+  // Look-back for the first fiber's carry-in: warp 0 finds the chain of A's
+  // ending in a P (32 predecessors per poll) and sums its scalar payloads.
+  if (tid < 32) {
     double carry = 0.0;
     if (cont_prev) {
-      uint32_t j = tile - 1;
-      while (true) {
-        uint32_t s;
-        do {
-          s = spt::ld_acquire(p.status + j);
-        } while ((s >> 3) != p.epoch || (s & 3u) == 0);
-        carry += spt::ld_cg(((s & kFlagP) ? p.payP : p.payA) + j);
-        if ((s & kFlagP) || j == 0) break;
-        --j;
-      }
-      if (cont_next && single) {
+      const uint32_t n = spt::lookback_chain(p.status, tile, p.epoch);
+      for (uint32_t q = 1 + tid; q <= n && q <= tile; q += 32)
+        carry += spt::ld_cg((q == n ? p.payP : p.payA) + (tile - q));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) carry += __shfl_xor_sync(0xffffffffu, carry, o);
+      if (tid == 0 && cont_next && single) {
         p.payP[tile] = carry + block_agg.v;
         __threadfence();
         spt::st_release(p.status + tile, tag | kFlagP);
       }
     }
-    s_carry = carry;
+    if (tid == 0) s_carry = carry;
   }
   __syncthreads();
   const double carry = s_carry;
