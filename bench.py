@@ -120,6 +120,17 @@ def tensor_bytes(nnz, order):
     return nnz * (4 * order + 4)
 
 
+DIST = None  # torch.distributed when running under torchrun with N > 1
+
+
+def allreduce(t):
+    """MTTKRP's one exchange step: every rank holds the
+    dims[n] x R partial of its own nnz shard; NCCL all-reduce over NVLink."""
+    if DIST is not None:
+        DIST.all_reduce(t, op=DIST.ReduceOp.SUM)
+    return t
+
+
 class Workload:
     name = ""
     desc = ""
@@ -261,8 +272,8 @@ class C1(Workload):
         self.z = DeviceCOO.empty(self.dims, self.nnz, device)
         n, N, R = self.nnz, 3, self.R
         self.ops = [
-            Op("mttkrp_m0", lambda: ops.mttkrp(self.x, self.f, 0, ops.MTTKRP_SEGMENTED,
-                                               out=self.out, sync=False),
+            Op("mttkrp_m0", lambda: allreduce(ops.mttkrp(self.x, self.f, 0, ops.MTTKRP_SEGMENTED,
+                                                         out=self.out, sync=False)),
                n, lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims)),
             Op("ts_add", lambda: ops.ts(self.x, 2.5, ops.SCALAR_ADD, out=self.z, sync=False), n,
                lambda: 2 * tensor_bytes(n, N)),
@@ -351,8 +362,9 @@ class C4(Workload):
                     for d in self.dims]
         n, N, R = self.nnz, 4, self.R
         self.ops = [Op(f"mttkrp_m{m}",
-                       lambda m=m: ops.mttkrp(self.xs[m], self.f, m, ops.MTTKRP_SEGMENTED,
-                                              out=self.out[m], sync=False),
+                       lambda m=m: allreduce(ops.mttkrp(self.xs[m], self.f, m,
+                                                        ops.MTTKRP_SEGMENTED, out=self.out[m],
+                                                        sync=False)),
                        n, lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims))
                     for m in range(4)]
 
@@ -412,6 +424,8 @@ def main():
     if world > 1 and args.impl == "ours":
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        global DIST
+        DIST = dist
 
     from paper_1902_03317_b200 import _lib
     wl = WORKLOADS[args.workload](args.seed + 1009 * rank, local, args.scale)
