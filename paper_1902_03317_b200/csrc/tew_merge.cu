@@ -324,9 +324,6 @@ __global__ void __launch_bounds__(kThreads, 4) merge64_kernel(MergeParams p) {
   unsigned long long* sy = smem64 + kTP64;    // [kTP64]
   float* sxv = reinterpret_cast<float*>(sy + kTP64);          // [kTP]
   float* syv = sxv + kTP;                                     // [kTP]
-  // Output staging aliases the x keys: they are dead once the merge is done
-  // (the Scan's barriers separate the last read from the first write).
-  uint32_t* s_obuf = reinterpret_cast<uint32_t*>(sx);  // [kTile]
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_base;
@@ -403,16 +400,31 @@ __global__ void __launch_bounds__(kThreads, 4) merge64_kernel(MergeParams p) {
   }
   uint32_t excl, tile_total;
   Scan(scan_tmp).ExclusiveSum(cnt, excl, tile_total);
-  // Decoupled look-back over the tile counts. The count travels inside the
-  // status word itself, so publication is a relaxed store (no MEMBAR) and
-  // polling is relaxed (no L1 invalidation).
+  // Publish this tile's count right away (relaxed: the count travels inside
+  // the status word, no payload to order, no MEMBAR).
+  const unsigned long long tag = (unsigned long long)p.epoch << 34;
+  if (tid == 0)
+    spt::st_relaxed64(p.status + tile,
+                      tag | ((tile == 0 ? kFlagP : kFlagA) << 32) | tile_total);
+  // Emitted (key, value) pairs go to tile-local slots; this needs no global
+  // offset, so it overlaps the predecessors' publication. The key arrays are
+  // dead (the Scan's barriers separate their last read from these writes).
+  {
+    unsigned long long* s_key = sx;
+    uint32_t* s_val = reinterpret_cast<uint32_t*>(sy);
+    int lp = static_cast<int>(excl);
+#pragma unroll
+    for (int k = 0; k < kIPT; ++k) {
+      if (!emit[k]) continue;
+      s_key[lp] = key[k];
+      s_val[lp] = vbits[k];
+      ++lp;
+    }
+  }
+  // Decoupled look-back (warp 0, relaxed polling of 32 predecessors).
   if (tid < 32) {
-    const unsigned long long tag = (unsigned long long)p.epoch << 34;
     unsigned long long base = 0;
-    if (tile == 0) {
-      if (tid == 0) spt::st_relaxed64(p.status + tile, tag | (kFlagP << 32) | tile_total);
-    } else {
-      if (tid == 0) spt::st_relaxed64(p.status + tile, tag | (kFlagA << 32) | tile_total);
+    if (tile != 0) {
       base = spt::lookback_count64(p.status, tile, p.epoch);
       if (tid == 0)
         spt::st_relaxed64(p.status + tile, tag | (kFlagP << 32) | (base + tile_total));
@@ -423,19 +435,16 @@ __global__ void __launch_bounds__(kThreads, 4) merge64_kernel(MergeParams p) {
     }
   }
   __syncthreads();
+  // One coalesced pass: each output element unpacks its N indices from the key.
   const uint64_t base = s_base;
-#pragma unroll 1
-  for (int q = 0; q <= N; ++q) {
-    int lp = static_cast<int>(excl);
+  const unsigned long long* s_key = sx;
+  const uint32_t* s_val = reinterpret_cast<const uint32_t*>(sy);
+  for (uint32_t o = tid; o < tile_total; o += kThreads) {
+    const unsigned long long k = s_key[o];
 #pragma unroll
-    for (int k = 0; k < kIPT; ++k) {
-      if (!emit[k]) continue;
-      s_obuf[lp++] = q == N ? vbits[k] : (uint32_t)((key[k] >> p.shift[q]) & p.mask[q]);
-    }
-    __syncthreads();
-    uint32_t* dst = q == N ? reinterpret_cast<uint32_t*>(p.zv) : p.zi[q];
-    for (uint32_t o = tid; o < tile_total; o += kThreads) spt::st_stream(dst + base + o, s_obuf[o]);
-    __syncthreads();
+    for (int q = 0; q < N; ++q)
+      spt::st_stream(p.zi[q] + base + o, (uint32_t)((k >> p.shift[q]) & p.mask[q]));
+    spt::st_stream(reinterpret_cast<uint32_t*>(p.zv) + base + o, s_val[o]);
   }
 }
 
