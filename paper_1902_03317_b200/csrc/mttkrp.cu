@@ -527,29 +527,28 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
     __syncthreads();
     if (tid == 0) spt::st_release(p.status + tile, tag | kFlagA);
   }
-  if (cont_prev) {
-    // Warp 0 finds the chain [tile-n, tile-1] (A's ending in a P) 32 tiles per
-    // poll; then every column thread sums the chain's payloads.
+  if (cont_prev && (boundary || !cont_next)) {
+    // This tile completes a row that started in an earlier tile: it sums the
+    // aggregates of every tile the row crossed (A's back to the P of the tile
+    // where the row started). Tiles strictly inside a heavy row publish only
+    // their A and never wait, so a row spanning thousands of tiles costs one
+    // walk at its end instead of a serial chain of inclusive prefixes.
     if (warp == 0) {
       const uint32_t n = spt::lookback_chain(p.status, tile, p.epoch);
       if (lane == 0) s_flag = n;
     }
     __syncthreads();
     const uint32_t n = s_flag;
-    if (c < CB) {
-      for (uint32_t q = 1; q <= n && q <= tile; ++q) {
-        const uint32_t j = tile - q;
-        carry += spt::ld_cg((q == n ? p.payP : p.payA) + (size_t)j * CB + c);
-      }
-    }
-    if (cont_next && !boundary) {
-      if (c < CB) {
-        p.payP[(size_t)tile * CB + c] = carry + head_acc;
-        __threadfence();
-      }
-      __syncthreads();
-      if (tid == 0) spt::st_release(p.status + tile, tag | kFlagP);
-    }
+    // The CTA sums the chain: NS slices per column, fixed order (deterministic).
+    constexpr int NS = kThreads / CB;
+    const int cc = tid % CB, sl = tid / CB;
+    double part = 0.0;
+    for (uint32_t q = 1 + sl; q <= n && q <= tile; q += NS)
+      part += spt::ld_cg((q == n ? p.payP : p.payA) + (size_t)(tile - q) * CB + cc);
+    s_gslot[sl * CB + cc] = part;  // group slots are free after the warp fold
+    __syncthreads();
+    if (c < CB)
+      for (int s = 0; s < NS; ++s) carry += s_gslot[s * CB + c];
   }
 
   // ---- rows completed by this tile ------------------------------------------

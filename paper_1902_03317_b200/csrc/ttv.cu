@@ -54,6 +54,7 @@ struct TtvParams {
   double* payA;
   double* payP;
   unsigned long long* tile_ctr;
+  int vec_ok;  // mode-index and value arrays 16-byte aligned (vector loads)
 };
 
 template <int NO>
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) ttv_kernel(TtvParams p) {
   const int e0 = tid * kEPT;
   float val[kEPT];
   uint32_t kk[kEPT];
-  if (cnt == kTile) {
+  if (cnt == kTile && p.vec_ok) {
     const uint4 k0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0));
     const uint4 k1 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0) + 1);
     const uint4 v0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0 + e0));
@@ -172,26 +173,28 @@ __global__ void __launch_bounds__(kThreads) ttv_kernel(TtvParams p) {
   }
   // Look-back for the first fiber's carry-in: warp 0 finds the chain of A's
   // ending in a P (32 predecessors per poll) and sums its scalar payloads.
+  // Only a tile that completes its first fiber walks back; tiles strictly
+  // inside a long fiber publish their aggregate and never wait.
   if (tid < 32) {
     double carry = 0.0;
-    if (cont_prev) {
+    if (cont_prev && !(single && cont_next)) {
       const uint32_t n = spt::lookback_chain(p.status, tile, p.epoch);
       for (uint32_t q = 1 + tid; q <= n && q <= tile; q += 32)
         carry += spt::ld_cg((q == n ? p.payP : p.payA) + (tile - q));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) carry += __shfl_xor_sync(0xffffffffu, carry, o);
-      if (tid == 0 && cont_next && single) {
-        p.payP[tile] = carry + block_agg.v;
-        __threadfence();
-        spt::st_release(p.status + tile, tag | kFlagP);
-      }
     }
     if (tid == 0) s_carry = carry;
   }
   __syncthreads();
   const double carry = s_carry;
 
-  // Emit fibers that end in this tile; heads write the index tuple.
+  // Fibers ending here get their value, fibers starting here their index
+  // tuple (gathered from the head entry), staged by local fiber id and then
+  // written with coalesced stores (consecutive fibers -> consecutive slots).
+  extern __shared__ uint32_t s_dyn[];
+  float* s_zv = reinterpret_cast<float*>(s_dyn);  // [kTile + 2]
+  uint32_t* s_zi = s_dyn + (kTile + 2);           // [NO][kTile + 2]
   double run = excl.v;
 #pragma unroll
   for (int i = 0; i < kEPT; ++i) {
@@ -199,14 +202,22 @@ __global__ void __launch_bounds__(kThreads) ttv_kernel(TtvParams p) {
     if (e >= cnt) break;
     const uint64_t m = t0 + e;
     run = head[i] ? (double)term[i] : run + (double)term[i];
-    const uint32_t f = f_lo + lf[i];
     if (head[i]) {
 #pragma unroll
-      for (int d = 0; d < NO; ++d) p.zidx[d][f] = p.hidx[d][m];
+      for (int d = 0; d < NO; ++d) s_zi[d * (kTile + 2) + lf[i]] = p.hidx[d][m];
     }
-    const bool fiber_end_here = s_fptr[lf[i] + 1] == m + 1;
-    if (fiber_end_here) p.zval[f] = (float)(run + (lf[i] == 0 ? carry : 0.0));
+    if (s_fptr[lf[i] + 1] == m + 1) s_zv[lf[i]] = (float)(run + (lf[i] == 0 ? carry : 0.0));
   }
+  __syncthreads();
+  const int last = s_meta[2];
+  const int end_hi = cont_next ? last : last + 1;  // fibers [0, end_hi) end here
+  const int head_lo = cont_prev ? 1 : 0;           // fibers [head_lo, last] start here
+  for (int o = tid; o < end_hi; o += kThreads) spt::st_stream(
+      reinterpret_cast<uint32_t*>(p.zval) + f_lo + o, __float_as_uint(s_zv[o]));
+#pragma unroll
+  for (int d = 0; d < NO; ++d)
+    for (int o = head_lo + tid; o <= last; o += kThreads)
+      spt::st_stream(p.zidx[d] + f_lo + o, s_zi[d * (kTile + 2) + o]);
 }
 
 // map[t] = fiber containing entry t*tile (fptr is non-decreasing, every fiber
@@ -219,6 +230,16 @@ __global__ void tile_fiber_kernel(const uint32_t* fptr, uint32_t nfibs, uint32_t
     const uint32_t a = (fptr[f] + tile - 1) / tile, b = (fptr[f + 1] + tile - 1) / tile;
     for (uint32_t t = a; t < b; ++t) map[t] = f;
   }
+}
+
+template <int NO>
+int launch_ttv(spt_ctx* ctx, const TtvParams& p, unsigned grid, cudaStream_t st) {
+  const size_t smem = (size_t)(NO + 1) * (kTile + 2) * sizeof(uint32_t);
+  SPT_CUDA(cudaFuncSetAttribute(ttv_kernel<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  ttv_kernel<NO><<<grid, kThreads, smem, st>>>(p);
+  SPT_LAUNCHED(ctx);
+  return SPT_OK;
 }
 
 }  // namespace
@@ -306,19 +327,17 @@ extern "C" int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uin
   p.payA = ctx->d_payload;
   p.payP = ctx->d_payload + ntiles;
   p.tile_ctr = ctx->d_tile_ctr;
-  const bool aligned = spt::aligned16(x->idx[mode]) && spt::aligned16(x->val);
-  if (!aligned) return spt::set_error(SPT_EINVAL, "ttv: index/value arrays must be 16-byte aligned");
+  p.vec_ok = spt::aligned16(x->idx[mode]) && spt::aligned16(x->val);
   const unsigned grid = static_cast<unsigned>(ntiles);
   switch (N - 1) {
-    case 1: ttv_kernel<1><<<grid, kThreads, 0, st>>>(p); break;
-    case 2: ttv_kernel<2><<<grid, kThreads, 0, st>>>(p); break;
-    case 3: ttv_kernel<3><<<grid, kThreads, 0, st>>>(p); break;
-    case 4: ttv_kernel<4><<<grid, kThreads, 0, st>>>(p); break;
-    case 5: ttv_kernel<5><<<grid, kThreads, 0, st>>>(p); break;
-    case 6: ttv_kernel<6><<<grid, kThreads, 0, st>>>(p); break;
-    default: ttv_kernel<7><<<grid, kThreads, 0, st>>>(p); break;
+    case 1: SPT_TRY(launch_ttv<1>(ctx, p, grid, st)); break;
+    case 2: SPT_TRY(launch_ttv<2>(ctx, p, grid, st)); break;
+    case 3: SPT_TRY(launch_ttv<3>(ctx, p, grid, st)); break;
+    case 4: SPT_TRY(launch_ttv<4>(ctx, p, grid, st)); break;
+    case 5: SPT_TRY(launch_ttv<5>(ctx, p, grid, st)); break;
+    case 6: SPT_TRY(launch_ttv<6>(ctx, p, grid, st)); break;
+    default: SPT_TRY(launch_ttv<7>(ctx, p, grid, st)); break;
   }
-  SPT_LAUNCHED(ctx);
   (void)flags;
   return SPT_OK;
 }
