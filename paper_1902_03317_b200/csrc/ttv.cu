@@ -58,7 +58,7 @@ struct TtvParams {
 };
 
 template <int NO>
-__global__ void __launch_bounds__(kThreads) ttv_kernel(TtvParams p) {
+__global__ void __launch_bounds__(kThreads, 4) ttv_kernel(TtvParams p) {
   using Scan = cub::BlockScan<SegPair, kThreads>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ uint32_t s_fptr[kTile + 2];
@@ -85,7 +85,17 @@ __global__ void __launch_bounds__(kThreads) ttv_kernel(TtvParams p) {
   const int e0 = tid * kEPT;
   float val[kEPT];
   uint32_t kk[kEPT];
+  // The other modes' indices are read up front (fiber heads take their output
+  // tuple from here), so the emission needs no second dependent round trip.
+  uint32_t oi[NO][kEPT];
   if (cnt == kTile && p.vec_ok) {
+#pragma unroll
+    for (int d = 0; d < NO; ++d) {
+      const uint4 a = spt::ld_stream(reinterpret_cast<const uint4*>(p.hidx[d] + t0 + e0));
+      const uint4 b = spt::ld_stream(reinterpret_cast<const uint4*>(p.hidx[d] + t0 + e0) + 1);
+      oi[d][0] = a.x, oi[d][1] = a.y, oi[d][2] = a.z, oi[d][3] = a.w;
+      oi[d][4] = b.x, oi[d][5] = b.y, oi[d][6] = b.z, oi[d][7] = b.w;
+    }
     const uint4 k0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0));
     const uint4 k1 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0) + 1);
     const uint4 v0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0 + e0));
@@ -102,6 +112,8 @@ __global__ void __launch_bounds__(kThreads) ttv_kernel(TtvParams p) {
       const bool ok = e0 + i < cnt;
       kk[i] = ok ? p.kidx[t0 + e0 + i] : 0;
       val[i] = ok ? p.val[t0 + e0 + i] : 0.0f;
+#pragma unroll
+      for (int d = 0; d < NO; ++d) oi[d][i] = ok ? p.hidx[d][t0 + e0 + i] : 0;
     }
   }
   float term[kEPT];
@@ -204,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) ttv_kernel(TtvParams p) {
     run = head[i] ? (double)term[i] : run + (double)term[i];
     if (head[i]) {
 #pragma unroll
-      for (int d = 0; d < NO; ++d) s_zi[d * (kTile + 2) + lf[i]] = p.hidx[d][m];
+      for (int d = 0; d < NO; ++d) s_zi[d * (kTile + 2) + lf[i]] = oi[d][i];
     }
     if (s_fptr[lf[i] + 1] == m + 1) s_zv[lf[i]] = (float)(run + (lf[i] == 0 ? carry : 0.0));
   }
@@ -327,7 +339,9 @@ extern "C" int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uin
   p.payA = ctx->d_payload;
   p.payP = ctx->d_payload + ntiles;
   p.tile_ctr = ctx->d_tile_ctr;
-  p.vec_ok = spt::aligned16(x->idx[mode]) && spt::aligned16(x->val);
+  p.vec_ok = 1;
+  for (uint32_t d = 0; d < N; ++d) p.vec_ok = p.vec_ok && spt::aligned16(x->idx[d]);
+  p.vec_ok = p.vec_ok && spt::aligned16(x->val);
   const unsigned grid = static_cast<unsigned>(ntiles);
   switch (N - 1) {
     case 1: SPT_TRY(launch_ttv<1>(ctx, p, grid, st)); break;
