@@ -64,6 +64,7 @@ struct MttkrpParams {
   double* payP;  // [ntiles][CB]
   unsigned long long* tile_ctr;
   unsigned long long* err;
+  int vec_ok;  // per-entry arrays 16-byte aligned (vector staging)
   // TTM (FIBER=true): output rows are fibers of an x sorted with `mode` last.
   const uint32_t* fptr;
   const uint32_t* tile_fiber;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
     nstage = f_end - f_lo + 1;
     for (uint32_t i = tid; i < nstage; i += kThreads) s_fptr[i] = p.fptr[f_lo + i];
   }
-  if (cnt == kTile) {
+  if (cnt == kTile && p.vec_ok) {
     const int nv = kTile / 4;
     for (int i = tid; i < nv; i += kThreads) {
       if constexpr (!FIBER)
@@ -205,11 +206,15 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
             spt::ld_stream(reinterpret_cast<const uint4*>(p.oidx[j] + t0) + i);
     }
   } else {
-    for (int i = tid; i < cnt; i += kThreads) {
-      if constexpr (!FIBER) s_out[sw(i)] = p.out_idx[t0 + i];
-      s_val[sw(i)] = p.val[t0 + i];
+    // Partial (or unaligned) tile: scalar loads; entries past the end get
+    // index 0 / value 0 so the gather loop can load unconditionally (their
+    // rows are marked dead and never accumulated).
+    for (int i = tid; i < kTile; i += kThreads) {
+      const bool ok = i < cnt;
+      if constexpr (!FIBER) s_out[sw(i)] = ok ? p.out_idx[t0 + i] : 0u;
+      s_val[sw(i)] = ok ? p.val[t0 + i] : 0.0f;
 #pragma unroll
-      for (int j = 0; j < NM1; ++j) s_oidx[j * kTileP + sw(i)] = p.oidx[j][t0 + i];
+      for (int j = 0; j < NM1; ++j) s_oidx[j * kTileP + sw(i)] = ok ? p.oidx[j][t0 + i] : 0u;
     }
   }
   for (int i = tid; i < NSLOT; i += kThreads) s_slot_row[i] = kNone;
@@ -265,6 +270,13 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
     a32[k] = 0.0f;
   }
 
+  // Per-lane byte bases of the factor slices (column folded in; lanes beyond
+  // ncols read column c0, never stored) and the byte row stride.
+  const char* fbase[NM1];
+#pragma unroll
+  for (int j = 0; j < NM1; ++j)
+    fbase[j] = reinterpret_cast<const char*>(p.ofac[j] + (col_ok ? col : p.c0));
+  const uint32_t rstride = p.R * 4u;
   constexpr int kUnroll = (NM1 * VEC <= 12) ? 4 : 2;
   for (int e = e_begin; e < e_end; e += kUnroll) {
     float prod[kUnroll][VEC];
@@ -278,23 +290,19 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
 #pragma unroll
     for (int j = 0; j < NM1; ++j) ld_batch<kUnroll>(s_oidx + j * kTileP + sw(e), ix[j]);
     const bool full = e + kUnroll <= e_end;
-    // Issue every gather of the batch before consuming any.
+    // Issue every gather of the batch before consuming any. Loads are
+    // unconditional (dead entries carry index 0, dead columns read a valid
+    // column) so the block is straight-line: one IMAD.WIDE + one LDG each.
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (e + u >= e_end) rr[u] = kNone;
     float f[kUnroll][NM1][VEC];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int eu = e + u;
-      if (eu < e_end && col_ok) {
+    for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
-        for (int j = 0; j < NM1; ++j)
-          Vec<VEC>::load(p.ofac[j] + (size_t)ix[j][u] * p.R + col, f[u][j]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < NM1; ++j)
-#pragma unroll
-          for (int k = 0; k < VEC; ++k) f[u][j][k] = 0.0f;
-      }
-      if (eu >= e_end) rr[u] = kNone;
-    }
+      for (int j = 0; j < NM1; ++j)
+        Vec<VEC>::load(reinterpret_cast<const float*>(fbase[j] + (size_t)ix[j][u] * rstride),
+                       f[u][j]);
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
 #pragma unroll
@@ -739,6 +747,7 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
   p.oidx[0] = x->idx[mode];
   p.ofac[0] = d_u;
   p.val = x->val;
+  p.vec_ok = spt::aligned16(x->idx[mode]) && spt::aligned16(x->val);
   p.out = z->val;
   p.nnz = x->nnz;
   p.rows = static_cast<uint32_t>(nfibs);
@@ -836,6 +845,9 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
   p.out = d_out;
   p.nnz = x->nnz;
   p.rows = I;
+  p.vec_ok = 1;
+  for (uint32_t d = 0; d < N; ++d) p.vec_ok = p.vec_ok && spt::aligned16(x->idx[d]);
+  p.vec_ok = p.vec_ok && spt::aligned16(x->val);
   p.R = static_cast<uint32_t>(R);
   p.err = ctx->d_err;
   p.tile_ctr = ctx->d_tile_ctr;
