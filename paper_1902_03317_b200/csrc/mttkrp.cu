@@ -116,6 +116,17 @@ struct Vec<4> {
   }
 };
 template <>
+struct Vec<2> {
+  static __device__ __forceinline__ void load(const float* p, float (&f)[2]) {
+    const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+    f[0] = v.x;
+    f[1] = v.y;
+  }
+  static __device__ __forceinline__ void store(float* p, const float (&f)[2]) {
+    *reinterpret_cast<float2*>(p) = make_float2(f[0], f[1]);
+  }
+};
+template <>
 struct Vec<1> {
   static __device__ __forceinline__ void load(const float* p, float (&f)[1]) { f[0] = __ldg(p); }
   static __device__ __forceinline__ void store(float* p, const float (&f)[1]) { *p = f[0]; }
