@@ -70,6 +70,7 @@ struct MttkrpParams {
   const uint32_t* tile_fiber;
   const uint32_t* hidx[SPT_MAX_ORDER];  // x.indices[d] for the output index tuples
   uint32_t* zidx[SPT_MAX_ORDER];        // z.indices[d]
+  const uint32_t* hnm[SPT_MAX_ORDER - 1];  // x.indices of the non-mode dims, ascending
   uint32_t N;
   uint32_t mode;
 };
@@ -77,17 +78,24 @@ struct MttkrpParams {
 // TTM output index tuples of fiber `row` for `ncol` columns starting at col:
 // z.indices[d][row*R + r] = head index of the fiber (d != mode) or r
 // (P/src/kernels_seq.cpp:128-138).
+// The fiber head's non-mode indices come from the tile's staged copy
+// (s_hid[j][sw(head - t0)], j = non-mode dims ascending) when the head lies in
+// the tile -- no dependent global load per output row -- else from global.
 template <int NCOL>
 __device__ __forceinline__ void ttm_emit_idx(const MttkrpParams& p, uint32_t head,
-                                             uint32_t row, uint32_t col) {
+                                             uint32_t row, uint32_t col, const uint32_t* s_hid,
+                                             uint64_t t0) {
   const size_t base = (size_t)row * p.R + col;
+  int j = 0;
   for (uint32_t d = 0; d < p.N; ++d) {
     uint32_t w[NCOL];
     if (d == p.mode) {
 #pragma unroll
       for (int k = 0; k < NCOL; ++k) w[k] = col + k;
     } else {
-      const uint32_t h = p.hidx[d][head];
+      const uint32_t h = head >= t0 ? s_hid[j * kTileP + sw(static_cast<int>(head - t0))]
+                                    : p.hidx[d][head];
+      ++j;
 #pragma unroll
       for (int k = 0; k < NCOL; ++k) w[k] = h;
     }
@@ -179,6 +187,8 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
   uint32_t* s_oidx = reinterpret_cast<uint32_t*>(s_val + kTileP);      // [NM1][kTileP]
   uint32_t* s_fptr = s_oidx + NM1 * kTileP;                            // FIBER: [kTile+2]
   double* s_gslot = reinterpret_cast<double*>(s_fptr + (FIBER ? kTile + 4 : 0));  // [GROUPS*2][CB]
+  // FIBER: the tile's non-mode indices (fiber head tuples), [N-1][kTileP].
+  uint32_t* s_hid = reinterpret_cast<uint32_t*>(s_gslot + 2 * GROUPS * CB);
   __shared__ uint32_t s_grow[2 * GROUPS];
   __shared__ uint32_t s_slot_row[NSLOT];
   __shared__ uint32_t s_tile, s_flag;
@@ -227,6 +237,10 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
 #pragma unroll
       for (int j = 0; j < NM1; ++j) s_oidx[j * kTileP + sw(i)] = ok ? p.oidx[j][t0 + i] : 0u;
     }
+  }
+  if constexpr (FIBER) {
+    for (uint32_t j = 0; j + 1 < p.N; ++j)
+      for (int i = tid; i < cnt; i += kThreads) s_hid[j * kTileP + sw(i)] = p.hnm[j][t0 + i];
   }
   for (int i = tid; i < NSLOT; i += kThreads) s_slot_row[i] = kNone;
   __syncthreads();
@@ -362,7 +376,8 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
 #pragma unroll
             for (int k = 0; k < VEC; ++k) o[k] = (float)acc[k];
             Vec<VEC>::store(p.out + (size_t)run_row * p.R + col, o);
-            if constexpr (FIBER) ttm_emit_idx<VEC>(p, s_fptr[run_row - f_lo], run_row, col);
+            if constexpr (FIBER)
+              ttm_emit_idx<VEC>(p, s_fptr[run_row - f_lo], run_row, col, s_hid, t0);
           }
           if (row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
         }
@@ -422,7 +437,8 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
 #pragma unroll
               for (int k = 0; k < VEC; ++k) o[k] = (float)w_acc[k];
               Vec<VEC>::store(p.out + (size_t)w_cur * p.R + col, o);
-              if constexpr (FIBER) ttm_emit_idx<VEC>(p, s_fptr[w_cur - f_lo], w_cur, col);
+              if constexpr (FIBER)
+                ttm_emit_idx<VEC>(p, s_fptr[w_cur - f_lo], w_cur, col, s_hid, t0);
             }
             if (g != cur_g && row > w_cur + 1 && writer)
               zero_rows<VEC>(p.out, w_cur + 1, row, p.R, col, true);
@@ -497,7 +513,8 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
           else if (cur_row == tail_row) tail_acc = cur;
           else if (cok) {
             p.out[(size_t)cur_row * p.R + p.c0 + c] = (float)cur;
-            if constexpr (FIBER) ttm_emit_idx<1>(p, s_fptr[cur_row - f_lo], cur_row, p.c0 + c);
+            if constexpr (FIBER)
+              ttm_emit_idx<1>(p, s_fptr[cur_row - f_lo], cur_row, p.c0 + c, s_hid, t0);
           }
           if ((s >> 1) != cur_group && r > cur_row + 1 && cok)
             for (uint32_t z = cur_row + 1; z < r; ++z) p.out[(size_t)z * p.R + p.c0 + c] = 0.0f;
@@ -576,12 +593,13 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
       p.out[(size_t)head_row * p.R + p.c0 + c] = (float)(carry + head_acc);
       if constexpr (FIBER) {
         // The head of the tile's first fiber may lie in an earlier tile.
-        ttm_emit_idx<1>(p, s_fptr[head_row - f_lo], head_row, p.c0 + c);
+        ttm_emit_idx<1>(p, s_fptr[head_row - f_lo], head_row, p.c0 + c, s_hid, t0);
       }
     }
     if (boundary && !cont_next) {
       p.out[(size_t)tail_row * p.R + p.c0 + c] = (float)tail_acc;
-      if constexpr (FIBER) ttm_emit_idx<1>(p, s_fptr[tail_row - f_lo], tail_row, p.c0 + c);
+      if constexpr (FIBER)
+        ttm_emit_idx<1>(p, s_fptr[tail_row - f_lo], tail_row, p.c0 + c, s_hid, t0);
     }
   }
 }
@@ -768,14 +786,16 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
   p.ntiles = static_cast<uint32_t>(ntiles);
   p.fptr = d_fptr;
   p.tile_fiber = map;
-  for (uint32_t d = 0; d < N; ++d) {
+  for (uint32_t d = 0, j = 0; d < N; ++d) {
     p.hidx[d] = x->idx[d];
     p.zidx[d] = z->idx[d];
+    if (d != mode) p.hnm[j++] = x->idx[d];
   }
   p.N = N;
   p.mode = mode;
+  const size_t smem = v.smem + (size_t)(N - 1) * kTileP * sizeof(uint32_t);
   SPT_CUDA(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(v.smem)));
+                                static_cast<int>(smem)));
   for (uint32_t c0 = 0; c0 < R; c0 += CB) {
     uint32_t epoch;
     SPT_TRY(spt::ctx_lookback(ctx, ntiles, 2 * ntiles * CB, &epoch));
@@ -785,7 +805,7 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
     p.epoch = epoch;
     p.c0 = c0;
     p.ncols = std::min<uint32_t>(CB, R - c0);
-    v.fn<<<static_cast<unsigned>(ntiles), kThreads, v.smem, st>>>(p);
+    v.fn<<<static_cast<unsigned>(ntiles), kThreads, smem, st>>>(p);
     SPT_LAUNCHED(ctx);
   }
   (void)flags;
