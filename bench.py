@@ -116,6 +116,35 @@ class Op:
         self.launches = 0
 
 
+def report_rows(wl, ops_list):
+    """Reference-schema rows (variant "gpu") for --report; flops are the
+    sequential reference's counts (P/src/kernels_seq.cpp:37,51,65,99,144,172)."""
+    from paper_1902_03317_b200 import report
+    rows = []
+    N = len(wl.dims)
+    R = getattr(wl, "R", 0)
+    for op in ops_list:
+        name = op.name
+        kind, _, rest = name.rpartition("_") if name.startswith("tew_eq") else name.partition("_")
+        mode = opn = None
+        if name.startswith("tew_eq"):
+            kernel, opn = "tew_eq", name.split("_")[-1]
+            fl = wl.nnz
+        elif name.startswith("tew_"):
+            kernel, opn = "tew", rest
+            nz = wl.nz[opn]
+            fl = 2 * wl.nnz - nz if opn == "add" else nz
+        elif name.startswith("ts_"):
+            kernel, opn, fl = "ts", rest, wl.nnz
+        else:
+            kernel, mode = kind, rest.lstrip("m")
+            fl = {"ttv": 2 * wl.nnz, "ttm": 2 * R * wl.nnz, "mttkrp": N * R * wl.nnz}[kernel]
+        rows.append(report.bench_report(wl.name, wl.dims, wl.nnz, kernel,
+                                        [t / 1e3 for t in op.times], fl, op=opn, mode=mode,
+                                        rank=R if kernel in ("ttm", "mttkrp") else 0))
+    return rows
+
+
 def tensor_bytes(nnz, order):
     return nnz * (4 * order + 4)
 
@@ -411,6 +440,9 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0, help="nnz scale (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--report", default=None,
+                    help="also write per-op rows in the reference's BenchReport schema "
+                         "(.json or .csv, P/include/spten/report.hpp)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -558,6 +590,12 @@ def main():
                 "gpu_launches": int(sum(op.launches for op in wl.ops)),
                 "clocks": clk, "ops": ops_out}
         print(json.dumps(line))
+        if args.report:
+            from paper_1902_03317_b200 import report
+            rows = report_rows(wl, wl.ops)
+            with open(args.report, "w") as fh:
+                fh.write(report.emit_csv(rows) if args.report.endswith(".csv")
+                         else report.emit_json(rows))
     if dist:
         dist.destroy_process_group()
 
