@@ -110,8 +110,9 @@ class Clocks:
 
 
 class Op:
-    def __init__(self, name, fn, units, bytes_fn, e2e=None):
+    def __init__(self, name, fn, units, bytes_fn, e2e=None, prep=None):
         self.name, self.fn, self.units, self.bytes_fn = name, fn, units, bytes_fn
+        self.prep = prep  # untimed setup before each call (e.g. restore an unsorted input)
         self.times = []
         self.launches = 0
 
@@ -403,7 +404,60 @@ class C4(Workload):
                 "mttkrp_input": "one mode-leading sorted copy per mode (preprocessing)"}
 
 
-WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4}
+class Pre(Workload):
+    """SURVEY 8(f) "next" row 1: GPU preprocessing at parity and speed --
+    sort_lexicographic (P/src/tensor.cpp:54-64; 4.56 s for 10M on the
+    reference here) and build_fiber_index (:92-120), on C2's 10M tensor in
+    draw (unsorted) order and C3's order for the fiber index."""
+
+    name = "pre-sort-fiber"
+
+    def __init__(self, seed, device, scale=1.0):
+        from paper_1902_03317_b200 import generate, ops
+        c = generate.CONFIGS["c2"]
+        self.dims = c["dims"]
+        self.nnz = int(c["nnz"] * scale)
+        self.src = generate.coo(self.dims, self.nnz, seed, c["zipf"], 0.5, 1.5, None, device)
+        self.work = self.src.clone()
+        self.sorted = self.src.clone()
+        ops.sort_lexicographic(self.sorted, [0, 1, 2])
+        self.fib = ops.build_fiber_index(self.sorted, 2)
+        n, N = self.nnz, 3
+
+        def restore():
+            for a, b in zip(self.work.indices, self.src.indices):
+                a.copy_(b)
+            self.work.values.copy_(self.src.values)
+            self.work.sort_order = None
+
+        self.ops = [
+            Op("sort_lexicographic", lambda: ops.sort_lexicographic(self.work, [0, 1, 2],
+                                                                    sync=False),
+               n, lambda: 2 * tensor_bytes(n, N), prep=restore),
+            Op("build_fiber_index", lambda: ops.build_fiber_index(self.sorted, 2),
+               n, lambda: 8 * n + 4 * (self.fib.nfibs + 1)),
+        ]
+
+    def config(self):
+        return {"workload": self.name, "dims": self.dims, "nnz": self.nnz,
+                "sort": "draw order -> (0,1,2), stable LSD radix, bit-exact vs std::stable_sort",
+                "fiber_index": "mode 2 on the (0,1,2)-sorted tensor",
+                "note": "preprocessing, timed separately like the reference's sort_s"}
+
+    def cpu_setup(self, ref, sample_nnz=2_000_000):
+        from oracle.oracle import HostTensor
+        h = self.src.to_host()
+        k = min(sample_nnz, self.nnz)
+        self.cpu_t = HostTensor(h.dims, [a[:k] for a in h.indices], h.values[:k], None, True)
+        self.cpu_units = k
+        return f"sort_lexicographic (0,1,2) of the first {k} entries (reference, serial)"
+
+    def cpu_step(self, ref, nthreads):
+        ref.sort_lexicographic(self.cpu_t, [0, 1, 2])
+        return self.cpu_units
+
+
+WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "pre": Pre}
 
 
 # ---------------------------------------------------------------------------
@@ -483,6 +537,8 @@ def main():
     sh = stream.cuda_stream
 
     def run_op(op, timed):
+        if op.prep is not None:
+            op.prep()
         lib.spt_l2_flush(ctx.handle, sh)
         l0 = ctx.launches()
         a = torch.cuda.Event(enable_timing=True)
