@@ -62,8 +62,11 @@ typedef enum spt_elem_op { SPT_ADD = 0, SPT_SUB = 1, SPT_MUL = 2, SPT_DIV = 3 } 
 typedef enum spt_scalar_op { SPT_SCALAR_ADD = 0, SPT_SCALAR_MUL = 1 } spt_scalar_op;
 typedef enum spt_mttkrp_strategy {
   SPT_MTTKRP_AUTO = -1,     /* segmented if sort_order[0]==mode, else atomic */
-  SPT_MTTKRP_SEGMENTED = 0, /* mode-sorted input; one writer per output row; deterministic */
-  SPT_MTTKRP_ATOMIC = 1     /* any order; vector red.global.add into a zeroed output */
+  SPT_MTTKRP_SEGMENTED = 0, /* mode-sorted input; one writer per output row; deterministic;
+                               tile shape (CTA / warp) picked by size */
+  SPT_MTTKRP_ATOMIC = 1,    /* any order; vector red.global.add into a zeroed output */
+  SPT_MTTKRP_SEGMENTED_CTA = 2,  /* segmented, forced 2048-entry CTA tiles */
+  SPT_MTTKRP_SEGMENTED_WARP = 3  /* segmented, forced 256-entry warp tiles */
 } spt_mttkrp_strategy;
 
 /* Device-resident COO tensor descriptor (mirror of SparseTensorCOO<float>,

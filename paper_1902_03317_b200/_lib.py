@@ -27,6 +27,7 @@ SPT_FLAG_ASYNC = 1
 ADD, SUB, MUL, DIV = 0, 1, 2, 3
 SCALAR_ADD, SCALAR_MUL = 0, 1
 MTTKRP_AUTO, MTTKRP_SEGMENTED, MTTKRP_ATOMIC = -1, 0, 1
+MTTKRP_SEGMENTED_CTA, MTTKRP_SEGMENTED_WARP = 2, 3  # forced tile shape (tuning/tests)
 
 
 class InvalidArgument(ValueError):

@@ -19,13 +19,14 @@ import torch
 
 from . import _lib
 from ._lib import (ADD, DIV, MUL, SUB, SCALAR_ADD, SCALAR_MUL, MTTKRP_AUTO, MTTKRP_ATOMIC,
+                   MTTKRP_SEGMENTED_CTA, MTTKRP_SEGMENTED_WARP,
                    MTTKRP_SEGMENTED, InvalidArgument, check)
 from .coo import DeviceCOO, FiberIndex, ptr
 
 __all__ = [
     "ADD", "SUB", "MUL", "DIV", "SCALAR_ADD", "SCALAR_MUL", "MTTKRP_AUTO", "MTTKRP_ATOMIC",
-    "MTTKRP_SEGMENTED", "flops", "ascending_order", "mode_last_order", "ts", "tew_eq", "tew",
-    "ttv", "ttm", "mttkrp", "sort_lexicographic", "coalesce", "build_fiber_index",
+    "MTTKRP_SEGMENTED", "MTTKRP_SEGMENTED_CTA", "MTTKRP_SEGMENTED_WARP", "flops",
+    "ascending_order", "mode_last_order", "ts", "tew_eq", "tew", "ttv", "ttm", "mttkrp", "sort_lexicographic", "coalesce", "build_fiber_index",
 ]
 
 

@@ -63,5 +63,5 @@ def test_cpals_recovers_exact_low_rank_dense_tensor():
     I, J, K = np.meshgrid(*[np.arange(d) for d in dims], indexing="ij")
     x = HostCOO(dims, [I.ravel().astype(np.uint32), J.ravel().astype(np.uint32),
                        K.ravel().astype(np.uint32)], full.ravel(), [0, 1, 2], True).to_device(0)
-    res = cp_als(x, R, iters=200, tol=1e-9, seed=3)
+    res = cp_als(x, R, iters=1000, tol=1e-12, seed=3)
     assert res.fits[-1] > 0.999, res.fits[-5:]

@@ -261,7 +261,8 @@ def test_mttkrp_shapes(sp, R, order):
         _, o64, oab = O.mttkrp(x, fs, mode)
         xs = x.copy()
         O.sort_lexicographic(xs, [mode] + [d for d in range(order) if d != mode])
-        for strat, t in ((ops.MTTKRP_SEGMENTED, xs), (ops.MTTKRP_AUTO, xs), (ops.MTTKRP_ATOMIC, x)):
+        for strat, t in ((ops.MTTKRP_SEGMENTED_CTA, xs), (ops.MTTKRP_SEGMENTED_WARP, xs),
+                         (ops.MTTKRP_AUTO, xs), (ops.MTTKRP_ATOMIC, x)):
             out = ops.mttkrp(dev(sp, t), [torch.from_numpy(f).cuda() for f in fs], mode,
                              strat).cpu().numpy()
             ok, worst = within_tol(out, o64, oab, 1e-5 if strat != ops.MTTKRP_ATOMIC else 1e-4)
@@ -286,10 +287,12 @@ def test_mttkrp_heavy_rows_and_gaps(sp):
     O.sort_lexicographic(x, [0, 1, 2])
     fs = [rng.uniform(0, 1, (d, 32)).astype(np.float32) for d in x.dims]
     _, o64, oab = O.mttkrp(x, fs, 0)
-    out = ops.mttkrp(dev(sp, x), [torch.from_numpy(f).cuda() for f in fs], 0).cpu().numpy()
-    ok, worst = within_tol(out, o64, oab)
-    assert ok, worst
-    assert np.all(out[o64 == 0] == 0)
+    for strat in (ops.MTTKRP_SEGMENTED_CTA, ops.MTTKRP_SEGMENTED_WARP):
+        out = ops.mttkrp(dev(sp, x), [torch.from_numpy(f).cuda() for f in fs], 0,
+                         strat).cpu().numpy()
+        ok, worst = within_tol(out, o64, oab)
+        assert ok, (strat, worst)
+        assert np.all(out[o64 == 0] == 0)
 
 
 @pytest.mark.parametrize("R", [1, 5, 16, 32])
