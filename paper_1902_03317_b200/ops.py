@@ -26,7 +26,8 @@ from .coo import DeviceCOO, FiberIndex, ptr
 __all__ = [
     "ADD", "SUB", "MUL", "DIV", "SCALAR_ADD", "SCALAR_MUL", "MTTKRP_AUTO", "MTTKRP_ATOMIC",
     "MTTKRP_SEGMENTED", "MTTKRP_SEGMENTED_CTA", "MTTKRP_SEGMENTED_WARP", "flops",
-    "ascending_order", "mode_last_order", "ts", "tew_eq", "tew", "ttv", "ttm", "mttkrp", "sort_lexicographic", "coalesce", "build_fiber_index",
+    "ascending_order", "mode_last_order", "check_deferred", "ts", "tew_eq", "tew", "ttv",
+    "ttm", "mttkrp", "sort_lexicographic", "coalesce", "build_fiber_index",
 ]
 
 
@@ -72,6 +73,14 @@ def _stream(dev: torch.device) -> int:
 
 def _flags(sync: bool) -> int:
     return 0 if sync else _lib.SPT_FLAG_ASYNC
+
+
+def check_deferred(device: int | torch.device = 0) -> None:
+    """Raise the first data-dependent error of earlier sync=False calls on this
+    device (synchronises torch's current stream; spt_ctx_check)."""
+    dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+    ctx = _lib.Context.get(dev.index if dev.index is not None else 0)
+    check(_lib.load().spt_ctx_check(ctx.handle, _stream(dev)))
 
 
 # ---------------------------------------------------------------------------

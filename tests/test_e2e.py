@@ -1,0 +1,47 @@
+"""The pipelined host-buffer path bench.py times as `e2e` (pinned uploads in
+chunks, kernels and downloads on separate streams) returns exactly what the
+oracle computes from the same host inputs."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle.oracle import HostTensor, Oracle
+from tests._golden import same
+
+pytestmark = pytest.mark.gpu
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def _ht(h):
+    return HostTensor(list(h.dims), [np.asarray(i, np.uint32).copy() for i in h.indices],
+                      np.asarray(h.values, np.float32).copy(), h.sort_order, h.coalesced)
+
+
+@pytest.mark.parametrize("scale", [0.0005, 0.0123])
+def test_c2_pipelined_e2e_matches_oracle(scale):
+    import bench
+    wl = bench.C2(20190210, 0, scale)
+    host = wl.e2e_host(0)
+    for _ in range(2):  # second pass reuses every buffer
+        for o in host["out_eq"] + host["out_tew"]:
+            o.val.fill_(np.nan)
+            o.nnz = 0
+        h2d, d2h = wl.e2e_step(host, "cuda:0")
+        torch.cuda.synchronize()
+    hx, hy, hy2 = (_ht(h) for h in wl.host_inputs())
+    assert h2d == 3 * wl.nnz * 16
+    O = Oracle()
+    for k, op in enumerate(range(4)):
+        got = host["out_eq"][k].to_host()
+        assert same(_ht(got), O.tew_eq(hx, hy, op)), op
+    n_out = 0
+    for k, op in enumerate((0, 2)):
+        ref, _ = O.tew(hx.copy(), hy2.copy(), op)
+        got = host["out_tew"][k].to_host()
+        assert same(_ht(got), ref), op
+        n_out += ref.nnz
+    assert d2h == (4 * wl.nnz + n_out) * 16
