@@ -147,6 +147,55 @@ __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long l
   return v;
 }
 
+// mbarrier + bulk async copy (TMA engine, non-tensor form): global -> shared
+// runs of 16-byte-aligned bytes, completion counted in the barrier's tx-count.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  unsigned long long state;
+  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];"
+               : "=l"(state)
+               : "r"(smem_addr(bar))
+               : "memory");
+  (void)state;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SPT_MBAR_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra SPT_MBAR_WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+// Named barrier over the first `n` threads (warp multiples) of the CTA.
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // Warp-parallel decoupled look-back over epoch-tagged u32 status words
 // (word = epoch << 3 | flags, flags & 3 == 1: aggregate A, == 2: inclusive P).
 // Called by one full warp for tile `tile` > 0. Polls (never blocks on) the 32
@@ -209,6 +258,76 @@ __device__ __forceinline__ unsigned long long lookback_count64(const unsigned lo
     if (pmask) return acc;
     if (prefix == 32) base += 32;
     else __nanosleep(32);
+  }
+}
+
+// Wide-window lookback_count64: one warp polls 32*W predecessors per round
+// trip (lane L owns tiles tile-1-W*L-k, k < W; all W loads in flight). For
+// persistent kernels where a whole wave of ~#CTAs tiles publishes A at once
+// and the nearest P sits a wave back, this turns ~wave/32 sequential round
+// trips into one or two.
+template <int W>
+__device__ __forceinline__ unsigned long long lookback_count64_wide(
+    const unsigned long long* status, uint32_t tile, uint32_t epoch,
+    uint32_t* stats = nullptr) {  // debug: [polls, distance to the P]
+  // Predecessor at distance 32*k + lane + 1 sits in lane `lane`, slot k, so
+  // each of the W loads is one coalesced 256-byte request.
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned long long acc = 0;
+  uint32_t base = 0;
+  uint32_t polls = 0;
+  while (true) {
+    ++polls;
+    uint32_t cnt[W];
+    unsigned ready[W], isP[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const int64_t j = (int64_t)tile - 1 - base - (int64_t)(32 * k + lane);
+      uint32_t flag = 2;
+      cnt[k] = 0;
+      if (j >= 0) {
+        const unsigned long long w = ld_relaxed64(status + j);
+        flag = ((w >> 34) == epoch) ? (uint32_t)((w >> 32) & 3u) : 0u;
+        cnt[k] = (uint32_t)w;
+      }
+      ready[k] = __ballot_sync(0xffffffffu, flag != 0);
+      isP[k] = __ballot_sync(0xffffffffu, flag == 2);
+    }
+    // walk the sub-windows nearest-first (warp-uniform)
+    int ks = W, ls = 31;  // take sub-windows < ks fully, sub-window ks up to lane ls
+    bool found = false, blocked = false;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      if (found || blocked) continue;
+      const int prefix = (~ready[k]) ? __ffs(~ready[k]) - 1 : 32;
+      const unsigned pm = isP[k] & (prefix == 32 ? 0xffffffffu : ((1u << prefix) - 1u));
+      if (pm) {
+        found = true;
+        ks = k;
+        ls = __ffs(pm) - 1;
+      } else if (prefix < 32) {
+        blocked = true;
+      }
+    }
+    if (blocked) {
+      __nanosleep(32);
+      continue;
+    }
+    unsigned long long v = 0;
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+      v += (k < ks || (k == ks && static_cast<int>(lane) <= ls)) ? cnt[k] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    acc += v;
+    if (found) {
+      if (stats) {
+        stats[0] = polls;
+        stats[1] = base + 32 * ks + ls + 1;
+      }
+      return acc;
+    }
+    base += 32 * W;
   }
 }
 

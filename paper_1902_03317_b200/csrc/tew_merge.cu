@@ -448,6 +448,389 @@ __global__ void __launch_bounds__(kThreads, 4) merge64_kernel(MergeParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent, pipelined, warp-specialised variant of merge64_kernel.
+//
+// A CTA (resident for the whole merge) = 8 merge warps + 1 emitter warp + 1
+// producer warp:
+//   * producer: takes tile tickets in order, reads the tile's merge-path split
+//     and moves the tile's x and y runs (N index arrays + values per side)
+//     into a shared-memory stage with bulk async copies (the TMA engine;
+//     16-byte-aligned body per run, <= 3 scalar head/tail words by lanes);
+//   * merge warps: pack u64 keys from the stage and free it (the producer
+//     refills it with the next tile at once), merge 8 items per thread, block
+//     scan, publish the tile's count (A), and leave the emitted (key, value)
+//     pairs in an emission buffer -- they never wait for other tiles;
+//   * emitter: decoupled look-back for that tile (wide window), publishes its
+//     inclusive count (P), writes the tile's output with coalesced streaming
+//     stores, frees the emission buffer.
+// So load latency hides behind the previous tile's merge, and look-back
+// latency behind the next tile's merge.
+#ifdef SPT_PHASES
+__device__ unsigned long long g_ph[65536 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPT_PH(tile, k) \
+  if ((tile) < 65536) g_ph[(size_t)(tile) * 8 + (k)] = gtime();
+#else
+#define SPT_PH(tile, k)
+#endif
+#ifndef SPT_MERGE_STAGES
+#define SPT_MERGE_STAGES 1
+#endif
+constexpr int kStages = SPT_MERGE_STAGES;
+constexpr int kSeg = kTile + 16;  // words per staged array (x run + y run + alignment slack)
+constexpr uint32_t kDone = 0xFFFFFFFFu;
+constexpr int kPThreads = kThreads + 64;
+// Emission buffers: threads write their emitted items ~8 apart, so pad one
+// slot per 16 (u64 keys) / per 8 (u32 values) to spread those rows over all
+// banks; the emitter reads them back consecutively.
+constexpr int kEK = kTile + kTile / 16;
+constexpr int kEV = kTile + kTile / 8;
+__device__ __forceinline__ int epad64(int o) { return o + (o >> 4); }
+__device__ __forceinline__ int epad(int o) { return o + (o >> 3); }
+
+struct StageInfo {
+  uint32_t tile, nxt, nyt, _pad;
+  uint32_t xoff[SPT_MAX_ORDER + 1], yoff[SPT_MAX_ORDER + 1];
+  unsigned long long x_before, y_after;
+  unsigned long long b0;
+};
+
+// smem: stages [kStages][(N+1) * kSeg] u32 | sk [kTP64] u64 | ek [2][kTile] u64 |
+//       sv [kTP] u32 | ev [2][kTile] u32 | info [kStages] | barriers | scalars
+template <int N>
+constexpr size_t pers_smem() {
+  return (size_t)kStages * (N + 1) * kSeg * 4 + (size_t)kTP64 * 8 + (size_t)2 * kEK * 8 +
+         (size_t)kTP * 4 + (size_t)2 * kEV * 4 + kStages * sizeof(StageInfo) +
+         (2 * kStages + 4) * 8 + 16 * 8;
+}
+
+// One run [e0, e0+n) of array `src` into stage words starting at `dst`, where
+// dst and src+e0 share their 16-byte phase: scalar head/tail, bulk body.
+__device__ __forceinline__ void copy_run(uint32_t* dst, const uint32_t* src, uint64_t e0,
+                                         uint32_t n, uint32_t head, uint32_t body,
+                                         unsigned long long* bar) {
+  for (uint32_t k = 0; k < head; ++k) dst[k] = __ldg(src + e0 + k);
+  for (uint32_t k = head + body; k < n; ++k) dst[k] = __ldg(src + e0 + k);
+  if (body) spt::bulk_g2s(dst + head, src + e0 + head, body * 4, bar);
+}
+
+__device__ __forceinline__ uint32_t word_phase(const uint32_t* p) {
+  return (static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p)) >> 2) & 3u;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint32_t nctas) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint32_t* stages = reinterpret_cast<uint32_t*>(smem_raw);
+  unsigned long long* sk =
+      reinterpret_cast<unsigned long long*>(stages + (size_t)kStages * (N + 1) * kSeg);
+  unsigned long long* ek0 = sk + kTP64;  // [2][kEK] emission buffers
+  uint32_t* sv = reinterpret_cast<uint32_t*>(ek0 + 2 * kEK);
+  uint32_t* ev0 = sv + kTP;  // [2][kEV]
+  StageInfo* info = reinterpret_cast<StageInfo*>(ev0 + 2 * kEV);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(info + kStages);
+  unsigned long long* empty = full + kStages;
+  unsigned long long* efull = empty + kStages;  // [2]
+  unsigned long long* eempty = efull + 2;       // [2]
+  uint32_t* s_wsum = reinterpret_cast<uint32_t*>(eempty + 2);  // [8], (tile, total) x 2
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      spt::mbar_init(full + s, 32);
+      spt::mbar_init(empty + s, kThreads / 32);
+    }
+    for (int b = 0; b < 2; ++b) {
+      spt::mbar_init(efull + b, kThreads);
+      spt::mbar_init(eempty + b, 32);
+    }
+    spt::mbar_fence_init();
+  }
+  __syncthreads();
+  const uint64_t total = p.nx + p.ny;
+  const unsigned lane = tid & 31u;
+  const unsigned long long tag = (unsigned long long)p.epoch << 34;
+
+  if (tid >= kThreads + 32) {
+    // ---- producer warp ----
+    for (uint32_t it = 0;; ++it) {
+      const int s = it % kStages;
+      unsigned long long t = 0;
+      if (lane == 0) {
+        t = atomicAdd(p.tile_ctr, 1ull);
+        if (t == (unsigned long long)p.ntiles + nctas - 1) atomicExch(p.tile_ctr, 0ull);
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      uint64_t a0 = 0, a1 = 0;
+      if (t < p.ntiles) {
+        a0 = p.split[t];
+        a1 = p.split[t + 1];
+      }
+      if (it >= kStages) spt::mbar_wait(empty + s, ((it / kStages) - 1) & 1u);
+      StageInfo& inf = info[s];
+      if (t >= p.ntiles) {
+        if (lane == 0) inf.tile = kDone;
+        __syncwarp();
+        spt::mbar_arrive(full + s);
+        break;
+      }
+      const uint64_t d0 = t * (uint64_t)kTile;
+      const uint64_t d1 = std::min<uint64_t>(d0 + kTile, total);
+      const uint64_t b0 = d0 - a0, b1 = d1 - a1;
+      const uint32_t nxt = static_cast<uint32_t>(a1 - a0), nyt = static_cast<uint32_t>(b1 - b0);
+      // lane q <= N: x run of array q (q == N: values); lane 16+q: y run.
+      const bool is_y = lane >= 16;
+      const uint32_t q = lane & 15u;
+      if (q <= static_cast<uint32_t>(N)) {
+        const uint32_t* xs =
+            q < static_cast<uint32_t>(N) ? p.xi[q] : reinterpret_cast<const uint32_t*>(p.xv);
+        const uint32_t* ys =
+            q < static_cast<uint32_t>(N) ? p.yi[q] : reinterpret_cast<const uint32_t*>(p.yv);
+        const uint32_t* src = is_y ? ys : xs;
+        const uint64_t e0 = is_y ? b0 : a0;
+        const uint32_t n = is_y ? nyt : nxt;
+        // x run at word xp (the 16-byte phase of xs+a0); y run after it, in
+        // its own phase.
+        const uint32_t xp = word_phase(xs + a0);
+        const uint32_t off = is_y ? ((xp + nxt + 3u) & ~3u) + word_phase(ys + b0) : xp;
+        if (is_y) inf.yoff[q] = off;
+        else inf.xoff[q] = off;
+        const uint32_t head = std::min<uint32_t>(n, (4u - word_phase(src + e0)) & 3u);
+        const uint32_t body = (n - head) & ~3u;
+        // announce this lane's bytes before its copy can complete
+        if (body) spt::mbar_expect_tx(full + s, body * 4);
+        copy_run(stages + ((size_t)s * (N + 1) + q) * kSeg + off, src, e0, n, head, body,
+                 full + s);
+      }
+      if (lane == 31) {
+        inf.tile = static_cast<uint32_t>(t);
+        inf.nxt = nxt;
+        inf.nyt = nyt;
+        inf.b0 = b0;
+        inf.y_after = (b1 < p.ny) ? pack_g<N>(p.yi, p, b1) : ~0ull;
+        inf.x_before = (a0 > 0) ? pack_g<N>(p.xi, p, a0 - 1) : ~0ull;
+      }
+      spt::mbar_arrive(full + s);
+    }
+    return;
+  }
+
+  if (tid >= kThreads) {
+    // ---- emitter warp: look-back + output ----
+    for (uint32_t it = 0;; ++it) {
+      const int b = it & 1;
+      spt::mbar_wait(efull + b, (it >> 1) & 1u);
+      const uint32_t tile = s_wsum[8 + 2 * b], tile_total = s_wsum[9 + 2 * b];
+      if (tile == kDone) break;
+      const unsigned long long* ek = ek0 + b * kEK;
+      const uint32_t* ev = ev0 + b * kEV;
+      unsigned long long base = 0;
+#ifdef SPT_PHASES
+      if (lane == 0 && tile < 65536) g_ph[(size_t)tile * 8 + 0] = gtime();
+#endif
+      if (tile != 0) {
+#ifdef SPT_PHASES
+        uint32_t stats[2];
+        base = spt::lookback_count64_wide<8>(p.status, tile, p.epoch, stats);
+        if (lane == 0 && tile < 65536)
+          g_ph[(size_t)tile * 8 + 6] = ((unsigned long long)stats[0] << 32) | stats[1];
+#else
+        base = spt::lookback_count64_wide<8>(p.status, tile, p.epoch);
+#endif
+        if (lane == 0)
+          spt::st_relaxed64(p.status + tile, tag | (kFlagP << 32) | (base + tile_total));
+      }
+      if (lane == 0 && tile == p.ntiles - 1) *p.total = base + tile_total;
+#ifdef SPT_PHASES
+      if (lane == 0) SPT_PH(tile, 4);
+#endif
+      for (uint32_t o = lane; o < tile_total; o += 32) {
+        const unsigned long long k = ek[epad64(o)];
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+          spt::st_stream(p.zi[q] + base + o, (uint32_t)((k >> p.shift[q]) & p.mask[q]));
+        spt::st_stream(reinterpret_cast<uint32_t*>(p.zv) + base + o, ev[epad(o)]);
+      }
+#ifdef SPT_PHASES
+      if (lane == 0) SPT_PH(tile, 5);
+#endif
+      spt::mbar_arrive(eempty + b);
+    }
+    return;
+  }
+
+  // ---- merge warps ----
+  using spt::bar_sync;
+  const int warp = tid >> 5;
+  for (uint32_t it = 0;; ++it) {
+    const int s = it % kStages;
+#ifdef SPT_PHASES
+    const unsigned long long t_w0 = gtime();
+#endif
+    spt::mbar_wait(full + s, (it / kStages) & 1u);
+    const StageInfo& inf = info[s];
+    const uint32_t tile = inf.tile;
+    const int eb = it & 1;
+    if (tile == kDone) {
+      if (it >= 2) spt::mbar_wait(eempty + eb, ((it >> 1) - 1) & 1u);
+      if (tid == 0) s_wsum[8 + 2 * eb] = kDone;
+      spt::mbar_arrive(efull + eb);
+      break;
+    }
+#ifdef SPT_PHASES
+    if (tid == 0 && tile < 65536) {
+      (void)t_w0;
+      g_ph[(size_t)tile * 8 + 7] = blockIdx.x;
+      SPT_PH(tile, 1);
+    }
+#endif
+    const int nxt = static_cast<int>(inf.nxt), nyt = static_cast<int>(inf.nyt);
+    const unsigned long long x_before = inf.x_before, y_after = inf.y_after;
+    const uint64_t b0 = inf.b0;
+    const int len = nxt + nyt;
+    {
+      const uint32_t* st0 = stages + (size_t)s * (N + 1) * kSeg;
+      uint32_t xo[N + 1], yo[N + 1];
+#pragma unroll
+      for (int q = 0; q <= N; ++q) {
+        xo[q] = inf.xoff[q];
+        yo[q] = inf.yoff[q] - nxt;  // y entry j sits at word yoff + j = (yoff - nxt) + i
+      }
+      for (int i = tid; i < len; i += kThreads) {
+        const bool isx = i < nxt;
+        unsigned long long k = 0;
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+          k |= (unsigned long long)st0[q * kSeg + (isx ? xo[q] : yo[q]) + i] << p.shift[q];
+        sk[pad64(i)] = k;
+        sv[pad(i)] = st0[N * kSeg + (isx ? xo[N] : yo[N]) + i];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) spt::mbar_arrive(empty + s);  // this warp is done with the stage
+    bar_sync(1, kThreads);
+#ifdef SPT_PHASES
+    if (tid == 0) SPT_PH(tile, 2);
+#endif
+
+    // x entry i at key index i, y entry j at key index nxt + j
+    const int dg = std::min(tid * kIPT, len);
+    int lo = std::max(0, dg - nyt), hi = std::min(dg, nxt);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sk[pad64(mid)] <= sk[pad64(nxt + dg - 1 - mid)]) lo = mid + 1;
+      else hi = mid;
+    }
+    int i = lo, j = dg - lo;
+    unsigned long long kx = i < nxt ? sk[pad64(i)] : ~0ull;
+    unsigned long long ky = j < nyt ? sk[pad64(nxt + j)] : ~0ull;
+    unsigned long long key[kIPT];
+    uint32_t vbits[kIPT];
+    bool emit[kIPT];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kIPT; ++k) {
+      emit[k] = false;
+      key[k] = 0;
+      vbits[k] = 0;
+      if (dg + k >= len) continue;
+      const bool take_x = j >= nyt || (i < nxt && kx <= ky);
+      if (take_x) {
+        const unsigned long long ny_key = j < nyt ? ky : y_after;  // next y in merge order
+        const bool m = kx == ny_key;
+        float v = __uint_as_float(sv[pad(i)]);
+        if (m)
+          v = apply(p.op, v,
+                    j < nyt ? __uint_as_float(sv[pad(nxt + j)]) : __ldg(p.yv + b0 + j));
+        emit[k] = (p.op != SPT_MUL) || m;
+        key[k] = kx;
+        vbits[k] = __float_as_uint(v);
+        ++i;
+        kx = i < nxt ? sk[pad64(i)] : ~0ull;
+      } else {
+        const unsigned long long px = i > 0 ? sk[pad64(i - 1)] : x_before;  // previous x
+        const bool m = px == ky;
+        const float yv = __uint_as_float(sv[pad(nxt + j)]);
+        emit[k] = (p.op != SPT_MUL) && !m;
+        key[k] = ky;
+        vbits[k] = __float_as_uint(p.op == SPT_SUB ? -yv : yv);
+        ++j;
+        ky = j < nyt ? sk[pad64(nxt + j)] : ~0ull;
+      }
+      cnt += emit[k] ? 1u : 0u;
+    }
+    // block exclusive scan of cnt over the 256 merge threads
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= static_cast<unsigned>(o)) incl += v;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    bar_sync(1, kThreads);
+    uint32_t wpre = 0, tile_total = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const uint32_t v = s_wsum[w];
+      wpre += w < warp ? v : 0u;
+      tile_total += v;
+    }
+    const uint32_t excl = wpre + incl - cnt;
+    if (tid == 0)
+      spt::st_relaxed64(p.status + tile,
+                        tag | ((tile == 0 ? kFlagP : kFlagA) << 32) | tile_total);
+#ifdef SPT_PHASES
+    if (tid == 0) SPT_PH(tile, 3);
+#endif
+    // emitter done with the tile that last used this buffer
+    if (it >= 2) spt::mbar_wait(eempty + eb, ((it >> 1) - 1) & 1u);
+    {
+      unsigned long long* ek = ek0 + eb * kEK;
+      uint32_t* ev = ev0 + eb * kEV;
+      int lp = static_cast<int>(excl);
+#pragma unroll
+      for (int k = 0; k < kIPT; ++k) {
+        if (!emit[k]) continue;
+        ek[epad64(lp)] = key[k];
+        ev[epad(lp)] = vbits[k];
+        ++lp;
+      }
+    }
+    if (tid == 0) {
+      s_wsum[8 + 2 * eb] = tile;
+      s_wsum[9 + 2 * eb] = tile_total;
+    }
+    // s_wsum[0..7] are rewritten only after the next pack barrier, which every
+    // thread reaches after its reads above.
+    spt::mbar_arrive(efull + eb);
+  }
+}
+
+template <int N>
+int launch64p(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
+  const uint32_t nt = p.ntiles;
+  partition_kernel<N><<<(nt + 1 + 7) / 8, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
+  SPT_LAUNCHED(ctx);
+  constexpr size_t smem = pers_smem<N>();
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    SPT_CUDA(cudaFuncSetAttribute(merge64p_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge64p_kernel<N>, kPThreads,
+                                                           smem));
+    per_sm = std::max(per_sm, 1);
+  }
+  const uint32_t nctas = std::min<uint32_t>(nt, (uint32_t)(per_sm * ctx->num_sms));
+  merge64p_kernel<N><<<nctas, kPThreads, smem, st>>>(p, nctas);
+  SPT_LAUNCHED(ctx);
+  return SPT_OK;
+}
+
 template <int N>
 int launch64(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
   const uint32_t nt = p.ntiles;
@@ -475,6 +858,12 @@ int launch(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
 }
 
 }  // namespace
+
+#ifdef SPT_PHASES
+extern "C" SPT_API int spt_debug_phases(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_ph, std::min(bytes, sizeof(g_ph))) == cudaSuccess ? 0 : 5;
+}
+#endif
 
 extern "C" int spt_tew_f32(spt_ctx* ctx, const spt_coo* x, const spt_coo* y, int op, spt_coo* z,
                            uint64_t z_capacity, uint64_t* h_nnz, uint64_t* d_nnz, unsigned flags,
@@ -567,14 +956,14 @@ extern "C" int spt_tew_f32(spt_ctx* ctx, const spt_coo* x, const spt_coo* y, int
         sh += width[k];
       }
       switch (N) {
-        case 1: SPT_TRY(launch64<1>(ctx, p, st)); break;
-        case 2: SPT_TRY(launch64<2>(ctx, p, st)); break;
-        case 3: SPT_TRY(launch64<3>(ctx, p, st)); break;
-        case 4: SPT_TRY(launch64<4>(ctx, p, st)); break;
-        case 5: SPT_TRY(launch64<5>(ctx, p, st)); break;
-        case 6: SPT_TRY(launch64<6>(ctx, p, st)); break;
-        case 7: SPT_TRY(launch64<7>(ctx, p, st)); break;
-        default: SPT_TRY(launch64<8>(ctx, p, st)); break;
+        case 1: SPT_TRY(launch64p<1>(ctx, p, st)); break;
+        case 2: SPT_TRY(launch64p<2>(ctx, p, st)); break;
+        case 3: SPT_TRY(launch64p<3>(ctx, p, st)); break;
+        case 4: SPT_TRY(launch64p<4>(ctx, p, st)); break;
+        case 5: SPT_TRY(launch64p<5>(ctx, p, st)); break;
+        case 6: SPT_TRY(launch64p<6>(ctx, p, st)); break;
+        case 7: SPT_TRY(launch64p<7>(ctx, p, st)); break;
+        default: SPT_TRY(launch64p<8>(ctx, p, st)); break;
       }
     } else switch (N) {
       case 1: SPT_TRY(launch<1>(ctx, p, st)); break;
