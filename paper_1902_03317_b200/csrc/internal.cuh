@@ -266,7 +266,7 @@ __device__ __forceinline__ unsigned long long lookback_count64(const unsigned lo
 // persistent kernels where a whole wave of ~#CTAs tiles publishes A at once
 // and the nearest P sits a wave back, this turns ~wave/32 sequential round
 // trips into one or two.
-template <int W>
+template <int W, int SH = 0>
 __device__ __forceinline__ unsigned long long lookback_count64_wide(
     const unsigned long long* status, uint32_t tile, uint32_t epoch,
     uint32_t* stats = nullptr) {  // debug: [polls, distance to the P]
@@ -278,21 +278,25 @@ __device__ __forceinline__ unsigned long long lookback_count64_wide(
   uint32_t polls = 0;
   while (true) {
     ++polls;
+    const long long c0 = clock64();
     uint32_t cnt[W];
     unsigned ready[W], isP[W];
+    unsigned long long w[W];
+    // all W loads in flight before the first use (the asm is volatile, so
+    // they must be issued ahead of the ballots explicitly)
 #pragma unroll
     for (int k = 0; k < W; ++k) {
       const int64_t j = (int64_t)tile - 1 - base - (int64_t)(32 * k + lane);
-      uint32_t flag = 2;
-      cnt[k] = 0;
-      if (j >= 0) {
-        const unsigned long long w = ld_relaxed64(status + j);
-        flag = ((w >> 34) == epoch) ? (uint32_t)((w >> 32) & 3u) : 0u;
-        cnt[k] = (uint32_t)w;
-      }
+      w[k] = j >= 0 ? ld_relaxed64(status + (j << SH)) : ((unsigned long long)epoch << 34) | (2ull << 32);
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const uint32_t flag = ((w[k] >> 34) == epoch) ? (uint32_t)((w[k] >> 32) & 3u) : 0u;
+      cnt[k] = (uint32_t)w[k];
       ready[k] = __ballot_sync(0xffffffffu, flag != 0);
       isP[k] = __ballot_sync(0xffffffffu, flag == 2);
     }
+    if (stats && polls == 1) stats[2] = (uint32_t)(clock64() - c0);
     // walk the sub-windows nearest-first (warp-uniform)
     int ks = W, ls = 31;  // take sub-windows < ks fully, sub-window ks up to lane ls
     bool found = false, blocked = false;

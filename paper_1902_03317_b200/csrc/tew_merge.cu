@@ -482,9 +482,14 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define SPT_MERGE_STAGES 1
 #endif
 constexpr int kStages = SPT_MERGE_STAGES;
+#ifndef SPT_STATUS_SHIFT
+#define SPT_STATUS_SHIFT 2
+#endif
+constexpr int kSS = SPT_STATUS_SHIFT;  // status word of tile t at t << kSS
 constexpr int kSeg = kTile + 16;  // words per staged array (x run + y run + alignment slack)
 constexpr uint32_t kDone = 0xFFFFFFFFu;
-constexpr int kPThreads = kThreads + 64;
+constexpr int kPThreads = kThreads + 96;  // + look-back, emitter, producer warps
+constexpr int kSlots = 4;                   // tile hand-off ring (merge -> look-back -> emitter)
 // Emission buffers: threads write their emitted items ~8 apart, so pad one
 // slot per 16 (u64 keys) / per 8 (u32 values) to spread those rows over all
 // banks; the emitter reads them back consecutively.
@@ -498,15 +503,22 @@ struct StageInfo {
   uint32_t xoff[SPT_MAX_ORDER + 1], yoff[SPT_MAX_ORDER + 1];
   unsigned long long x_before, y_after;
   unsigned long long b0;
+  uint32_t yv_after, _pad2;  // value of the first y after the tile (matches across the edge)
 };
 
-// smem: stages [kStages][(N+1) * kSeg] u32 | sk [kTP64] u64 | ek [2][kTile] u64 |
-//       sv [kTP] u32 | ev [2][kTile] u32 | info [kStages] | barriers | scalars
+// Packed tile in shared memory: x keys at key slots [0, nxt), a sentinel slot
+// at nxt, y keys at [nxt+1, nxt+1+nyt), a sentinel slot after them whose value
+// is the first y after the tile. Clamped head reads land on the sentinels, so
+// the merge loop has no bounds branches.
+constexpr int kSK = (kTile + 2 + (kTile + 2) / 16 + 4) & ~3;  // >= pad64(kTile + 1) + 1
+constexpr int kSV = (kTile + 2 + (kTile + 2) / 32 + 8) & ~3;  // >= pad(kTile + 2) + 1, 16B multiple
+// smem: stages [kStages][(N+1) * kSeg] u32 | sk [kSK] u64 | ek [2][kEK] u64 |
+//       sv [kSV] u32 | ev [2][kEV] u32 | info [kStages] | barriers | scalars
 template <int N>
 constexpr size_t pers_smem() {
-  return (size_t)kStages * (N + 1) * kSeg * 4 + (size_t)kTP64 * 8 + (size_t)2 * kEK * 8 +
-         (size_t)kTP * 4 + (size_t)2 * kEV * 4 + kStages * sizeof(StageInfo) +
-         (2 * kStages + 4) * 8 + 16 * 8;
+  return (size_t)kStages * (N + 1) * kSeg * 4 + (size_t)kSK * 8 + (size_t)2 * kEK * 8 +
+         (size_t)kSV * 4 + (size_t)2 * kEV * 4 + kStages * sizeof(StageInfo) +
+         (2 * kStages + 4 + 3 * kSlots) * 8 + kSlots * 16 + 16 * 8;
 }
 
 // One run [e0, e0+n) of array `src` into stage words starting at `dst`, where
@@ -523,21 +535,29 @@ __device__ __forceinline__ uint32_t word_phase(const uint32_t* p) {
   return (static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p)) >> 2) & 3u;
 }
 
-template <int N>
+template <int N, int OP>
 __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint32_t nctas) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint32_t* stages = reinterpret_cast<uint32_t*>(smem_raw);
   unsigned long long* sk =
       reinterpret_cast<unsigned long long*>(stages + (size_t)kStages * (N + 1) * kSeg);
-  unsigned long long* ek0 = sk + kTP64;  // [2][kEK] emission buffers
+  unsigned long long* ek0 = sk + kSK;  // [2][kEK] emission buffers
   uint32_t* sv = reinterpret_cast<uint32_t*>(ek0 + 2 * kEK);
-  uint32_t* ev0 = sv + kTP;  // [2][kEV]
+  uint32_t* ev0 = sv + kSV;  // [2][kEV]
   StageInfo* info = reinterpret_cast<StageInfo*>(ev0 + 2 * kEV);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(info + kStages);
   unsigned long long* empty = full + kStages;
   unsigned long long* efull = empty + kStages;  // [2]
   unsigned long long* eempty = efull + 2;       // [2]
-  uint32_t* s_wsum = reinterpret_cast<uint32_t*>(eempty + 2);  // [8], (tile, total) x 2
+  unsigned long long* lbfull = eempty + 2;      // [kSlots] merge -> look-back
+  unsigned long long* bfull = lbfull + kSlots;  // [kSlots] look-back -> emitter
+  unsigned long long* sempty = bfull + kSlots;  // [kSlots] emitter -> merge
+  struct Slot {
+    uint32_t tile, total;
+    unsigned long long base;
+  };
+  Slot* slot = reinterpret_cast<Slot*>(sempty + kSlots);
+  uint32_t* s_wsum = reinterpret_cast<uint32_t*>(slot + kSlots);  // [8]
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -549,6 +569,11 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
       spt::mbar_init(efull + b, kThreads);
       spt::mbar_init(eempty + b, 32);
     }
+    for (int r = 0; r < kSlots; ++r) {
+      spt::mbar_init(lbfull + r, 1);
+      spt::mbar_init(bfull + r, 1);
+      spt::mbar_init(sempty + r, 1);
+    }
     spt::mbar_fence_init();
   }
   __syncthreads();
@@ -556,7 +581,7 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
   const unsigned lane = tid & 31u;
   const unsigned long long tag = (unsigned long long)p.epoch << 34;
 
-  if (tid >= kThreads + 32) {
+  if (tid >= kThreads + 64) {
     // ---- producer warp ----
     for (uint32_t it = 0;; ++it) {
       const int s = it % kStages;
@@ -614,41 +639,26 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
         inf.b0 = b0;
         inf.y_after = (b1 < p.ny) ? pack_g<N>(p.yi, p, b1) : ~0ull;
         inf.x_before = (a0 > 0) ? pack_g<N>(p.xi, p, a0 - 1) : ~0ull;
+        inf.yv_after = (b1 < p.ny) ? __float_as_uint(__ldg(p.yv + b1)) : 0u;
       }
       spt::mbar_arrive(full + s);
     }
     return;
   }
 
-  if (tid >= kThreads) {
-    // ---- emitter warp: look-back + output ----
+  if (tid >= kThreads + 32) {
+    // ---- emitter warp: coalesced output of each tile at its base ----
     for (uint32_t it = 0;; ++it) {
-      const int b = it & 1;
-      spt::mbar_wait(efull + b, (it >> 1) & 1u);
-      const uint32_t tile = s_wsum[8 + 2 * b], tile_total = s_wsum[9 + 2 * b];
+      const int r = it % kSlots, b = it & 1;
+      spt::mbar_wait(bfull + r, (it / kSlots) & 1u);
+      const uint32_t tile = slot[r].tile, tile_total = slot[r].total;
+      const unsigned long long base = slot[r].base;
+      __syncwarp();
+      if (lane == 0) spt::mbar_arrive(sempty + r);
       if (tile == kDone) break;
+      spt::mbar_wait(efull + b, (it >> 1) & 1u);
       const unsigned long long* ek = ek0 + b * kEK;
       const uint32_t* ev = ev0 + b * kEV;
-      unsigned long long base = 0;
-#ifdef SPT_PHASES
-      if (lane == 0 && tile < 65536) g_ph[(size_t)tile * 8 + 0] = gtime();
-#endif
-      if (tile != 0) {
-#ifdef SPT_PHASES
-        uint32_t stats[2];
-        base = spt::lookback_count64_wide<8>(p.status, tile, p.epoch, stats);
-        if (lane == 0 && tile < 65536)
-          g_ph[(size_t)tile * 8 + 6] = ((unsigned long long)stats[0] << 32) | stats[1];
-#else
-        base = spt::lookback_count64_wide<8>(p.status, tile, p.epoch);
-#endif
-        if (lane == 0)
-          spt::st_relaxed64(p.status + tile, tag | (kFlagP << 32) | (base + tile_total));
-      }
-      if (lane == 0 && tile == p.ntiles - 1) *p.total = base + tile_total;
-#ifdef SPT_PHASES
-      if (lane == 0) SPT_PH(tile, 4);
-#endif
       for (uint32_t o = lane; o < tile_total; o += 32) {
         const unsigned long long k = ek[epad64(o)];
 #pragma unroll
@@ -664,6 +674,44 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
     return;
   }
 
+  if (tid >= kThreads) {
+    // ---- look-back warp: exclusive output offset of each tile, publish P ----
+    for (uint32_t it = 0;; ++it) {
+      const int r = it % kSlots;
+      spt::mbar_wait(lbfull + r, (it / kSlots) & 1u);
+      const uint32_t tile = slot[r].tile, tile_total = slot[r].total;
+      unsigned long long base = 0;
+      if (tile != kDone) {
+#ifdef SPT_PHASES
+        if (lane == 0 && tile < 65536) g_ph[(size_t)tile * 8 + 0] = gtime();
+#endif
+        if (tile != 0) {
+#ifdef SPT_PHASES
+          uint32_t stats[3];
+          base = spt::lookback_count64_wide<8, kSS>(p.status, tile, p.epoch, stats);
+          if (lane == 0 && tile < 65536)
+            g_ph[(size_t)tile * 8 + 6] = ((unsigned long long)stats[0] << 32) | stats[2];
+#else
+          base = spt::lookback_count64_wide<8, kSS>(p.status, tile, p.epoch);
+#endif
+          if (lane == 0)
+            spt::st_relaxed64(p.status + ((size_t)tile << kSS),
+                              tag | (kFlagP << 32) | (base + tile_total));
+        }
+        if (lane == 0 && tile == p.ntiles - 1) *p.total = base + tile_total;
+#ifdef SPT_PHASES
+        if (lane == 0) SPT_PH(tile, 4);
+#endif
+      }
+      if (lane == 0) {
+        slot[r].base = base;
+        spt::mbar_arrive(bfull + r);
+      }
+      if (tile == kDone) break;
+    }
+    return;
+  }
+
   // ---- merge warps ----
   using spt::bar_sync;
   const int warp = tid >> 5;
@@ -675,11 +723,13 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
     spt::mbar_wait(full + s, (it / kStages) & 1u);
     const StageInfo& inf = info[s];
     const uint32_t tile = inf.tile;
-    const int eb = it & 1;
+    const int eb = it & 1, r = it % kSlots;
     if (tile == kDone) {
-      if (it >= 2) spt::mbar_wait(eempty + eb, ((it >> 1) - 1) & 1u);
-      if (tid == 0) s_wsum[8 + 2 * eb] = kDone;
-      spt::mbar_arrive(efull + eb);
+      if (tid == 0) {
+        if (it >= kSlots) spt::mbar_wait(sempty + r, ((it / kSlots) - 1) & 1u);
+        slot[r].tile = kDone;
+        spt::mbar_arrive(lbfull + r);
+      }
       break;
     }
 #ifdef SPT_PHASES
@@ -691,8 +741,8 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
 #endif
     const int nxt = static_cast<int>(inf.nxt), nyt = static_cast<int>(inf.nyt);
     const unsigned long long x_before = inf.x_before, y_after = inf.y_after;
-    const uint64_t b0 = inf.b0;
     const int len = nxt + nyt;
+    const int Y0 = nxt + 1;  // key slot of y entry 0
     {
       const uint32_t* st0 = stages + (size_t)s * (N + 1) * kSeg;
       uint32_t xo[N + 1], yo[N + 1];
@@ -707,8 +757,14 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
 #pragma unroll
         for (int q = 0; q < N; ++q)
           k |= (unsigned long long)st0[q * kSeg + (isx ? xo[q] : yo[q]) + i] << p.shift[q];
-        sk[pad64(i)] = k;
-        sv[pad(i)] = st0[N * kSeg + (isx ? xo[N] : yo[N]) + i];
+        const int slot_i = isx ? i : i + 1;
+        sk[pad64(slot_i)] = k;
+        sv[pad(slot_i)] = st0[N * kSeg + (isx ? xo[N] : yo[N]) + i];
+      }
+      if (tid == 0) {
+        sk[pad64(nxt)] = ~0ull;
+        sk[pad64(Y0 + nyt)] = ~0ull;
+        sv[pad(Y0 + nyt)] = inf.yv_after;
       }
     }
     __syncwarp();
@@ -718,52 +774,50 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
     if (tid == 0) SPT_PH(tile, 2);
 #endif
 
-    // x entry i at key index i, y entry j at key index nxt + j
     const int dg = std::min(tid * kIPT, len);
     int lo = std::max(0, dg - nyt), hi = std::min(dg, nxt);
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (sk[pad64(mid)] <= sk[pad64(nxt + dg - 1 - mid)]) lo = mid + 1;
+      if (sk[pad64(mid)] <= sk[pad64(Y0 + dg - 1 - mid)]) lo = mid + 1;
       else hi = mid;
     }
+    // Branch-free serial merge: per item one key load (the new head of the
+    // side just consumed, clamped onto the sentinels) and one value load; the
+    // previous x and the next y that decide matches ride in registers.
     int i = lo, j = dg - lo;
-    unsigned long long kx = i < nxt ? sk[pad64(i)] : ~0ull;
-    unsigned long long ky = j < nyt ? sk[pad64(nxt + j)] : ~0ull;
+    unsigned long long kx = sk[pad64(i)];
+    unsigned long long ky = sk[pad64(Y0 + j)];
+    unsigned long long px = i > 0 ? sk[pad64(i - 1)] : x_before;  // last x before item
     unsigned long long key[kIPT];
     uint32_t vbits[kIPT];
-    bool emit[kIPT];
-    uint32_t cnt = 0;
+    uint32_t emitm = 0;
 #pragma unroll
     for (int k = 0; k < kIPT; ++k) {
-      emit[k] = false;
-      key[k] = 0;
-      vbits[k] = 0;
-      if (dg + k >= len) continue;
-      const bool take_x = j >= nyt || (i < nxt && kx <= ky);
-      if (take_x) {
-        const unsigned long long ny_key = j < nyt ? ky : y_after;  // next y in merge order
-        const bool m = kx == ny_key;
-        float v = __uint_as_float(sv[pad(i)]);
-        if (m)
-          v = apply(p.op, v,
-                    j < nyt ? __uint_as_float(sv[pad(nxt + j)]) : __ldg(p.yv + b0 + j));
-        emit[k] = (p.op != SPT_MUL) || m;
-        key[k] = kx;
-        vbits[k] = __float_as_uint(v);
-        ++i;
-        kx = i < nxt ? sk[pad64(i)] : ~0ull;
-      } else {
-        const unsigned long long px = i > 0 ? sk[pad64(i - 1)] : x_before;  // previous x
-        const bool m = px == ky;
-        const float yv = __uint_as_float(sv[pad(nxt + j)]);
-        emit[k] = (p.op != SPT_MUL) && !m;
-        key[k] = ky;
-        vbits[k] = __float_as_uint(p.op == SPT_SUB ? -yv : yv);
-        ++j;
-        ky = j < nyt ? sk[pad64(nxt + j)] : ~0ull;
+      const bool valid = dg + k < len;
+      const bool xin = i < nxt, yin = j < nyt;
+      const bool take_x = xin && (!yin || kx <= ky);
+      const bool mx = kx == (yin ? ky : y_after);  // x matched by the following y
+      const bool my = px == ky;                    // y matched by the preceding x
+      float v = __uint_as_float(sv[take_x ? pad(i) : pad(Y0 + j)]);
+      if (take_x && mx) {
+        // the y head's value; past the run, the sentinel slot holds the next y's
+        const float w = __uint_as_float(sv[pad(Y0 + j)]);
+        v = OP == SPT_ADD ? v + w : (OP == SPT_SUB ? v - w : v * w);
       }
-      cnt += emit[k] ? 1u : 0u;
+      if (OP == SPT_SUB && !take_x) v = -v;
+      const bool e = valid && (take_x ? (OP != SPT_MUL || mx) : (OP != SPT_MUL && !my));
+      emitm |= e ? (1u << k) : 0u;
+      key[k] = take_x ? kx : ky;
+      vbits[k] = __float_as_uint(v);
+      px = take_x ? kx : px;
+      i += take_x ? 1 : 0;
+      j += take_x ? 0 : 1;
+      const unsigned long long nk =
+          sk[take_x ? pad64(min(i, nxt)) : pad64(Y0 + min(j, nyt))];
+      kx = take_x ? nk : kx;
+      ky = take_x ? ky : nk;
     }
+    const uint32_t cnt = __popc(emitm);
     // block exclusive scan of cnt over the 256 merge threads
     uint32_t incl = cnt;
 #pragma unroll
@@ -781,9 +835,16 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
       tile_total += v;
     }
     const uint32_t excl = wpre + incl - cnt;
-    if (tid == 0)
-      spt::st_relaxed64(p.status + tile,
+    if (tid == 0) {
+      spt::st_relaxed64(p.status + ((size_t)tile << kSS),
                         tag | ((tile == 0 ? kFlagP : kFlagA) << 32) | tile_total);
+      // hand the tile to the look-back warp at once (before the emission
+      // buffer is free), so its look-back overlaps everything after
+      if (it >= kSlots) spt::mbar_wait(sempty + r, ((it / kSlots) - 1) & 1u);
+      slot[r].tile = tile;
+      slot[r].total = tile_total;
+      spt::mbar_arrive(lbfull + r);
+    }
 #ifdef SPT_PHASES
     if (tid == 0) SPT_PH(tile, 3);
 #endif
@@ -795,15 +856,11 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
       int lp = static_cast<int>(excl);
 #pragma unroll
       for (int k = 0; k < kIPT; ++k) {
-        if (!emit[k]) continue;
+        if (!((emitm >> k) & 1u)) continue;
         ek[epad64(lp)] = key[k];
         ev[epad(lp)] = vbits[k];
         ++lp;
       }
-    }
-    if (tid == 0) {
-      s_wsum[8 + 2 * eb] = tile;
-      s_wsum[9 + 2 * eb] = tile_total;
     }
     // s_wsum[0..7] are rewritten only after the next pack barrier, which every
     // thread reaches after its reads above.
@@ -811,24 +868,34 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
   }
 }
 
+template <int N, int OP>
+int launch64p_op(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
+  constexpr size_t smem = pers_smem<N>();
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    SPT_CUDA(cudaFuncSetAttribute(merge64p_kernel<N, OP>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge64p_kernel<N, OP>,
+                                                           kPThreads, smem));
+    per_sm = std::max(per_sm, 1);
+  }
+  const uint32_t nctas = std::min<uint32_t>(p.ntiles, (uint32_t)(per_sm * ctx->num_sms));
+  merge64p_kernel<N, OP><<<nctas, kPThreads, smem, st>>>(p, nctas);
+  SPT_LAUNCHED(ctx);
+  return SPT_OK;
+}
+
 template <int N>
 int launch64p(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
   const uint32_t nt = p.ntiles;
   partition_kernel<N><<<(nt + 1 + 7) / 8, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
   SPT_LAUNCHED(ctx);
-  constexpr size_t smem = pers_smem<N>();
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    SPT_CUDA(cudaFuncSetAttribute(merge64p_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge64p_kernel<N>, kPThreads,
-                                                           smem));
-    per_sm = std::max(per_sm, 1);
+  switch (p.op) {
+    case SPT_ADD: return launch64p_op<N, SPT_ADD>(ctx, p, st);
+    case SPT_SUB: return launch64p_op<N, SPT_SUB>(ctx, p, st);
+    default: return launch64p_op<N, SPT_MUL>(ctx, p, st);
   }
-  const uint32_t nctas = std::min<uint32_t>(nt, (uint32_t)(per_sm * ctx->num_sms));
-  merge64p_kernel<N><<<nctas, kPThreads, smem, st>>>(p, nctas);
-  SPT_LAUNCHED(ctx);
-  return SPT_OK;
 }
 
 template <int N>
@@ -935,7 +1002,7 @@ extern "C" int spt_tew_f32(spt_ctx* ctx, const spt_coo* x, const spt_coo* y, int
     p.total = cnt;
     uint32_t epoch;
     SPT_TRY(spt::ctx_lookback(ctx, 1, 1, &epoch));
-    SPT_TRY(spt::ctx_status64(ctx, ntiles, &p.status));
+    SPT_TRY(spt::ctx_status64(ctx, ntiles << 3, &p.status));  // room for strided layouts
     p.epoch = epoch;
     // Packed u64 keys when the per-mode index widths fit (sort order = key
     // significance; indices are < dims as validate() requires).

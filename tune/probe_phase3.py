@@ -31,3 +31,11 @@ for op in (ops.ADD, ops.MUL):
     st("emit(prev)->estart", egap)
     stt = ph[:, 6]; polls = stt >> 32
     print("   polls mean", polls[1:].mean().round(2))
+    lb = (ph[1:,4]-ph[1:,0])/1e3; pl = polls[1:]
+    for k in (1,2,3):
+        sel = pl == k
+        if sel.any(): print(f"   polls=={k}: n={sel.sum()} lookback mean {lb[sel].mean():.2f} p50 {np.median(lb[sel]):.2f}")
+    dist = (ph[1:,6] & 0xffffffff)
+    print("   dist p50", np.median(dist), "mean", dist.mean().round(1))
+    cyc = (ph[1:,6] & 0xffffffff)
+    print("   first poll cycles p50", np.median(cyc), "mean", cyc.mean().round(0), "p90", np.percentile(cyc, 90))
