@@ -165,12 +165,7 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t
                : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  unsigned long long state;
-  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];"
-               : "=l"(state)
-               : "r"(smem_addr(bar))
-               : "memory");
-  (void)state;
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
   asm volatile(

@@ -44,7 +44,7 @@ constexpr int kTile = 2048;
 constexpr int kTileP = kTile + kTile / 8;  // padded per-entry smem arrays
 __device__ __forceinline__ int sw(int e) { return e + ((e >> 5) << 2); }
 constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr uint32_t kFlagA = 1, kFlagP = 2, kFlagBoundary = 4;
+constexpr uint32_t kFlagA = 1, kFlagP = 2;
 
 struct MttkrpParams {
   const uint32_t* out_idx;
@@ -121,17 +121,6 @@ struct Vec<4> {
   }
   static __device__ __forceinline__ void store(float* p, const float (&f)[4]) {
     *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
-  }
-};
-template <>
-struct Vec<2> {
-  static __device__ __forceinline__ void load(const float* p, float (&f)[2]) {
-    const float2 v = __ldg(reinterpret_cast<const float2*>(p));
-    f[0] = v.x;
-    f[1] = v.y;
-  }
-  static __device__ __forceinline__ void store(float* p, const float (&f)[2]) {
-    *reinterpret_cast<float2*>(p) = make_float2(f[0], f[1]);
   }
 };
 template <>

@@ -5,16 +5,16 @@
 // add/sub; unmatched y -> y (add) or -y (sub); mul keeps matches only),
 // tew_output_dims :97-102, par::tew P/src/kernels_par.cpp:144-177.
 //
-// One pass, no host round trip:
+// Two launches, no host round trip:
 //   * a partition kernel places every 2048-item tile boundary on the merge
-//     path of x and y (binary search on the diagonal; ties take x first, so
-//     a matched pair is always "x then y" and each tuple is emitted once);
-//   * a CTA stages its x and y key runs (N u32 arrays each, permuted into sort
-//     order) in shared memory, each thread merges 8 items serially, decides
-//     what it emits, counts, and the CTA gets its global output offset from a
-//     block scan plus a decoupled look-back over 64-bit epoch-tagged tile
-//     counts; then every thread scatters its entries (tuple + value, one IEEE
-//     op, bit-identical to the reference).
+//     path of x and y ((G+1)-ary search on the diagonal; ties take x first,
+//     so a matched pair is always "x then y" and each tuple is emitted once);
+//   * when the N index widths fit 64 bits (the usual case) a persistent,
+//     warp-specialised kernel (merge64p_kernel, below) streams the tiles:
+//     bulk-async staging, u64-key merge of 8 items per thread, block scan,
+//     decoupled look-back over 64-bit epoch-tagged tile counts, coalesced
+//     emission (tuple + value, one IEEE op, bit-identical to the reference);
+//   * otherwise merge_kernel does the same per CTA with N-word compares.
 // The merge order equals the reference's two-pointer merge order, so the
 // output is entry-for-entry identical to seq::tew's.
 #include <cub/cub.cuh>
@@ -77,31 +77,44 @@ __device__ __forceinline__ int cmp_g(const MergeParams& p, uint64_t i, uint64_t 
 
 // Tile boundaries on the merge path (x-first on ties): split[t] = number of x
 // items among the first t*kTile merged items = the first m in [lo, hi) where
-// x[m] <= y[diag-1-m] fails. One warp per diagonal runs a 33-ary search (32
-// probes per round trip, ~5 rounds for 10M) instead of a 24-step binary one.
-template <int N>
-__global__ void partition_kernel(MergeParams p, uint32_t* split) {
-  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const unsigned lane = threadIdx.x & 31u;
-  if (t > p.ntiles) return;  // warp-uniform
+// x[m] <= y[diag-1-m] fails. G lanes per diagonal run a (G+1)-ary search.
+// Each probe is a random sector pair, so the total sector traffic (rounds x
+// G) -- not the round count -- bounds this kernel; G = 8 balances traffic
+// against the number of dependent round trips (measured: 17.6 us vs 21.9 us
+// for G = 32 at 10M + 10M).
+#ifndef SPT_PART_G
+#define SPT_PART_G 8
+#endif
+template <int N, int G>
+__global__ void partition_g_kernel(MergeParams p, uint32_t* split) {
+  const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const unsigned lane = threadIdx.x & 31u, gl = lane % G;
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane - gl);
+  const uint32_t t = gid;
+  const bool live = t <= p.ntiles;
   const uint64_t total = p.nx + p.ny;
-  const uint64_t diag = std::min<uint64_t>((uint64_t)t * kTile, total);
+  const uint64_t diag = live ? std::min<uint64_t>((uint64_t)t * kTile, total) : 0;
   uint64_t lo = diag > p.ny ? diag - p.ny : 0;
   uint64_t hi = std::min<uint64_t>(diag, p.nx);
-  while (hi - lo > 32) {
+  while (__any_sync(0xffffffffu, hi - lo > G)) {
     const uint64_t span = hi - lo;
-    const uint64_t m = lo + (span * (lane + 1)) / 33;
-    const bool pred = cmp_g<N>(p, m, diag - 1 - m) <= 0;
-    const int ntrue = __popc(__ballot_sync(0xffffffffu, pred));
-    const uint64_t m_last = __shfl_sync(0xffffffffu, m, ntrue > 0 ? ntrue - 1 : 0);
-    const uint64_t m_first_false = __shfl_sync(0xffffffffu, m, ntrue < 32 ? ntrue : 31);
-    if (ntrue > 0) lo = m_last + 1;
-    if (ntrue < 32) hi = m_first_false;
+    const bool act = span > G;
+    const uint64_t m = lo + (span * (gl + 1)) / (G + 1);
+    const bool pred = act && cmp_g<N>(p, m, diag - 1 - m) <= 0;
+    const unsigned bal = (__ballot_sync(0xffffffffu, pred) & gmask) >> (lane - gl);
+    const int ntrue = __popc(bal);
+    const uint64_t m_last = __shfl_sync(0xffffffffu, m, (lane - gl) + (ntrue > 0 ? ntrue - 1 : 0));
+    const uint64_t m_first_false =
+        __shfl_sync(0xffffffffu, m, (lane - gl) + (ntrue < G ? ntrue : G - 1));
+    if (act) {
+      if (ntrue > 0) lo = m_last + 1;
+      if (ntrue < G) hi = m_first_false;
+    }
   }
-  const uint64_t m = lo + lane;
+  const uint64_t m = lo + gl;
   const bool pred = m < hi && cmp_g<N>(p, m, diag - 1 - m) <= 0;
-  const int ntrue = __popc(__ballot_sync(0xffffffffu, pred));
-  if (lane == 0) split[t] = static_cast<uint32_t>(lo + ntrue);
+  const int ntrue = __popc((__ballot_sync(0xffffffffu, pred) & gmask));
+  if (gl == 0 && live) split[t] = static_cast<uint32_t>(lo + ntrue);
 }
 
 template <int N>
@@ -130,7 +143,6 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(MergeParams p) {
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_base;
-  __shared__ spt::LookbackSmem s_lb;
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -284,172 +296,10 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(MergeParams p) {
 // entry; indices are unpacked from the key on emission. u64 smem arrays get
 // one pad element per 16 so the ~4-apart merge positions of a half-warp hit
 // distinct banks.
-constexpr int kTP64 = kTile + kTile / 16;
 __device__ __forceinline__ int pad64(int i) { return i + (i >> 4); }
 
-template <int N>
-__device__ __forceinline__ void stage_side(const uint32_t* const* idx, const float* val,
-                                           uint64_t a0, int n, const uint32_t* shift,
-                                           unsigned long long* sk, float* sv, int tid) {
-  constexpr int R = kTile / kThreads;
-  uint32_t t[R][N];
-  float v[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = tid + r * kThreads;
-    if (i < n) {
-#pragma unroll
-      for (int q = 0; q < N; ++q) t[r][q] = spt::ld_stream(idx[q] + a0 + i);
-      v[r] = __ldcs(val + a0 + i);
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = tid + r * kThreads;
-    if (i < n) {
-      unsigned long long k = 0;
-#pragma unroll
-      for (int q = 0; q < N; ++q) k |= (unsigned long long)t[r][q] << shift[q];
-      sk[pad64(i)] = k;
-      sv[pad(i)] = v[r];
-    }
-  }
-}
-
-template <int N>
-__global__ void __launch_bounds__(kThreads, 4) merge64_kernel(MergeParams p) {
-  using Scan = cub::BlockScan<uint32_t, kThreads>;
-  extern __shared__ __align__(16) unsigned long long smem64[];
-  unsigned long long* sx = smem64;            // [kTP64]
-  unsigned long long* sy = smem64 + kTP64;    // [kTP64]
-  float* sxv = reinterpret_cast<float*>(sy + kTP64);          // [kTP]
-  float* syv = sxv + kTP;                                     // [kTP]
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ uint32_t s_tile;
-  __shared__ unsigned long long s_base;
-  __shared__ spt::LookbackSmem s_lb;
-
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    const unsigned long long t = atomicAdd(p.tile_ctr, 1ull);
-    if (t == p.ntiles - 1) atomicExch(p.tile_ctr, 0ull);
-    s_tile = static_cast<uint32_t>(t);
-  }
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t total = p.nx + p.ny;
-  const uint64_t d0 = (uint64_t)tile * kTile;
-  const uint64_t d1 = std::min<uint64_t>(d0 + kTile, total);
-  const uint64_t a0 = p.split[tile], a1 = p.split[tile + 1];
-  const uint64_t b0 = d0 - a0, b1 = d1 - a1;
-  const int nxt = static_cast<int>(a1 - a0), nyt = static_cast<int>(b1 - b0);
-  // Stage both runs with every global load of a side in flight at once (one
-  // round trip per side instead of one per loop iteration).
-  // The neighbours just outside the tile (for match tests at the edges),
-  // loaded together with the staging loads.
-  const unsigned long long y_after =
-      (b0 + nyt < p.ny) ? pack_g<N>(p.yi, p, b0 + nyt) : ~0ull;
-  const unsigned long long x_before = (a0 > 0) ? pack_g<N>(p.xi, p, a0 - 1) : ~0ull;
-  stage_side<N>(p.xi, p.xv, a0, nxt, p.shift, sx, sxv, tid);
-  stage_side<N>(p.yi, p.yv, b0, nyt, p.shift, sy, syv, tid);
-  __syncthreads();
-
-  const int len = nxt + nyt;
-  const int dg = std::min(tid * kIPT, len);
-  int lo = std::max(0, dg - nyt), hi = std::min(dg, nxt);
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (sx[pad64(mid)] <= sy[pad64(dg - 1 - mid)]) lo = mid + 1;
-    else hi = mid;
-  }
-  int i = lo, j = dg - lo;
-  unsigned long long kx = i < nxt ? sx[pad64(i)] : ~0ull;
-  unsigned long long ky = j < nyt ? sy[pad64(j)] : ~0ull;
-  unsigned long long key[kIPT];
-  uint32_t vbits[kIPT];
-  bool emit[kIPT];
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int k = 0; k < kIPT; ++k) {
-    emit[k] = false;
-    key[k] = 0;
-    vbits[k] = 0;
-    if (dg + k >= len) continue;
-    const bool take_x = j >= nyt || (i < nxt && kx <= ky);
-    if (take_x) {
-      const unsigned long long ny_key = j < nyt ? ky : y_after;  // next y in merge order
-      const bool m = kx == ny_key;
-      float v = sxv[pad(i)];
-      if (m) v = apply(p.op, v, j < nyt ? syv[pad(j)] : __ldg(p.yv + b0 + j));
-      emit[k] = (p.op != SPT_MUL) || m;
-      key[k] = kx;
-      vbits[k] = __float_as_uint(v);
-      ++i;
-      kx = i < nxt ? sx[pad64(i)] : ~0ull;
-    } else {
-      const unsigned long long px = i > 0 ? sx[pad64(i - 1)] : x_before;  // previous x
-      const bool m = px == ky;
-      const float yv = syv[pad(j)];
-      emit[k] = (p.op != SPT_MUL) && !m;
-      key[k] = ky;
-      vbits[k] = __float_as_uint(p.op == SPT_SUB ? -yv : yv);
-      ++j;
-      ky = j < nyt ? sy[pad64(j)] : ~0ull;
-    }
-    cnt += emit[k] ? 1u : 0u;
-  }
-  uint32_t excl, tile_total;
-  Scan(scan_tmp).ExclusiveSum(cnt, excl, tile_total);
-  // Publish this tile's count right away (relaxed: the count travels inside
-  // the status word, no payload to order, no MEMBAR).
-  const unsigned long long tag = (unsigned long long)p.epoch << 34;
-  if (tid == 0)
-    spt::st_relaxed64(p.status + tile,
-                      tag | ((tile == 0 ? kFlagP : kFlagA) << 32) | tile_total);
-  // Emitted (key, value) pairs go to tile-local slots; this needs no global
-  // offset, so it overlaps the predecessors' publication. The key arrays are
-  // dead (the Scan's barriers separate their last read from these writes).
-  {
-    unsigned long long* s_key = sx;
-    uint32_t* s_val = reinterpret_cast<uint32_t*>(sy);
-    int lp = static_cast<int>(excl);
-#pragma unroll
-    for (int k = 0; k < kIPT; ++k) {
-      if (!emit[k]) continue;
-      s_key[lp] = key[k];
-      s_val[lp] = vbits[k];
-      ++lp;
-    }
-  }
-  // Decoupled look-back (warp 0, relaxed polling of 32 predecessors).
-  if (tid < 32) {
-    unsigned long long base = 0;
-    if (tile != 0) {
-      base = spt::lookback_count64(p.status, tile, p.epoch);
-      if (tid == 0)
-        spt::st_relaxed64(p.status + tile, tag | (kFlagP << 32) | (base + tile_total));
-    }
-    if (tid == 0) {
-      s_base = base;
-      if (tile == p.ntiles - 1) *p.total = base + tile_total;
-    }
-  }
-  __syncthreads();
-  // One coalesced pass: each output element unpacks its N indices from the key.
-  const uint64_t base = s_base;
-  const unsigned long long* s_key = sx;
-  const uint32_t* s_val = reinterpret_cast<const uint32_t*>(sy);
-  for (uint32_t o = tid; o < tile_total; o += kThreads) {
-    const unsigned long long k = s_key[o];
-#pragma unroll
-    for (int q = 0; q < N; ++q)
-      spt::st_stream(p.zi[q] + base + o, (uint32_t)((k >> p.shift[q]) & p.mask[q]));
-    spt::st_stream(reinterpret_cast<uint32_t*>(p.zv) + base + o, s_val[o]);
-  }
-}
-
 // ---------------------------------------------------------------------------
-// Persistent, pipelined, warp-specialised variant of merge64_kernel.
+// Persistent, pipelined, warp-specialised merge (packed u64 keys).
 //
 // A CTA (resident for the whole merge) = 8 merge warps + 1 emitter warp + 1
 // producer warp:
@@ -488,7 +338,8 @@ constexpr int kStages = SPT_MERGE_STAGES;
 constexpr int kSS = SPT_STATUS_SHIFT;  // status word of tile t at t << kSS
 constexpr int kSeg = kTile + 16;  // words per staged array (x run + y run + alignment slack)
 constexpr uint32_t kDone = 0xFFFFFFFFu;
-constexpr int kPThreads = kThreads + 96;  // + look-back, emitter, producer warps
+constexpr int kLB = 2;                      // look-back warps (alternate tiles)
+constexpr int kPThreads = kThreads + 32 * (kLB + 2);  // + look-back x2, emitter, producer
 constexpr int kSlots = 4;                   // tile hand-off ring (merge -> look-back -> emitter)
 // Emission buffers: threads write their emitted items ~8 apart, so pad one
 // slot per 16 (u64 keys) / per 8 (u32 values) to spread those rows over all
@@ -526,9 +377,20 @@ constexpr size_t pers_smem() {
 __device__ __forceinline__ void copy_run(uint32_t* dst, const uint32_t* src, uint64_t e0,
                                          uint32_t n, uint32_t head, uint32_t body,
                                          unsigned long long* bar) {
-  for (uint32_t k = 0; k < head; ++k) dst[k] = __ldg(src + e0 + k);
-  for (uint32_t k = head + body; k < n; ++k) dst[k] = __ldg(src + e0 + k);
   if (body) spt::bulk_g2s(dst + head, src + e0 + head, body * 4, bar);
+  // <= 3 head and <= 3 tail words: all six loads in flight, then the stores
+  const uint32_t tail = n - head - body;
+  uint32_t hv[3], tv[3];
+#pragma unroll
+  for (uint32_t k = 0; k < 3; ++k) {
+    if (k < head) hv[k] = __ldg(src + e0 + k);
+    if (k < tail) tv[k] = __ldg(src + e0 + head + body + k);
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < 3; ++k) {
+    if (k < head) dst[k] = hv[k];
+    if (k < tail) dst[head + body + k] = tv[k];
+  }
 }
 
 __device__ __forceinline__ uint32_t word_phase(const uint32_t* p) {
@@ -536,7 +398,7 @@ __device__ __forceinline__ uint32_t word_phase(const uint32_t* p) {
 }
 
 template <int N, int OP>
-__global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint32_t nctas) {
+__global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, uint32_t nctas) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint32_t* stages = reinterpret_cast<uint32_t*>(smem_raw);
   unsigned long long* sk =
@@ -581,7 +443,7 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
   const unsigned lane = tid & 31u;
   const unsigned long long tag = (unsigned long long)p.epoch << 34;
 
-  if (tid >= kThreads + 64) {
+  if (tid >= kThreads + 32 * (kLB + 1)) {
     // ---- producer warp ----
     for (uint32_t it = 0;; ++it) {
       const int s = it % kStages;
@@ -646,7 +508,7 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
     return;
   }
 
-  if (tid >= kThreads + 32) {
+  if (tid >= kThreads + 32 * kLB) {
     // ---- emitter warp: coalesced output of each tile at its base ----
     for (uint32_t it = 0;; ++it) {
       const int r = it % kSlots, b = it & 1;
@@ -675,8 +537,10 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
   }
 
   if (tid >= kThreads) {
-    // ---- look-back warp: exclusive output offset of each tile, publish P ----
-    for (uint32_t it = 0;; ++it) {
+    // ---- look-back warps: exclusive output offset of each tile, publish P.
+    // kLB warps take the CTA's tiles round-robin, so a look-back that waits
+    // on a slow predecessor does not hold up the next tile's.
+    for (uint32_t it = (tid - kThreads) >> 5;; it += kLB) {
       const int r = it % kSlots;
       spt::mbar_wait(lbfull + r, (it / kSlots) & 1u);
       const uint32_t tile = slot[r].tile, tile_total = slot[r].total;
@@ -715,6 +579,28 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
   // ---- merge warps ----
   using spt::bar_sync;
   const int warp = tid >> 5;
+  // A tile's emitted items stay in registers until the next tile has been
+  // merged, and only then go to an emission buffer: by that time the tile's
+  // look-back has mostly resolved, so each buffer is held only for the
+  // emission itself (two buffers + this register stage = three in flight).
+  unsigned long long pkey[kIPT];
+  uint32_t pvb[kIPT];
+  uint32_t pmask = 0, pexcl = 0;
+  auto flush = [&](uint32_t eseq) {
+    const int b = eseq & 1;
+    if (eseq >= 2) spt::mbar_wait(eempty + b, ((eseq >> 1) - 1) & 1u);
+    unsigned long long* ek = ek0 + b * kEK;
+    uint32_t* ev = ev0 + b * kEV;
+    int lp = static_cast<int>(pexcl);
+#pragma unroll
+    for (int k = 0; k < kIPT; ++k) {
+      if (!((pmask >> k) & 1u)) continue;
+      ek[epad64(lp)] = pkey[k];
+      ev[epad(lp)] = pvb[k];
+      ++lp;
+    }
+    spt::mbar_arrive(efull + b);
+  };
   for (uint32_t it = 0;; ++it) {
     const int s = it % kStages;
 #ifdef SPT_PHASES
@@ -723,12 +609,17 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
     spt::mbar_wait(full + s, (it / kStages) & 1u);
     const StageInfo& inf = info[s];
     const uint32_t tile = inf.tile;
-    const int eb = it & 1, r = it % kSlots;
+    const int r = it % kSlots;
     if (tile == kDone) {
+      if (it > 0) flush(it - 1);
       if (tid == 0) {
-        if (it >= kSlots) spt::mbar_wait(sempty + r, ((it / kSlots) - 1) & 1u);
-        slot[r].tile = kDone;
-        spt::mbar_arrive(lbfull + r);
+        // one kDone per look-back warp (each waits on its own slots)
+        for (uint32_t d = it; d < it + kLB; ++d) {
+          const int rd = d % kSlots;
+          if (d >= kSlots) spt::mbar_wait(sempty + rd, ((d / kSlots) - 1) & 1u);
+          slot[rd].tile = kDone;
+          spt::mbar_arrive(lbfull + rd);
+        }
       }
       break;
     }
@@ -848,23 +739,16 @@ __global__ void __launch_bounds__(kPThreads) merge64p_kernel(MergeParams p, uint
 #ifdef SPT_PHASES
     if (tid == 0) SPT_PH(tile, 3);
 #endif
-    // emitter done with the tile that last used this buffer
-    if (it >= 2) spt::mbar_wait(eempty + eb, ((it >> 1) - 1) & 1u);
-    {
-      unsigned long long* ek = ek0 + eb * kEK;
-      uint32_t* ev = ev0 + eb * kEV;
-      int lp = static_cast<int>(excl);
+    if (it > 0) flush(it - 1);
 #pragma unroll
-      for (int k = 0; k < kIPT; ++k) {
-        if (!((emitm >> k) & 1u)) continue;
-        ek[epad64(lp)] = key[k];
-        ev[epad(lp)] = vbits[k];
-        ++lp;
-      }
+    for (int k = 0; k < kIPT; ++k) {
+      pkey[k] = key[k];
+      pvb[k] = vbits[k];
     }
+    pmask = emitm;
+    pexcl = excl;
     // s_wsum[0..7] are rewritten only after the next pack barrier, which every
     // thread reaches after its reads above.
-    spt::mbar_arrive(efull + eb);
   }
 }
 
@@ -889,7 +773,7 @@ int launch64p_op(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
 template <int N>
 int launch64p(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
   const uint32_t nt = p.ntiles;
-  partition_kernel<N><<<(nt + 1 + 7) / 8, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
+  partition_g_kernel<N, SPT_PART_G><<<((uint64_t)(nt + 1) * SPT_PART_G + 255) / 256, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
   SPT_LAUNCHED(ctx);
   switch (p.op) {
     case SPT_ADD: return launch64p_op<N, SPT_ADD>(ctx, p, st);
@@ -899,22 +783,9 @@ int launch64p(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
 }
 
 template <int N>
-int launch64(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
-  const uint32_t nt = p.ntiles;
-  partition_kernel<N><<<(nt + 1 + 7) / 8, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
-  SPT_LAUNCHED(ctx);
-  const size_t smem = (size_t)2 * kTP64 * 8 + (size_t)2 * kTP * 4;
-  SPT_CUDA(cudaFuncSetAttribute(merge64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-  merge64_kernel<N><<<nt, kThreads, smem, st>>>(p);
-  SPT_LAUNCHED(ctx);
-  return SPT_OK;
-}
-
-template <int N>
 int launch(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
   const uint32_t nt = p.ntiles;
-  partition_kernel<N><<<(nt + 1 + 7) / 8, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
+  partition_g_kernel<N, SPT_PART_G><<<((uint64_t)(nt + 1) * SPT_PART_G + 255) / 256, 256, 0, st>>>(p, const_cast<uint32_t*>(p.split));
   SPT_LAUNCHED(ctx);
   const size_t smem = (size_t)(2 * N + 2) * kTP * sizeof(uint32_t) + kTile * sizeof(uint32_t);
   SPT_CUDA(cudaFuncSetAttribute(merge_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
