@@ -1,0 +1,6 @@
+#!/bin/bash
+# usage: tune/mk_mvariant.sh <out.so> <extra nvcc flags...>  (rebuilds mttkrp.cu only)
+out=$1; shift
+cd /root/repo/paper_1902_03317_b200/csrc
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr "$@" -c mttkrp.cu -o /tmp/mt_var.o && \
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o /root/repo/$out ../../build/csrc/capi.o ../../build/csrc/elementwise.o ../../build/csrc/gen.o /tmp/mt_var.o ../../build/csrc/sort.o ../../build/csrc/tew_merge.o ../../build/csrc/ttv.o -lcudart
