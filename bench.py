@@ -421,6 +421,58 @@ class C4(Workload):
                 "mttkrp_input": "one mode-leading sorted copy per mode (preprocessing)"}
 
 
+class C5(Workload):
+    """BASELINE configs[4] (C5): MTTKRP modes 0-2 (R=32) + TEW-eq mul on a
+    1B-nnz order-3 tensor, every mode Zipf(1.1). One GPU holds the tensor
+    (16 GB), one mode-leading copy per mode and the TEW-eq operand/output;
+    under torchrun every rank runs its own instance and MTTKRP adds the NCCL
+    all-reduce of the I_n x R partials."""
+
+    name = "c5-mttkrp-tew_eq"
+
+    def __init__(self, seed, device, scale=1.0):
+        from paper_1902_03317_b200 import generate, ops
+        from paper_1902_03317_b200.coo import DeviceCOO
+        c = generate.CONFIGS["c5"]
+        self.dims, self.R = c["dims"], c["R"]
+        self.nnz = int(c["nnz"] * scale)
+        dev = f"cuda:{device}"
+        base = generate.coo(self.dims, self.nnz, seed, c["zipf"], 0.0, 1.0, None, device)
+        self.f = [generate.uniform((d, self.R), seed, 100 + k, 0.0, 1.0, device)
+                  for k, d in enumerate(self.dims)]
+        self.xs = []
+        for mode in range(3):
+            xs = base if mode == 2 else base.clone()
+            ops.sort_lexicographic(xs, [mode] + [d for d in range(3) if d != mode])
+            self.xs.append(xs)
+        del base
+        torch.cuda.empty_cache()
+        x = self.xs[0]
+        # TEW-eq operand: same pattern in its own buffers (as SURVEY 8(d) counts
+        # the bytes), values U[0.5,1.5)
+        self.y = DeviceCOO(list(self.dims), [i.clone() for i in x.indices],
+                           generate.uniform(self.nnz, seed, 77, 0.5, 1.5, device),
+                           list(x.sort_order), x.coalesced)
+        self.z = DeviceCOO.empty(self.dims, self.nnz, device)
+        self.out = [torch.empty((d, self.R), dtype=torch.float32, device=dev) for d in self.dims]
+        n, N, R = self.nnz, 3, self.R
+        self.ops = [Op(f"mttkrp_m{m}",
+                       lambda m=m: allreduce(ops.mttkrp(self.xs[m], self.f, m,
+                                                        ops.MTTKRP_SEGMENTED, out=self.out[m],
+                                                        sync=False)),
+                       n, lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims))
+                    for m in range(3)]
+        self.ops.append(Op("tew_eq_mul",
+                           lambda: ops.tew_eq(x, self.y, ops.MUL, out=self.z, sync=False),
+                           n, lambda: 3 * tensor_bytes(n, N)))
+
+    def config(self):
+        return {"workload": self.name, "baseline_config": "configs[4] (C5)", "dims": self.dims,
+                "nnz": self.nnz, "R": self.R, "dist": "every mode Zipf(1.1), shuffled ids",
+                "mttkrp_input": "one mode-leading sorted copy per mode (preprocessing)",
+                "tew_eq": "mul against the same pattern, y U[0.5,1.5)"}
+
+
 class Pre(Workload):
     """SURVEY 8(f) "next" row 1: GPU preprocessing at parity and speed --
     sort_lexicographic (P/src/tensor.cpp:54-64; 4.56 s for 10M on the
@@ -474,7 +526,7 @@ class Pre(Workload):
         return self.cpu_units
 
 
-WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "pre": Pre}
+WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c5": C5, "pre": Pre}
 
 
 # ---------------------------------------------------------------------------
