@@ -100,7 +100,8 @@ __device__ __forceinline__ void ttm_emit_idx(const MttkrpParams& p, uint32_t hea
       for (int k = 0; k < NCOL; ++k) w[k] = h;
     }
     if constexpr (NCOL == 4) {
-      *reinterpret_cast<uint4*>(p.zidx[d] + base) = make_uint4(w[0], w[1], w[2], w[3]);
+      // outputs are written once and never re-read here: evict-first stores
+      __stcs(reinterpret_cast<uint4*>(p.zidx[d] + base), make_uint4(w[0], w[1], w[2], w[3]));
     } else {
 #pragma unroll
       for (int k = 0; k < NCOL; ++k) p.zidx[d][base + k] = w[k];
@@ -120,7 +121,7 @@ struct Vec<4> {
     f[3] = v.w;
   }
   static __device__ __forceinline__ void store(float* p, const float (&f)[4]) {
-    *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+    __stcs(reinterpret_cast<float4*>(p), make_float4(f[0], f[1], f[2], f[3]));
   }
 };
 template <>
