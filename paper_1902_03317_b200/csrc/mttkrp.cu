@@ -1048,7 +1048,7 @@ TtmVariant choose_ttm(uint32_t R, bool aligned) {
 
 namespace spt {
 int build_tile_fiber_map(spt_ctx* ctx, const uint32_t* d_fptr, uint32_t nfibs, uint32_t tile,
-                         uint32_t* d_map, cudaStream_t st);
+                         uint32_t ntiles, uint32_t* d_map, cudaStream_t st);
 int check_fiber_inputs(const spt_coo* x, uint32_t mode, const uint32_t* d_fptr, uint64_t nfibs,
                        const char* k);
 }  // namespace spt
@@ -1095,7 +1095,8 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
   const uint64_t ntiles = (x->nnz + kTile - 1) / kTile;
   uint32_t* map;
   SPT_TRY(spt::ctx_scratch(ctx, ntiles * sizeof(uint32_t), reinterpret_cast<void**>(&map)));
-  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), kTile, map, st));
+  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), kTile,
+                                    static_cast<uint32_t>(ntiles), map, st));
 
   MttkrpParams p{};
   p.oidx[0] = x->idx[mode];

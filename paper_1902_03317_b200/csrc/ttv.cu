@@ -232,16 +232,38 @@ __global__ void __launch_bounds__(kThreads, 4) ttv_kernel(TtvParams p) {
       spt::st_stream(p.zidx[d] + f_lo + o, s_zi[d * (kTile + 2) + o]);
 }
 
-// map[t] = fiber containing entry t*tile (fptr is non-decreasing, every fiber
-// non-empty); one thread per fiber, streaming over fptr.
+// map[t] = fiber containing entry t*tile = the largest f < nfibs with
+// fptr[f] <= t*tile (fptr is non-decreasing, fptr[0] = 0). G = 8 lanes per
+// tile run a 9-ary search over fptr: ~8 dependent rounds for 5e7 fibers, all
+// tiles in parallel -- instead of a streaming pass over every fiber.
+constexpr int kMapG = 8;
 __global__ void tile_fiber_kernel(const uint32_t* fptr, uint32_t nfibs, uint32_t tile,
-                                  uint32_t* map) {
-  uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (; f < nfibs; f += stride) {
-    const uint32_t a = (fptr[f] + tile - 1) / tile, b = (fptr[f + 1] + tile - 1) / tile;
-    for (uint32_t t = a; t < b; ++t) map[t] = f;
+                                  uint32_t ntiles, uint32_t* map) {
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) / kMapG;
+  const unsigned lane = threadIdx.x & 31u, gl = lane % kMapG, g0 = lane - gl;
+  const unsigned gmask = ((1u << kMapG) - 1u) << g0;
+  const bool live = t < ntiles;
+  const uint64_t target = (uint64_t)t * tile;
+  uint32_t lo = 0, hi = live ? nfibs : 0;  // answer in [lo, hi): fptr[lo] <= target
+  while (__any_sync(0xffffffffu, hi - lo > kMapG)) {
+    const uint32_t span = hi - lo;
+    const bool act = span > kMapG;
+    const uint32_t m = lo + (uint32_t)(((uint64_t)span * (gl + 1)) / (kMapG + 1));
+    const bool pred = act && fptr[m] <= target;
+    const int ntrue = __popc((__ballot_sync(0xffffffffu, pred) & gmask) >> g0);
+    const uint32_t m_last = __shfl_sync(0xffffffffu, m, g0 + (ntrue > 0 ? ntrue - 1 : 0));
+    const uint32_t m_first_false =
+        __shfl_sync(0xffffffffu, m, g0 + (ntrue < kMapG ? ntrue : kMapG - 1));
+    if (act) {
+      if (ntrue > 0) lo = m_last;
+      if (ntrue < kMapG) hi = m_first_false;
+    }
   }
+  // final: the last m in [lo, hi) with fptr[m] <= target (fptr[lo] <= target holds)
+  const uint32_t m = lo + gl;
+  const bool pred = m < hi && fptr[m] <= target;
+  const int ntrue = __popc((__ballot_sync(0xffffffffu, pred) & gmask) >> g0);
+  if (gl == 0 && live) map[t] = lo + (ntrue > 0 ? ntrue - 1 : 0);
 }
 
 template <int NO>
@@ -259,9 +281,10 @@ int launch_ttv(spt_ctx* ctx, const TtvParams& p, unsigned grid, cudaStream_t st)
 namespace spt {
 
 int build_tile_fiber_map(spt_ctx* ctx, const uint32_t* d_fptr, uint32_t nfibs, uint32_t tile,
-                         uint32_t* d_map, cudaStream_t st) {
-  tile_fiber_kernel<<<grid_for(nfibs, 256, ctx->num_sms * 16), 256, 0, st>>>(d_fptr, nfibs, tile,
-                                                                            d_map);
+                         uint32_t ntiles, uint32_t* d_map, cudaStream_t st) {
+  const uint64_t threads = (uint64_t)ntiles * kMapG;
+  tile_fiber_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
+      d_fptr, nfibs, tile, ntiles, d_map);
   SPT_LAUNCHED(ctx);
   return SPT_OK;
 }
@@ -314,7 +337,8 @@ extern "C" int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uin
   const uint64_t ntiles = (x->nnz + kTile - 1) / kTile;
   uint32_t* map;
   SPT_TRY(spt::ctx_scratch(ctx, ntiles * sizeof(uint32_t), reinterpret_cast<void**>(&map)));
-  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), kTile, map, st));
+  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), kTile,
+                                    static_cast<uint32_t>(ntiles), map, st));
   uint32_t epoch;
   SPT_TRY(spt::ctx_lookback(ctx, ntiles, 2 * ntiles, &epoch));
   TtvParams p{};
