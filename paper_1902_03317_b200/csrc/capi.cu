@@ -203,6 +203,14 @@ int spt_ctx_create(int device, spt_ctx** out) {
   SPT_CUDA(cudaMalloc(&c->d_tile_ctr, 4 * sizeof(unsigned long long)));
   SPT_CUDA(cudaMemset(c->d_tile_ctr, 0, 4 * sizeof(unsigned long long)));
   SPT_CUDA(cudaMallocHost(&c->h_pinned, 8 * sizeof(unsigned long long)));
+  // Stream-ordered temporaries (sort permutations) come from the device's
+  // default pool; keep its freed memory mapped instead of trimming it at every
+  // synchronisation (an unmap/remap of tens of MB per call otherwise).
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   *out = c;
   return SPT_OK;
 }
