@@ -373,3 +373,57 @@ def test_generator_contract(sp):
     c0 = np.bincount(h.indices[0], minlength=1000)
     c1 = np.bincount(h.indices[1], minlength=800)
     assert c0.max() > 20 * c0.mean() and c1.max() < 3 * c1.mean()
+
+
+def _wide_tensor(rng, dims, nnz, lo=0.5, hi=1.5):
+    """Distinct tuples drawn mode by mode (index spaces beyond 2^63)."""
+    idx = np.stack([rng.integers(0, d, size=nnz + nnz // 4, dtype=np.uint64) for d in dims], 1)
+    idx = np.unique(idx, axis=0)
+    rng.shuffle(idx)
+    idx = idx[:nnz]
+    return HostTensor(list(dims), [idx[:, d].astype(np.uint32).copy() for d in range(len(dims))],
+                      rng.uniform(lo, hi, idx.shape[0]).astype(np.float32), None, True)
+
+
+@pytest.mark.parametrize("dims", [
+    [1 << 30, 1 << 30, 1 << 30],            # 90-bit keys: generic N-word merge
+    [40000, 40000, 40000, 40000, 40000],    # 80 bits: generic
+    [256] * 8,                              # exactly 64 bits, order 8: packed
+    [3, 5, 7, 11],                          # tiny widths, many duplicates across x and y
+])
+def test_tew_key_widths(sp, dims):
+    ops = sp[0]
+    rng = np.random.default_rng(len(dims) * 7 + dims[0] % 97)
+    cap = float(np.prod([float(d) for d in dims]))
+    n = int(min(60_000, cap // 3))
+    x = _wide_tensor(rng, dims, n)
+    y = _wide_tensor(rng, dims, n)
+    for op in range(3):
+        got = host(ops.tew(dev(sp, x), dev(sp, y), op))
+        want, _ = O.tew(x.copy(), y.copy(), op)
+        assert same(got, want), (dims, op)
+
+
+@pytest.mark.parametrize("nnz", [2047, 2048, 4096 + 5, 50_000])
+def test_tew_matches_at_tile_edges(sp, nnz):
+    """x and y share most tuples, so matched pairs straddle every merge tile
+    boundary (the pair is split between two tiles' x and y runs)."""
+    ops = sp[0]
+    rng = np.random.default_rng(nnz)
+    base = rand_tensor(rng, [300, 300, 300], nnz + nnz // 3, 0.5, 1.5)
+    keep_x = rng.random(base.nnz) < 0.8
+    keep_y = rng.random(base.nnz) < 0.8
+    sub = lambda m: HostTensor(base.dims, [a[m].copy() for a in base.indices],
+                               rng.uniform(0.5, 1.5, int(m.sum())).astype(np.float32), None, True)
+    x, y = sub(keep_x), sub(keep_y)
+    for op in range(3):
+        got = host(ops.tew(dev(sp, x), dev(sp, y), op))
+        want, _ = O.tew(x.copy(), y.copy(), op)
+        assert same(got, want), (nnz, op)
+    # identical patterns: every item of x matches
+    y2 = HostTensor(x.dims, [a.copy() for a in x.indices], (x.values * 2).astype(np.float32),
+                    None, True)
+    for op in range(3):
+        got = host(ops.tew(dev(sp, x), dev(sp, y2), op))
+        want, _ = O.tew(x.copy(), y2.copy(), op)
+        assert same(got, want), ("identical", nnz, op)
