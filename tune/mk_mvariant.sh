@@ -3,4 +3,4 @@
 out=$1; shift
 cd /root/repo/paper_1902_03317_b200/csrc
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr "$@" -c mttkrp.cu -o /tmp/mt_var.o && \
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o /root/repo/$out ../../build/csrc/capi.o ../../build/csrc/elementwise.o ../../build/csrc/gen.o /tmp/mt_var.o ../../build/csrc/sort.o ../../build/csrc/tew_merge.o ../../build/csrc/ttv.o -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o /root/repo/$out $(ls ../../build/csrc/*.o | grep -v /mttkrp.o) /tmp/mt_var.o -lcudart
