@@ -79,6 +79,27 @@ __global__ void head_flags_kernel(TupleCmp t, uint32_t* flags, uint64_t n) {
   }
 }
 
+// Inverse of pack_keys_kernel for a tuple that fits one key: idx[d][i] from
+// the sorted key (constant modes -> 0), values from the co-sorted payload.
+struct UnpackSpec {
+  uint32_t* idx[SPT_MAX_ORDER];
+  uint32_t shift[SPT_MAX_ORDER];
+  uint32_t mask[SPT_MAX_ORDER];
+  int n;
+};
+template <typename K>
+__global__ void unpack_keys_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                   UnpackSpec spec, uint32_t* __restrict__ out_val, uint64_t n) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    const K k = keys[i];
+    for (int j = 0; j < spec.n; ++j)
+      spt::st_stream(spec.idx[j] + i, static_cast<uint32_t>(k >> spec.shift[j]) & spec.mask[j]);
+    if (out_val != vals) spt::st_stream(out_val + i, vals[i]);
+  }
+}
+
 // Coalesce: heads write the tuple and the sequential fp32 sum of their group
 // in storage order (acc = v[m]; acc += v[e] ...; P/src/tensor.cpp:79-88).
 __global__ void coalesce_write_kernel(TupleCmp t, const float* vals, const uint32_t* flags,
@@ -230,7 +251,76 @@ int spt_sort_f32(spt_ctx* ctx, spt_coo* x, const uint32_t* mode_order, unsigned 
   }
   cudaStream_t st = spt::as_stream(stream);
   const uint64_t n = x->nnz;
-  if (n > 1) {
+  // Whole tuple in one key (the common case: C2 42 bits, C3 48): sort
+  // (packed key, value) pairs and unpack the indices from the sorted keys --
+  // no permutation and no gather pass.
+  uint32_t total_bits = 0;
+  for (uint32_t d = 0; d < x->order; ++d) total_bits += bits_for(x->dims[d]);
+  if (n > 1 && total_bits <= 64) {
+    PackSpec spec{};
+    UnpackSpec un{};
+    uint32_t used = 0;
+    for (int k = static_cast<int>(x->order) - 1; k >= 0; --k) {
+      const uint32_t d = mode_order[k];
+      const uint32_t b = bits_for(x->dims[d]);
+      un.idx[un.n] = x->idx[d];
+      un.shift[un.n] = used;
+      un.mask[un.n] = b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u);
+      un.n++;
+      if (b == 0) continue;
+      spec.idx[spec.n] = x->idx[d];
+      spec.shift[spec.n] = used;
+      spec.n++;
+      used += b;
+    }
+    const int nb = static_cast<int>(std::max<uint32_t>(used, 1));
+    const bool k32 = used <= 32;
+    size_t temp = 0;
+    {
+      cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
+      if (k32) {
+        cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
+        SPT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k, v, static_cast<int64_t>(n), 0,
+                                                 nb, st));
+      } else {
+        cub::DoubleBuffer<unsigned long long> k(nullptr, nullptr);
+        SPT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k, v, static_cast<int64_t>(n), 0,
+                                                 nb, st));
+      }
+    }
+    const size_t kb = align_up(n * (k32 ? 4 : 8)), vb = align_up(n * 4);
+    void* scratch;
+    SPT_TRY(spt::ctx_scratch(ctx, 2 * kb + vb + align_up(temp), &scratch));
+    char* base = static_cast<char*>(scratch);
+    uint32_t* val_b = reinterpret_cast<uint32_t*>(base + 2 * kb);
+    void* tmp = base + 2 * kb + vb;
+    uint32_t* xv = reinterpret_cast<uint32_t*>(x->val);
+    const unsigned g = grid_of(ctx, n);
+    if (k32) {
+      uint32_t* ka = reinterpret_cast<uint32_t*>(base);
+      pack_keys_kernel<uint32_t><<<g, 256, 0, st>>>(spec, nullptr, ka, nullptr, n);
+      SPT_LAUNCHED(ctx);
+      cub::DoubleBuffer<uint32_t> keys(ka, reinterpret_cast<uint32_t*>(base + kb));
+      cub::DoubleBuffer<uint32_t> vals(xv, val_b);
+      SPT_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, keys, vals, static_cast<int64_t>(n), 0,
+                                               nb, st));
+      ctx->launches += (nb + 7) / 8 + 2;
+      unpack_keys_kernel<uint32_t><<<g, 256, 0, st>>>(keys.Current(), vals.Current(), un, xv, n);
+    } else {
+      auto* ka = reinterpret_cast<unsigned long long*>(base);
+      pack_keys_kernel<unsigned long long><<<g, 256, 0, st>>>(spec, nullptr, ka, nullptr, n);
+      SPT_LAUNCHED(ctx);
+      cub::DoubleBuffer<unsigned long long> keys(ka,
+                                                 reinterpret_cast<unsigned long long*>(base + kb));
+      cub::DoubleBuffer<uint32_t> vals(xv, val_b);
+      SPT_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, keys, vals, static_cast<int64_t>(n), 0,
+                                               nb, st));
+      ctx->launches += (nb + 7) / 8 + 2;
+      unpack_keys_kernel<unsigned long long><<<g, 256, 0, st>>>(keys.Current(), vals.Current(),
+                                                                un, xv, n);
+    }
+    SPT_LAUNCHED(ctx);
+  } else if (n > 1) {
     // perm lives in its own allocation (sort_tuples uses the ctx scratch).
     uint32_t* perm = nullptr;
     uint32_t* tmp = nullptr;
