@@ -23,7 +23,13 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kEPT = 8;
+#ifndef SPT_TTV_EPT
+#define SPT_TTV_EPT 8
+#endif
+#ifndef SPT_TTV_MINB
+#define SPT_TTV_MINB 4
+#endif
+constexpr int kEPT = SPT_TTV_EPT;
 constexpr int kTile = kThreads * kEPT;
 constexpr uint32_t kFlagA = 1, kFlagP = 2;
 
@@ -58,7 +64,7 @@ struct TtvParams {
 };
 
 template <int NO>
-__global__ void __launch_bounds__(kThreads, 4) ttv_kernel(TtvParams p) {
+__global__ void __launch_bounds__(kThreads, SPT_TTV_MINB) ttv_kernel(TtvParams p) {
   using Scan = cub::BlockScan<SegPair, kThreads>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ uint32_t s_fptr[kTile + 2];
@@ -90,22 +96,18 @@ __global__ void __launch_bounds__(kThreads, 4) ttv_kernel(TtvParams p) {
   uint32_t oi[NO][kEPT];
   if (cnt == kTile && p.vec_ok) {
 #pragma unroll
-    for (int d = 0; d < NO; ++d) {
-      const uint4 a = spt::ld_stream(reinterpret_cast<const uint4*>(p.hidx[d] + t0 + e0));
-      const uint4 b = spt::ld_stream(reinterpret_cast<const uint4*>(p.hidx[d] + t0 + e0) + 1);
-      oi[d][0] = a.x, oi[d][1] = a.y, oi[d][2] = a.z, oi[d][3] = a.w;
-      oi[d][4] = b.x, oi[d][5] = b.y, oi[d][6] = b.z, oi[d][7] = b.w;
+    for (int c = 0; c < kEPT / 4; ++c) {
+#pragma unroll
+      for (int d = 0; d < NO; ++d) {
+        const uint4 a = spt::ld_stream(reinterpret_cast<const uint4*>(p.hidx[d] + t0 + e0) + c);
+        oi[d][4 * c] = a.x, oi[d][4 * c + 1] = a.y, oi[d][4 * c + 2] = a.z, oi[d][4 * c + 3] = a.w;
+      }
+      const uint4 k0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0) + c);
+      const uint4 v0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0 + e0) + c);
+      kk[4 * c] = k0.x, kk[4 * c + 1] = k0.y, kk[4 * c + 2] = k0.z, kk[4 * c + 3] = k0.w;
+      val[4 * c] = __uint_as_float(v0.x), val[4 * c + 1] = __uint_as_float(v0.y);
+      val[4 * c + 2] = __uint_as_float(v0.z), val[4 * c + 3] = __uint_as_float(v0.w);
     }
-    const uint4 k0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0));
-    const uint4 k1 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0) + 1);
-    const uint4 v0 = spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0 + e0));
-    const uint4 v1 = spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0 + e0) + 1);
-    kk[0] = k0.x, kk[1] = k0.y, kk[2] = k0.z, kk[3] = k0.w;
-    kk[4] = k1.x, kk[5] = k1.y, kk[6] = k1.z, kk[7] = k1.w;
-    val[0] = __uint_as_float(v0.x), val[1] = __uint_as_float(v0.y);
-    val[2] = __uint_as_float(v0.z), val[3] = __uint_as_float(v0.w);
-    val[4] = __uint_as_float(v1.x), val[5] = __uint_as_float(v1.y);
-    val[6] = __uint_as_float(v1.z), val[7] = __uint_as_float(v1.w);
   } else {
 #pragma unroll
     for (int i = 0; i < kEPT; ++i) {
