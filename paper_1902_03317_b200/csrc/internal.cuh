@@ -263,17 +263,13 @@ __device__ __forceinline__ unsigned long long lookback_count64(const unsigned lo
 // trips into one or two.
 template <int W, int SH = 0>
 __device__ __forceinline__ unsigned long long lookback_count64_wide(
-    const unsigned long long* status, uint32_t tile, uint32_t epoch,
-    uint32_t* stats = nullptr) {  // debug: [polls, distance to the P]
+    const unsigned long long* status, uint32_t tile, uint32_t epoch) {
   // Predecessor at distance 32*k + lane + 1 sits in lane `lane`, slot k, so
   // each of the W loads is one coalesced 256-byte request.
   const unsigned lane = threadIdx.x & 31u;
   unsigned long long acc = 0;
   uint32_t base = 0;
-  uint32_t polls = 0;
   while (true) {
-    ++polls;
-    const long long c0 = clock64();
     uint32_t cnt[W];
     unsigned ready[W], isP[W];
     unsigned long long w[W];
@@ -291,7 +287,6 @@ __device__ __forceinline__ unsigned long long lookback_count64_wide(
       ready[k] = __ballot_sync(0xffffffffu, flag != 0);
       isP[k] = __ballot_sync(0xffffffffu, flag == 2);
     }
-    if (stats && polls == 1) stats[2] = (uint32_t)(clock64() - c0);
     // walk the sub-windows nearest-first (warp-uniform)
     int ks = W, ls = 31;  // take sub-windows < ks fully, sub-window ks up to lane ls
     bool found = false, blocked = false;
@@ -319,75 +314,11 @@ __device__ __forceinline__ unsigned long long lookback_count64_wide(
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     acc += v;
-    if (found) {
-      if (stats) {
-        stats[0] = polls;
-        stats[1] = base + 32 * ks + ls + 1;
-      }
-      return acc;
-    }
+    if (found) return acc;
     base += 32 * W;
   }
 }
 
-// CTA-wide variant of lookback_count64: all NT threads poll NT predecessors
-// per round trip. When hundreds of tiles are in flight, the tiles between a
-// tile and the nearest inclusive prefix are mostly still in their own
-// look-back (A only), so a 32-wide window needed several sequential round
-// trips; NT-wide needs one. Must be called by every thread of the CTA.
-struct LookbackSmem {
-  uint32_t ready[32], isp[32];
-  unsigned long long sum;
-};
-template <int NT>
-__device__ __forceinline__ unsigned long long lookback_count64_block(
-    const unsigned long long* status, uint32_t tile, uint32_t epoch, LookbackSmem& sm) {
-  constexpr int NW = NT / 32;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  unsigned long long acc = 0;
-  uint32_t base = 0;
-  while (true) {
-    const int64_t j = (int64_t)tile - 1 - base - tid;
-    uint32_t flag = 2, cnt = 0;
-    if (j >= 0) {
-      const unsigned long long w = ld_relaxed64(status + j);
-      flag = ((w >> 34) == epoch) ? (uint32_t)((w >> 32) & 3u) : 0u;
-      cnt = (uint32_t)w;
-    }
-    const unsigned r = __ballot_sync(0xffffffffu, flag != 0);
-    const unsigned q = __ballot_sync(0xffffffffu, flag == 2);
-    if (lane == 0) {
-      sm.ready[warp] = r;
-      sm.isp[warp] = q;
-    }
-    if (tid == 0) sm.sum = 0;
-    __syncthreads();
-    int prefix = 0, upto = -1;  // upto: index past the nearest P inside the ready prefix
-    for (int w = 0; w < NW; ++w) {
-      const unsigned rw = sm.ready[w];
-      const int pw = (~rw) ? __ffs(~rw) - 1 : 32;
-      const unsigned pm = sm.isp[w] & (pw == 32 ? 0xffffffffu : ((1u << pw) - 1));
-      if (pm) {
-        upto = prefix + __ffs(pm);
-        break;
-      }
-      prefix += pw;
-      if (pw < 32) break;
-    }
-    const bool slide = upto < 0 && prefix == NT;
-    const int take = upto >= 0 ? upto : (slide ? NT : 0);
-    unsigned long long v = (tid < take) ? cnt : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && v) atomicAdd(&sm.sum, v);
-    __syncthreads();
-    acc += sm.sum;
-    __syncthreads();
-    if (upto >= 0) return acc;
-    if (slide) base += NT;
-    else __nanosleep(32);
-  }
-}
 
 // Philox4x32-10 counter-based RNG (Salmon et al., SC'11).
 struct Philox {

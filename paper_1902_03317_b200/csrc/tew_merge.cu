@@ -316,18 +316,6 @@ __device__ __forceinline__ int pad64(int i) { return i + (i >> 4); }
 //     stores, frees the emission buffer.
 // So load latency hides behind the previous tile's merge, and look-back
 // latency behind the next tile's merge.
-#ifdef SPT_PHASES
-__device__ unsigned long long g_ph[65536 * 8];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define SPT_PH(tile, k) \
-  if ((tile) < 65536) g_ph[(size_t)(tile) * 8 + (k)] = gtime();
-#else
-#define SPT_PH(tile, k)
-#endif
 #ifndef SPT_MERGE_STAGES
 #define SPT_MERGE_STAGES 1
 #endif
@@ -528,9 +516,6 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
           spt::st_stream(p.zi[q] + base + o, (uint32_t)((k >> p.shift[q]) & p.mask[q]));
         spt::st_stream(reinterpret_cast<uint32_t*>(p.zv) + base + o, ev[epad(o)]);
       }
-#ifdef SPT_PHASES
-      if (lane == 0) SPT_PH(tile, 5);
-#endif
       spt::mbar_arrive(eempty + b);
     }
     return;
@@ -546,26 +531,13 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
       const uint32_t tile = slot[r].tile, tile_total = slot[r].total;
       unsigned long long base = 0;
       if (tile != kDone) {
-#ifdef SPT_PHASES
-        if (lane == 0 && tile < 65536) g_ph[(size_t)tile * 8 + 0] = gtime();
-#endif
         if (tile != 0) {
-#ifdef SPT_PHASES
-          uint32_t stats[3];
-          base = spt::lookback_count64_wide<8, kSS>(p.status, tile, p.epoch, stats);
-          if (lane == 0 && tile < 65536)
-            g_ph[(size_t)tile * 8 + 6] = ((unsigned long long)stats[0] << 32) | stats[2];
-#else
           base = spt::lookback_count64_wide<8, kSS>(p.status, tile, p.epoch);
-#endif
           if (lane == 0)
             spt::st_relaxed64(p.status + ((size_t)tile << kSS),
                               tag | (kFlagP << 32) | (base + tile_total));
         }
         if (lane == 0 && tile == p.ntiles - 1) *p.total = base + tile_total;
-#ifdef SPT_PHASES
-        if (lane == 0) SPT_PH(tile, 4);
-#endif
       }
       if (lane == 0) {
         slot[r].base = base;
@@ -603,9 +575,6 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
   };
   for (uint32_t it = 0;; ++it) {
     const int s = it % kStages;
-#ifdef SPT_PHASES
-    const unsigned long long t_w0 = gtime();
-#endif
     spt::mbar_wait(full + s, (it / kStages) & 1u);
     const StageInfo& inf = info[s];
     const uint32_t tile = inf.tile;
@@ -623,13 +592,6 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
       }
       break;
     }
-#ifdef SPT_PHASES
-    if (tid == 0 && tile < 65536) {
-      (void)t_w0;
-      g_ph[(size_t)tile * 8 + 7] = blockIdx.x;
-      SPT_PH(tile, 1);
-    }
-#endif
     const int nxt = static_cast<int>(inf.nxt), nyt = static_cast<int>(inf.nyt);
     const unsigned long long x_before = inf.x_before, y_after = inf.y_after;
     const int len = nxt + nyt;
@@ -661,9 +623,6 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
     __syncwarp();
     if (lane == 0) spt::mbar_arrive(empty + s);  // this warp is done with the stage
     bar_sync(1, kThreads);
-#ifdef SPT_PHASES
-    if (tid == 0) SPT_PH(tile, 2);
-#endif
 
     const int dg = std::min(tid * kIPT, len);
     int lo = std::max(0, dg - nyt), hi = std::min(dg, nxt);
@@ -736,9 +695,6 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
       slot[r].total = tile_total;
       spt::mbar_arrive(lbfull + r);
     }
-#ifdef SPT_PHASES
-    if (tid == 0) SPT_PH(tile, 3);
-#endif
     if (it > 0) flush(it - 1);
 #pragma unroll
     for (int k = 0; k < kIPT; ++k) {
@@ -796,12 +752,6 @@ int launch(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
 }
 
 }  // namespace
-
-#ifdef SPT_PHASES
-extern "C" SPT_API int spt_debug_phases(void* host, size_t bytes) {
-  return cudaMemcpyFromSymbol(host, g_ph, std::min(bytes, sizeof(g_ph))) == cudaSuccess ? 0 : 5;
-}
-#endif
 
 extern "C" int spt_tew_f32(spt_ctx* ctx, const spt_coo* x, const spt_coo* y, int op, spt_coo* z,
                            uint64_t z_capacity, uint64_t* h_nnz, uint64_t* d_nnz, unsigned flags,
