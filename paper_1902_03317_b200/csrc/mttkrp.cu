@@ -595,6 +595,504 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
 }
 
 // ---------------------------------------------------------------------------
+// Persistent segmented MTTKRP with an asynchronous tile fold (16-byte-aligned
+// inputs, > 4M nnz). CTA = 8 gather warps + 1 fold warp, resident for the
+// whole launch:
+//   * gather warps stream their 256-entry slice of each tile through a
+//     per-warp cp.async ring (no CTA staging barrier), gather and accumulate
+//     exactly as mttkrp_seg_kernel does, fold their P groups, write the rows
+//     complete inside the warp and hand the warp's first/last-row partials to
+//     the fold warp -- then move straight on to the next tile;
+//   * the fold warp takes tile tickets (in order, 4 ahead), folds the 8
+//     warps' partials, zero-fills the gaps, publishes the tail partial and
+//     runs the decoupled look-back for the head row, writing the tile's
+//     boundary rows -- while the gather warps already work on the next tile.
+// The end-of-tile CTA barriers of the non-persistent kernel (about a fifth of
+// its time on the Zipf configs) disappear from the gather warps' path.
+constexpr int kPfRingD = 3;
+#ifndef SPT_PF_TICKETS
+#define SPT_PF_TICKETS 4
+#endif
+constexpr int kPfTickets = SPT_PF_TICKETS;
+#ifndef SPT_PF_CBUF
+#define SPT_PF_CBUF 4
+#endif
+constexpr int kPfCBuf = SPT_PF_CBUF;  // tiles of fold slack for the gather warps
+constexpr int kPfThreads = kThreads + 32;
+
+__device__ __forceinline__ void pf_cp_async(void* dst, const void* src, int bytes,
+                                            int src_bytes) {
+  const uint32_t d = spt::smem_addr(dst);
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void pf_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void pf_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int NM1, int G, int VEC>
+struct PfShape {
+  static constexpr int P = 32 / G;
+  static constexpr int CB = G * VEC;
+  static constexpr int kU = (NM1 * VEC <= 12) ? 4 : 2;
+  static constexpr int NA = 2 + NM1;
+  static constexpr int EG = kTile / kWarps / P;  // entries per group
+  static constexpr int NB = EG / kU;              // batches per group
+  static constexpr int kSlotW = NA * P * kU;      // ring words per batch (warp)
+  static constexpr size_t ring = (size_t)kWarps * kPfRingD * kSlotW * 4;
+  static constexpr size_t gslot = (size_t)kWarps * 2 * P * CB * 8;
+  static constexpr size_t cslot = (size_t)kPfCBuf * 2 * kWarps * CB * 8;
+  static constexpr size_t smem = gslot + cslot + ring;
+};
+
+template <int NM1, int G, int VEC>
+__global__ void __launch_bounds__(kPfThreads, 3) mttkrp_pf_kernel(MttkrpParams p, uint32_t nctas) {
+  using S = PfShape<NM1, G, VEC>;
+  constexpr int P = S::P, CB = S::CB, kU = S::kU, NA = S::NA, EG = S::EG, NB = S::NB;
+  constexpr int NSL = 2 * kWarps;  // CTA slots per tile: head/tail of each warp
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_gslot = reinterpret_cast<double*>(smem_raw);               // [kWarps][2P][CB]
+  double* s_cslot = s_gslot + (size_t)kWarps * 2 * P * CB;             // [kPfCBuf][NSL][CB]
+  uint32_t* s_ring = reinterpret_cast<uint32_t*>(s_cslot + kPfCBuf * NSL * CB);
+  __shared__ uint32_t s_grow[kWarps][2 * P];
+  __shared__ uint32_t s_crow[kPfCBuf][NSL];
+  __shared__ uint32_t s_ticket[kPfTickets];
+  __shared__ __align__(8) unsigned long long s_bar[2 * kPfTickets + 2 * kPfCBuf];
+  unsigned long long* tfull = s_bar;                 // [4] ticket published (count 1)
+  unsigned long long* tempty = s_bar + kPfTickets;   // [4] ticket read by all gather warps (8)
+  unsigned long long* cfull = s_bar + 2 * kPfTickets;  // [kPfCBuf] slots written (256 threads)
+  unsigned long long* cempty = cfull + kPfCBuf;        // [kPfCBuf] slots folded (32 lanes)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int r = 0; r < kPfTickets; ++r) {
+      spt::mbar_init(tfull + r, 1);
+      spt::mbar_init(tempty + r, kWarps);
+    }
+    for (int b = 0; b < kPfCBuf; ++b) {
+      spt::mbar_init(cfull + b, kThreads);
+      spt::mbar_init(cempty + b, 32);
+    }
+    spt::mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == kWarps) {
+    // ================= fold warp =================
+    bool got_end = false;
+    auto fetch = [&]() -> uint32_t {
+      unsigned long long t = 0;
+      if (lane == 0) {
+        t = atomicAdd(p.tile_ctr, 1ull);
+        if (t == (unsigned long long)p.ntiles + nctas - 1) atomicExch(p.tile_ctr, 0ull);
+      }
+      return static_cast<uint32_t>(__shfl_sync(0xffffffffu, t, 0));
+    };
+    for (int r = 0; r < kPfTickets; ++r) {
+      uint32_t t = p.ntiles;
+      if (!got_end) {
+        t = fetch();
+        got_end = t >= p.ntiles;
+      }
+      if (lane == 0) {
+        s_ticket[r] = t;
+        spt::mbar_arrive(tfull + r);
+      }
+    }
+    const uint32_t tag = p.epoch << 3;
+    for (uint32_t i = 0;; ++i) {
+      const int r = i % kPfTickets, cb = i % kPfCBuf;
+      const uint32_t tile = s_ticket[r];
+      if (tile >= p.ntiles) break;
+      const uint64_t t0 = (uint64_t)tile * kTile;
+      const uint32_t cnt = static_cast<uint32_t>(std::min<uint64_t>(kTile, p.nnz - t0));
+      // neighbours (issued before the wait, consumed after it)
+      const uint32_t prev_row = tile > 0 ? __ldg(p.out_idx + t0 - 1) : kNone;
+      const uint32_t next_row = t0 + cnt < p.nnz ? __ldg(p.out_idx + t0 + cnt) : kNone;
+      spt::mbar_wait(cfull + cb, (i / kPfCBuf) & 1u);
+      const double* cs = s_cslot + (size_t)cb * NSL * CB;
+      const uint32_t* crow = s_crow[cb];
+      uint32_t head_row = kNone, tail_row = kNone;
+      for (int s = 0; s < NSL; ++s) {
+        const uint32_t rw = crow[s];
+        if (rw == kNone) continue;
+        if (head_row == kNone) head_row = rw;
+        tail_row = rw;
+      }
+      if (lane == 0) {
+        if (prev_row != kNone && prev_row > head_row) atomicMin(p.err + 2, (unsigned long long)t0);
+        if (next_row != kNone && next_row < tail_row)
+          atomicMin(p.err + 2, (unsigned long long)(t0 + cnt));
+      }
+      const bool cont_prev = prev_row == head_row;
+      const bool cont_next = next_row == tail_row;
+      const bool boundary = head_row != tail_row;
+      bool ext = false;  // interior tile whose predecessor already published P
+      if (cont_prev && cont_next && !boundary) {
+        uint32_t sp = lane == 0 ? spt::ld_relaxed(p.status + tile - 1) : 0u;
+        sp = __shfl_sync(0xffffffffu, sp, 0);
+        ext = (sp >> 3) == p.epoch && (sp & 3u) == kFlagP;
+        if (ext) __threadfence();  // acquire: the predecessor's payload is visible
+      }
+      for (int c = lane; c < CB; c += 32) {
+        const bool cok = static_cast<uint32_t>(c) < p.ncols;
+        const uint32_t col = p.c0 + c;
+        // fold of the warps' first/last-row partials (rows complete here)
+        double head_acc = 0.0, tail_acc = 0.0, cur = 0.0;
+        uint32_t cur_row = kNone;
+        int cur_w = -1;
+        for (int s = 0; s < NSL; ++s) {
+          const uint32_t rw = crow[s];
+          if (rw == kNone) continue;
+          const double v = cs[s * CB + c];
+          if (rw == cur_row) {
+            cur += v;
+          } else {
+            if (cur_row != kNone) {
+              if (cur_row == head_row) head_acc = cur;
+              else if (cok) __stcs(p.out + (size_t)cur_row * p.R + col, (float)cur);
+              if ((s >> 1) != cur_w && rw > cur_row + 1 && cok)
+                for (uint32_t z = cur_row + 1; z < rw; ++z) __stcs(p.out + (size_t)z * p.R + col, 0.0f);
+            }
+            cur_row = rw;
+            cur = v;
+          }
+          cur_w = s >> 1;
+        }
+        if (cur_row == head_row) head_acc = cur;
+        else tail_acc = cur;
+        if (!boundary) tail_acc = head_acc;
+        // inter-tile zero fill
+        if (cok) {
+          if (tile == 0)
+            for (uint32_t z = 0; z < head_row; ++z) __stcs(p.out + (size_t)z * p.R + col, 0.0f);
+          const uint32_t stop = next_row == kNone ? p.rows : next_row;
+          for (uint32_t z = tail_row + 1; z < stop; ++z) __stcs(p.out + (size_t)z * p.R + col, 0.0f);
+        }
+        // publish this tile's tail partial for successors; a tile strictly
+        // inside a long row extends its predecessor's inclusive prefix when
+        // that is already there (no waiting), which keeps the walk of the
+        // row's last tile short
+        if (cont_next) {
+          const bool incl = boundary || !cont_prev || ext;
+          double v = boundary || !cont_prev ? tail_acc : head_acc;
+          if (ext) v += spt::ld_cg(p.payP + (size_t)(tile - 1) * CB + c);
+          (incl ? p.payP : p.payA)[(size_t)tile * CB + c] = v;
+        }
+      }
+      if (cont_next) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0)
+          spt::st_release(p.status + tile,
+                          tag | ((boundary || !cont_prev || ext) ? kFlagP : kFlagA));
+      }
+      uint32_t n_chain = 0;
+      if (cont_prev && (boundary || !cont_next)) n_chain = spt::lookback_chain(p.status, tile, p.epoch);
+      for (int c = lane; c < CB; c += 32) {
+        const bool cok = static_cast<uint32_t>(c) < p.ncols;
+        const uint32_t col = p.c0 + c;
+        // head/tail partials again (same fold, no stores) -- cheaper than
+        // keeping CB/32 pairs of doubles per lane across the look-back
+        double head_acc = 0.0, tail_acc = 0.0, cur = 0.0;
+        uint32_t cur_row = kNone;
+        for (int s = 0; s < NSL; ++s) {
+          const uint32_t rw = crow[s];
+          if (rw == kNone) continue;
+          const double v = cs[s * CB + c];
+          if (rw == cur_row) {
+            cur += v;
+          } else {
+            if (cur_row == head_row) head_acc = cur;
+            cur_row = rw;
+            cur = v;
+          }
+        }
+        if (cur_row == head_row) head_acc = cur;
+        else tail_acc = cur;
+        // chain sum, 8 independent partials so the loads overlap (a row
+        // spanning thousands of tiles makes this walk long)
+        const uint32_t nq = std::min<uint32_t>(n_chain, tile);
+        double part[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        uint32_t q = 1;
+        for (; q + 7 < nq; q += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            part[u] += spt::ld_cg(p.payA + (size_t)(tile - q - u) * CB + c);
+        }
+        for (; q <= nq; ++q)
+          part[0] += spt::ld_cg((q == n_chain ? p.payP : p.payA) + (size_t)(tile - q) * CB + c);
+        const double carry = ((part[0] + part[1]) + (part[2] + part[3])) +
+                             ((part[4] + part[5]) + (part[6] + part[7]));
+        if (cok) {
+          if (boundary || !cont_next)
+            __stcs(p.out + (size_t)head_row * p.R + col, (float)(carry + head_acc));
+          if (boundary && !cont_next) __stcs(p.out + (size_t)tail_row * p.R + col, (float)tail_acc);
+        }
+      }
+      __syncwarp();
+      spt::mbar_arrive(cempty + cb);
+      // refill this ticket slot for the CTA's tile i + kPfTickets
+      spt::mbar_wait(tempty + r, (i / kPfTickets) & 1u);
+      uint32_t t = p.ntiles;
+      if (!got_end) {
+        t = fetch();
+        got_end = t >= p.ntiles;
+      }
+      if (lane == 0) {
+        s_ticket[r] = t;
+        spt::mbar_arrive(tfull + r);
+      }
+    }
+    return;
+  }
+
+  // ================= gather warps =================
+  const int gw = lane / G, gl = lane % G;
+  const uint32_t lcol = gl * VEC;
+  const bool col_ok = lcol < p.ncols;
+  const uint32_t col = p.c0 + lcol;
+  const char* fbase[NM1];
+#pragma unroll
+  for (int j = 0; j < NM1; ++j)
+    fbase[j] = reinterpret_cast<const char*>(p.ofac[j] + (col_ok ? col : p.c0));
+  const uint32_t rstride = p.R * 4u;
+  double* my_gslot = s_gslot + (size_t)warp * (2 * P) * CB;
+  uint32_t* my_grow = s_grow[warp];
+  uint32_t* my_ring = s_ring + (size_t)warp * kPfRingD * S::kSlotW;
+  const int wbase = warp * P * EG;
+
+  for (uint32_t i = 0;; ++i) {
+    const int r = i % kPfTickets;
+    spt::mbar_wait(tfull + r, (i / kPfTickets) & 1u);
+    const uint32_t tile = s_ticket[r];
+    __syncwarp();
+    if (lane == 0) spt::mbar_arrive(tempty + r);
+    if (tile >= p.ntiles) break;
+    const uint64_t t0 = (uint64_t)tile * kTile;
+    const int cnt = static_cast<int>(std::min<uint64_t>(kTile, p.nnz - t0));
+    // batch k of every group of this warp: lane c < NA*P (two roles when
+    // NA*P > 32) copies array c/P of group c%P; source and destination are
+    // fixed per tile, so a batch costs one address add and one cp.async
+    constexpr int kRoles = (NA * P + 31) / 32;
+    const uint32_t* rsrc[kRoles];
+    int rrem[kRoles], rdst[kRoles];
+#pragma unroll
+    for (int q = 0; q < kRoles; ++q) {
+      const int c = lane + 32 * q;
+      const int a = c / P, g = c % P;
+      const uint32_t* src = a == 0 ? p.out_idx : reinterpret_cast<const uint32_t*>(p.val);
+#pragma unroll
+      for (int j = 0; j < NM1; ++j)
+        if (a == 2 + j) src = p.oidx[j];
+      const int ee = wbase + g * EG;
+      rsrc[q] = src + t0 + ee;
+      rrem[q] = c < NA * P ? cnt - ee : -1;  // -1: no role
+      rdst[q] = a * P * kU + g * kU;
+    }
+    auto issue = [&](int k) {
+      if (k < NB) {
+#pragma unroll
+        for (int q = 0; q < kRoles; ++q) {
+          if (rrem[q] < 0 && lane + 32 * q >= NA * P) continue;
+          const int rem = rrem[q] - k * kU;
+          const int sb = rem >= kU ? kU * 4 : (rem > 0 ? rem * 4 : 0);
+          pf_cp_async(my_ring + (k % kPfRingD) * S::kSlotW + rdst[q],
+                      sb > 0 ? rsrc[q] + k * kU : p.out_idx, kU * 4, sb);
+        }
+      }
+      pf_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < kPfRingD - 1; ++k) issue(k);
+
+    const int e_begin = wbase + gw * EG;
+    const int e_end = min(e_begin + EG, cnt);
+    if (gl == 0) {
+      my_grow[2 * gw] = kNone;
+      my_grow[2 * gw + 1] = kNone;
+    }
+    uint32_t run_row = kNone;
+    bool first_run = true;
+    double acc[VEC];
+    float a32[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      acc[q] = 0.0;
+      a32[q] = 0.0f;
+    }
+    for (int k = 0; k < NB; ++k) {
+      const int e = e_begin + k * kU;
+      __syncwarp();  // every lane is done with the slot about to be refilled
+      issue(k + kPfRingD - 1);
+      pf_wait<kPfRingD - 1>();
+      __syncwarp();  // batch k (copied by several lanes) is visible
+      const uint32_t* slot = my_ring + (k % kPfRingD) * S::kSlotW + gw * kU;
+      uint32_t rr[kU], ix[NM1][kU];
+      float vv[kU];
+      ld_batch<kU>(slot, rr);
+      ld_batch<kU>(slot + P * kU, reinterpret_cast<uint32_t(&)[kU]>(vv));
+#pragma unroll
+      for (int j = 0; j < NM1; ++j) ld_batch<kU>(slot + (2 + j) * P * kU, ix[j]);
+      const bool full = e + kU <= e_end;
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (e + u >= e_end) rr[u] = kNone;
+      float f[kU][NM1][VEC];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int j = 0; j < NM1; ++j)
+          Vec<VEC>::load(reinterpret_cast<const float*>(fbase[j] + (size_t)ix[j][u] * rstride),
+                         f[u][j]);
+      float prod[kU][VEC];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          float t = vv[u];
+#pragma unroll
+          for (int j = 0; j < NM1; ++j) t = __fmul_rn(t, f[u][j][q]);
+          prod[u][q] = t;
+        }
+      bool same = full && rr[0] == run_row;
+#pragma unroll
+      for (int u = 1; u < kU; ++u) same = same && rr[u] == run_row;
+      if (same) {
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          float s = prod[0][q];
+#pragma unroll
+          for (int u = 1; u < kU; ++u) s += prod[u][q];
+          acc[q] += (double)s;
+        }
+        continue;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (rr[u] == kNone) continue;
+        const uint32_t row = rr[u];
+        if (row == run_row) {
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) a32[q] += prod[u][q];
+        } else {
+          if (run_row != kNone) {
+            if (row < run_row && gl == 0) atomicMin(p.err + 2, (unsigned long long)(t0 + e + u));
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[q] += (double)a32[q];
+            if (first_run) {
+              if (gl == 0) my_grow[2 * gw] = run_row;
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) my_gslot[(2 * gw) * CB + lcol + q] = acc[q];
+              first_run = false;
+            } else if (col_ok) {
+              float o[VEC];
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) o[q] = (float)acc[q];
+              Vec<VEC>::store(p.out + (size_t)run_row * p.R + col, o);
+            }
+            if (row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
+          }
+          run_row = row;
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) {
+            acc[q] = 0.0;
+            a32[q] = prod[u][q];
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        acc[q] += (double)a32[q];
+        a32[q] = 0.0f;
+      }
+    }
+    if (run_row != kNone) {
+      const int sl = 2 * gw + (first_run ? 0 : 1);
+      if (gl == 0) my_grow[sl] = run_row;
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) my_gslot[sl * CB + lcol + q] = acc[q];
+    }
+    __syncwarp();
+    // ---- warp fold of the P groups (as mttkrp_seg_kernel)
+    uint32_t w_cur = kNone, h_row = kNone;
+    int cur_g = -1;
+    double w_acc[VEC], h_acc[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) w_acc[q] = h_acc[q] = 0.0;
+    const bool writer = gw == 0 && col_ok;
+#pragma unroll 1
+    for (int g = 0; g < P; ++g) {
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int sl = 2 * g + it;
+        const uint32_t row = my_grow[sl];
+        if (row == kNone) continue;
+        double v[VEC];
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) v[q] = my_gslot[sl * CB + lcol + q];
+        if (row == w_cur) {
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) w_acc[q] += v[q];
+        } else {
+          if (w_cur != kNone) {
+            if (h_row == kNone) {
+              h_row = w_cur;
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) h_acc[q] = w_acc[q];
+            } else if (writer) {
+              float o[VEC];
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) o[q] = (float)w_acc[q];
+              Vec<VEC>::store(p.out + (size_t)w_cur * p.R + col, o);
+            }
+            if (g != cur_g && row > w_cur + 1 && writer)
+              zero_rows<VEC>(p.out, w_cur + 1, row, p.R, col, true);
+          }
+          w_cur = row;
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) w_acc[q] = v[q];
+        }
+        cur_g = g;
+      }
+    }
+    uint32_t t_row = kNone;
+    if (h_row == kNone) {
+      h_row = w_cur;
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) h_acc[q] = w_acc[q];
+    } else {
+      t_row = w_cur;
+    }
+    // ---- hand the warp's first/last-row partials to the fold warp
+    const int cb = i % kPfCBuf;
+    if (i >= kPfCBuf) spt::mbar_wait(cempty + cb, ((i / kPfCBuf) - 1) & 1u);
+    double* cs = s_cslot + (size_t)cb * NSL * CB;
+    if (gw == 0) {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        cs[(2 * warp) * CB + lcol + q] = h_acc[q];
+        cs[(2 * warp + 1) * CB + lcol + q] = w_acc[q];
+      }
+    }
+    if (lane == 0) {
+      s_crow[cb][2 * warp] = h_row;
+      s_crow[cb][2 * warp + 1] = t_row;
+    }
+    spt::mbar_arrive(cfull + cb);
+  }
+  pf_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
 // Warp-tile variant of the segmented MTTKRP: every warp is an independent
 // tile of kWT consecutive entries with its own shared-memory slice, its own
 // head/tail partials and its own decoupled look-back -- no CTA barrier, so a
@@ -990,6 +1488,39 @@ KernelFn pick_atomic(int nm1) {
   }
 }
 
+using KernelFnP = void (*)(MttkrpParams, uint32_t);
+struct PfVariant {
+  KernelFnP fn;
+  size_t smem;
+};
+template <int G, int VEC>
+PfVariant pick_pf(int nm1) {
+  switch (nm1) {
+#define SPT_PF_CASE(n) \
+  case n: return {mttkrp_pf_kernel<n, G, VEC>, PfShape<n, G, VEC>::smem};
+    SPT_PF_CASE(1)
+    SPT_PF_CASE(2)
+    SPT_PF_CASE(3)
+    SPT_PF_CASE(4)
+    SPT_PF_CASE(5)
+    SPT_PF_CASE(6)
+#undef SPT_PF_CASE
+    default: return {mttkrp_pf_kernel<7, G, VEC>, PfShape<7, G, VEC>::smem};
+  }
+}
+PfVariant choose_pf(int G, int VEC, int nm1) {
+  if (VEC == 4) {
+    switch (G) {
+      case 2: return pick_pf<2, 4>(nm1);
+      case 4: return pick_pf<4, 4>(nm1);
+      case 8: return pick_pf<8, 4>(nm1);
+      case 16: return pick_pf<16, 4>(nm1);
+      default: return pick_pf<32, 4>(nm1);
+    }
+  }
+  return pick_pf<32, 1>(nm1);
+}
+
 struct Variant {
   int G, VEC;
   KernelFn seg, atomic;
@@ -1251,6 +1782,33 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
   }
   const uint64_t ntiles = (x->nnz + kTile - 1) / kTile;
   p.ntiles = static_cast<uint32_t>(ntiles);
+#ifndef SPT_MTTKRP_PF
+#define SPT_MTTKRP_PF 1
+#endif
+  if (SPT_MTTKRP_PF && p.vec_ok) {
+    // persistent CTAs with the asynchronous tile fold
+    const PfVariant pv = choose_pf(v.G, v.VEC, nm1);
+    SPT_CUDA(cudaFuncSetAttribute(pv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(pv.smem)));
+    int per_sm = 0;
+    SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pv.fn, kPfThreads, pv.smem));
+    const uint32_t nctas = static_cast<uint32_t>(
+        std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)std::max(per_sm, 1) * ctx->num_sms)));
+    for (uint32_t c0 = 0; c0 < R; c0 += CB) {
+      uint32_t epoch;
+      SPT_TRY(spt::ctx_lookback(ctx, ntiles, 2 * ntiles * CB, &epoch));
+      p.status = ctx->d_status;
+      p.payA = ctx->d_payload;
+      p.payP = ctx->d_payload + ntiles * CB;
+      p.epoch = epoch;
+      p.c0 = c0;
+      p.ncols = static_cast<uint32_t>(std::min<uint64_t>(CB, R - c0));
+      pv.fn<<<nctas, kPfThreads, pv.smem, st>>>(p, nctas);
+      SPT_LAUNCHED(ctx);
+    }
+    if (flags & SPT_FLAG_ASYNC) return SPT_OK;
+    return spt::sync_and_check(ctx, st);
+  }
   SPT_CUDA(cudaFuncSetAttribute(v.seg, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(v.smem)));
   for (uint32_t c0 = 0; c0 < R; c0 += CB) {
