@@ -1720,10 +1720,10 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
   if (strategy < SPT_MTTKRP_SEGMENTED || strategy > SPT_MTTKRP_SEGMENTED_WARP)
     return spt::set_error(SPT_EINVAL, "mttkrp: unknown strategy %d", strategy);
   // Warp tiles win in the latency-bound small-problem regime (C1: 1M nnz,
-  // -17%); 2048-entry CTA tiles win at scale (fewer look-back chains on
-  // short Zipf rows).
+  // 29 vs 37 us); from ~2M nnz the persistent CTA-tile kernel wins (4M: 82 vs
+  // 94 us, C4 shape at 8M: 301 vs 528 us).
   if (strategy == SPT_MTTKRP_SEGMENTED)
-    strategy = x->nnz <= (4ull << 20) ? SPT_MTTKRP_SEGMENTED_WARP : SPT_MTTKRP_SEGMENTED_CTA;
+    strategy = x->nnz <= 1500000 ? SPT_MTTKRP_SEGMENTED_WARP : SPT_MTTKRP_SEGMENTED_CTA;
 
   MttkrpParams p{};
   p.out_idx = x->idx[mode];
