@@ -268,6 +268,210 @@ __global__ void tile_fiber_kernel(const uint32_t* fptr, uint32_t nfibs, uint32_t
   if (gl == 0 && live) map[t] = lo + (ntrue > 0 ? ntrue - 1 : 0);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-tile TTV: every warp owns a tile of kWT = 256 consecutive entries (8
+// per lane) and does everything itself -- head flags from its slice of fptr,
+// fp32 terms, an fp64 segmented warp scan, staging of its fibers' outputs in
+// its own shared-memory slice, coalesced stores -- so no warp ever waits at a
+// CTA barrier. A fiber crossing a warp-tile boundary is completed by the tile
+// holding its last entry through the same epoch-tagged decoupled look-back
+// (scalar fp64 payloads); C3's short fibers rarely cross one. A CTA draws one
+// ticket for its 8 consecutive warp tiles, so predecessors are resident.
+constexpr int kWT = 256;
+constexpr int kWE = kWT / 32;  // entries per lane (blocked)
+
+template <int NO>
+constexpr size_t ttv_wt_slice() {
+  return (size_t)(kWT + 8) + (size_t)(kWT + 1) * 4 * (1 + NO);  // heads | zv | zi[NO]
+}
+
+template <int NO>
+#ifndef SPT_TTV_WT_MINB
+#define SPT_TTV_WT_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, SPT_TTV_WT_MINB) ttv_wt_kernel(TtvParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t s_ticket;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    const unsigned long long t = atomicAdd(p.tile_ctr, 1ull);
+    if (t == gridDim.x - 1) atomicExch(p.tile_ctr, 0ull);
+    s_ticket = static_cast<uint32_t>(t);
+  }
+  __syncthreads();  // the only CTA barrier
+  const uint32_t wt = s_ticket * (kThreads / 32) + warp;
+  if (wt >= p.ntiles) return;
+  unsigned char* base = smem_raw + warp * ((ttv_wt_slice<NO>() + 15) & ~size_t(15));
+  uint8_t* s_head = base;                                             // [kWT + 8]
+  float* s_zv = reinterpret_cast<float*>(base + kWT + 8);             // [kWT + 1]
+  uint32_t* s_zi = reinterpret_cast<uint32_t*>(s_zv + (kWT + 1));      // [NO][kWT + 1]
+  const uint64_t t0 = (uint64_t)wt * kWT;
+  const int cnt = (p.nnz - t0 < (uint64_t)kWT) ? static_cast<int>(p.nnz - t0) : kWT;
+  const uint32_t f_lo = __ldg(p.tile_fiber + wt);  // fiber containing entry t0
+
+  // ---- entries (issued first: the longest round trip)
+  const int e0 = lane * kWE;
+  uint32_t kk[kWE], oi[NO][kWE];
+  float val[kWE];
+  if (cnt == kWT && p.vec_ok) {
+#pragma unroll
+    for (int c = 0; c < kWE / 4; ++c) {
+      const uint4 k4 = spt::ld_stream(reinterpret_cast<const uint4*>(p.kidx + t0 + e0) + c);
+      const uint4 v4 = spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0 + e0) + c);
+      kk[4 * c] = k4.x, kk[4 * c + 1] = k4.y, kk[4 * c + 2] = k4.z, kk[4 * c + 3] = k4.w;
+      val[4 * c] = __uint_as_float(v4.x), val[4 * c + 1] = __uint_as_float(v4.y);
+      val[4 * c + 2] = __uint_as_float(v4.z), val[4 * c + 3] = __uint_as_float(v4.w);
+#pragma unroll
+      for (int d = 0; d < NO; ++d) {
+        const uint4 a = spt::ld_stream(reinterpret_cast<const uint4*>(p.hidx[d] + t0 + e0) + c);
+        oi[d][4 * c] = a.x, oi[d][4 * c + 1] = a.y, oi[d][4 * c + 2] = a.z, oi[d][4 * c + 3] = a.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kWE; ++i) {
+      const bool ok = e0 + i < cnt;
+      kk[i] = ok ? p.kidx[t0 + e0 + i] : 0u;
+      val[i] = ok ? p.val[t0 + e0 + i] : 0.0f;
+#pragma unroll
+      for (int d = 0; d < NO; ++d) oi[d][i] = ok ? p.hidx[d][t0 + e0 + i] : 0u;
+    }
+  }
+
+  // ---- head flags from fptr[f_lo ...]: at most kWT + 2 fiber starts matter
+  reinterpret_cast<uint2*>(s_head)[lane] = make_uint2(0u, 0u);
+  __syncwarp();
+  const uint64_t t_end = t0 + cnt;
+  uint64_t next_start = ~0ull;  // first fiber start >= t_end (this lane's share)
+#pragma unroll
+  for (int r = 0; r < (kWT + 2 + 31) / 32; ++r) {
+    const uint64_t f = (uint64_t)f_lo + lane + 32 * r;
+    if (f > p.nfibs) continue;
+    const uint64_t s = __ldg(p.fptr + f);
+    if (s >= t0 && s < t_end) s_head[s - t0] = 1;
+    if (s >= t_end && s < next_start) next_start = s;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t v = __shfl_xor_sync(0xffffffffu, next_start, o);
+    next_start = v < next_start ? v : next_start;
+  }
+  __syncwarp();
+
+  // ---- terms, segmented warp scan (fp64), local fiber ids
+  float term[kWE];
+  bool head[kWE];
+#pragma unroll
+  for (int i = 0; i < kWE; ++i) {
+    const bool ok = e0 + i < cnt;
+    term[i] = ok ? __fmul_rn(val[i], __ldg(p.v + kk[i])) : 0.0f;
+    head[i] = ok && s_head[e0 + i];
+  }
+  int nh = 0;  // heads in this lane
+  bool any = false;
+  double lsum = 0.0;  // sum since this lane's last head (or lane start)
+#pragma unroll
+  for (int i = 0; i < kWE; ++i) {
+    nh += head[i] ? 1 : 0;
+    if (head[i]) {
+      any = true;
+      lsum = (double)term[i];
+    } else {
+      lsum += (double)term[i];
+    }
+  }
+  // exclusive scan of (any-head, sum) and of the head counts
+  int hx = nh;
+  bool fx = any;
+  double sx = lsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int hv = __shfl_up_sync(0xffffffffu, hx, o);
+    const bool fv = __shfl_up_sync(0xffffffffu, fx ? 1 : 0, o) != 0;
+    const double sv = __shfl_up_sync(0xffffffffu, sx, o);
+    if (lane >= o) {
+      hx += hv;
+      if (!fx) sx += sv;  // combine(prev, mine): mine has no head -> prev + mine
+      fx = fx || fv;
+    }
+  }
+  // exclusive values for this lane = inclusive of lane - 1
+  int h_before = __shfl_up_sync(0xffffffffu, hx, 1);
+  double s_before = __shfl_up_sync(0xffffffffu, sx, 1);
+  if (lane == 0) {
+    h_before = 0;
+    s_before = 0.0;
+  }
+  const bool head0 = __shfl_sync(0xffffffffu, head[0] ? 1 : 0, 0) != 0;  // entry t0 starts a fiber
+  const bool cont_prev = !head0;
+  const bool cont_nx = next_start != t_end;  // the last fiber goes on past this tile
+  const int hc0 = head0 ? 1 : 0;
+  const int total_h = __shfl_sync(0xffffffffu, hx, 31);
+  const int last_lf = total_h - hc0;  // local id of the tile's last fiber
+  const bool single = last_lf == 0;
+  const double tile_tail = __shfl_sync(0xffffffffu, sx, 31);  // sum of the last fiber in this tile
+
+  // ---- publish the tail partial, then look back for the first fiber's carry
+  const uint32_t tag = p.epoch << 3;
+  if (cont_nx && lane == 0) {
+    if (!single || !cont_prev) {
+      p.payP[wt] = tile_tail;
+      __threadfence();
+      spt::st_release(p.status + wt, tag | kFlagP);
+    } else {
+      p.payA[wt] = tile_tail;
+      __threadfence();
+      spt::st_release(p.status + wt, tag | kFlagA);
+    }
+  }
+  double carry = 0.0;
+  if (cont_prev && !(single && cont_nx)) {
+    const uint32_t n = spt::lookback_chain(p.status, wt, p.epoch);
+    for (uint32_t q = 1 + lane; q <= n && q <= wt; q += 32)
+      carry += spt::ld_cg((q == n ? p.payP : p.payA) + (wt - q));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) carry += __shfl_xor_sync(0xffffffffu, carry, o);
+  }
+
+  // ---- stage outputs by local fiber id, then coalesced stores
+  int hcount = h_before;
+  double run = s_before;
+#pragma unroll
+  for (int i = 0; i < kWE; ++i) {
+    const int e = e0 + i;
+    if (e >= cnt) break;
+    hcount += head[i] ? 1 : 0;
+    run = head[i] ? (double)term[i] : run + (double)term[i];
+    const int lf = hcount - hc0;
+    if (head[i]) {
+#pragma unroll
+      for (int d = 0; d < NO; ++d) s_zi[d * (kWT + 1) + lf] = oi[d][i];
+    }
+    const bool ends = (e + 1 < cnt) ? s_head[e + 1] != 0 : !cont_nx;
+    if (ends) s_zv[lf] = (float)(run + (lf == 0 ? carry : 0.0));
+  }
+  __syncwarp();
+  const int end_hi = cont_nx ? last_lf : last_lf + 1;  // fibers [0, end_hi) end here
+  const int head_lo = cont_prev ? 1 : 0;            // fibers [head_lo, last_lf] start here
+  for (int o = lane; o < end_hi; o += 32)
+    spt::st_stream(reinterpret_cast<uint32_t*>(p.zval) + f_lo + o, __float_as_uint(s_zv[o]));
+#pragma unroll
+  for (int d = 0; d < NO; ++d)
+    for (int o = head_lo + lane; o <= last_lf; o += 32)
+      spt::st_stream(p.zidx[d] + f_lo + o, s_zi[d * (kWT + 1) + o]);
+}
+
+template <int NO>
+int launch_ttv_wt(spt_ctx* ctx, const TtvParams& p, cudaStream_t st) {
+  const size_t smem = (size_t)(kThreads / 32) * ((ttv_wt_slice<NO>() + 15) & ~size_t(15));
+  SPT_CUDA(cudaFuncSetAttribute(ttv_wt_kernel<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  const unsigned grid = static_cast<unsigned>((p.ntiles + kThreads / 32 - 1) / (kThreads / 32));
+  ttv_wt_kernel<NO><<<grid, kThreads, smem, st>>>(p);
+  SPT_LAUNCHED(ctx);
+  return SPT_OK;
+}
+
 template <int NO>
 int launch_ttv(spt_ctx* ctx, const TtvParams& p, unsigned grid, cudaStream_t st) {
   const size_t smem = (size_t)(NO + 1) * (kTile + 2) * sizeof(uint32_t);
@@ -336,10 +540,14 @@ extern "C" int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uin
   if (!z->val || !d_v) return spt::set_error(SPT_EINVAL, "ttv: null vector or output values");
 
   cudaStream_t st = spt::as_stream(stream);
-  const uint64_t ntiles = (x->nnz + kTile - 1) / kTile;
+#ifndef SPT_TTV_WARP_TILES
+#define SPT_TTV_WARP_TILES 1
+#endif
+  const uint32_t tile_entries = SPT_TTV_WARP_TILES ? kWT : kTile;
+  const uint64_t ntiles = (x->nnz + tile_entries - 1) / tile_entries;
   uint32_t* map;
   SPT_TRY(spt::ctx_scratch(ctx, ntiles * sizeof(uint32_t), reinterpret_cast<void**>(&map)));
-  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), kTile,
+  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), tile_entries,
                                     static_cast<uint32_t>(ntiles), map, st));
   uint32_t epoch;
   SPT_TRY(spt::ctx_lookback(ctx, ntiles, 2 * ntiles, &epoch));
@@ -368,6 +576,19 @@ extern "C" int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uin
   p.vec_ok = 1;
   for (uint32_t d = 0; d < N; ++d) p.vec_ok = p.vec_ok && spt::aligned16(x->idx[d]);
   p.vec_ok = p.vec_ok && spt::aligned16(x->val);
+  if (SPT_TTV_WARP_TILES) {
+    switch (N - 1) {
+      case 1: SPT_TRY(launch_ttv_wt<1>(ctx, p, st)); break;
+      case 2: SPT_TRY(launch_ttv_wt<2>(ctx, p, st)); break;
+      case 3: SPT_TRY(launch_ttv_wt<3>(ctx, p, st)); break;
+      case 4: SPT_TRY(launch_ttv_wt<4>(ctx, p, st)); break;
+      case 5: SPT_TRY(launch_ttv_wt<5>(ctx, p, st)); break;
+      case 6: SPT_TRY(launch_ttv_wt<6>(ctx, p, st)); break;
+      default: SPT_TRY(launch_ttv_wt<7>(ctx, p, st)); break;
+    }
+    (void)flags;
+    return SPT_OK;
+  }
   const unsigned grid = static_cast<unsigned>(ntiles);
   switch (N - 1) {
     case 1: SPT_TRY(launch_ttv<1>(ctx, p, grid, st)); break;
