@@ -1102,7 +1102,41 @@ __global__ void __launch_bounds__(kPfThreads, 3) mttkrp_pf_kernel(MttkrpParams p
 constexpr int kWT = 256;
 constexpr int kWTP = kWT + kWT / 8;  // padded (sw layout)
 
-template <int NM1, int G, int VEC>
+// TTM output index tuples of fiber `row` (head entry h) for NCOL columns at
+// col, head indices from the warp's staged copy when h lies in its tile.
+template <int NCOL>
+__device__ __forceinline__ void wt_emit_idx(const MttkrpParams& p, uint32_t h, uint32_t row,
+                                            uint32_t col, const uint32_t* s_hid, uint64_t t0) {
+  const size_t base = (size_t)row * p.R + col;
+  int j = 0;
+  for (uint32_t d = 0; d < p.N; ++d) {
+    uint32_t w[NCOL];
+    if (d == p.mode) {
+#pragma unroll
+      for (int k = 0; k < NCOL; ++k) w[k] = col + k;
+    } else {
+      const uint32_t hv = h >= t0 ? s_hid[j * kWTP + sw(static_cast<int>(h - t0))] : p.hidx[d][h];
+      ++j;
+#pragma unroll
+      for (int k = 0; k < NCOL; ++k) w[k] = hv;
+    }
+    if constexpr (NCOL == 4) {
+      __stcs(reinterpret_cast<uint4*>(p.zidx[d] + base), make_uint4(w[0], w[1], w[2], w[3]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < NCOL; ++k) __stcs(p.zidx[d] + base + k, w[k]);
+    }
+  }
+}
+
+// per-warp shared-memory slice of the warp-tile kernels
+template <int NM1, int G, int VEC, bool FIBER>
+__host__ __device__ constexpr size_t wt_slice(uint32_t n_modes) {
+  return (size_t)2 * (32 / G) * G * VEC * sizeof(double) + (size_t)(2 + NM1) * kWTP * 4 +
+         (FIBER ? (size_t)(kWT + 4) * 4 + (size_t)(n_modes - 1) * kWTP * 4 + (kWT + 16) : 0);
+}
+
+template <int NM1, int G, int VEC, bool FIBER = false>
 __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) {
   constexpr int P = 32 / G;
   constexpr int EG = kWT / P;
@@ -1110,12 +1144,16 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // per-warp slice: [2P][CB] doubles of group slots, then the staged entries
-  constexpr size_t kSlice = (size_t)2 * P * CB * sizeof(double) + (size_t)(2 + NM1) * kWTP * 4;
+  // (TTM adds the fiber offsets, the head index tuples and head flags)
+  const size_t kSlice = (wt_slice<NM1, G, VEC, FIBER>(p.N) + 15) & ~size_t(15);
   unsigned char* base = smem_raw + warp * kSlice;
   double* s_gslot = reinterpret_cast<double*>(base);
   uint32_t* s_out = reinterpret_cast<uint32_t*>(s_gslot + 2 * P * CB);
   float* s_val = reinterpret_cast<float*>(s_out + kWTP);
   uint32_t* s_oidx = reinterpret_cast<uint32_t*>(s_val + kWTP);
+  uint32_t* s_fp = s_oidx + NM1 * kWTP;           // FIBER: fptr[f_lo + i]
+  uint32_t* s_hid = s_fp + (kWT + 4);              // FIBER: [N-1][kWTP]
+  uint8_t* s_hd = reinterpret_cast<uint8_t*>(s_hid + (FIBER ? (p.N - 1) * kWTP : 0));
   __shared__ uint32_t s_ticket;
   __shared__ uint32_t s_grow_all[kWarps][64];
 
@@ -1136,8 +1174,9 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
 #pragma unroll
     for (int r = 0; r < kWT / 128; ++r) {
       const int i = lane + 32 * r;  // uint4 chunk
-      reinterpret_cast<uint4*>(s_out)[i + (i >> 3)] =
-          spt::ld_stream(reinterpret_cast<const uint4*>(p.out_idx + t0) + i);
+      if constexpr (!FIBER)
+        reinterpret_cast<uint4*>(s_out)[i + (i >> 3)] =
+            spt::ld_stream(reinterpret_cast<const uint4*>(p.out_idx + t0) + i);
       reinterpret_cast<uint4*>(s_val)[i + (i >> 3)] =
           spt::ld_stream(reinterpret_cast<const uint4*>(p.val + t0) + i);
 #pragma unroll
@@ -1148,7 +1187,7 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
   } else {
     for (int i = lane; i < kWT; i += 32) {
       const bool ok = i < cnt;
-      s_out[sw(i)] = ok ? p.out_idx[t0 + i] : 0u;
+      if constexpr (!FIBER) s_out[sw(i)] = ok ? p.out_idx[t0 + i] : 0u;
       s_val[sw(i)] = ok ? p.val[t0 + i] : 0.0f;
 #pragma unroll
       for (int j = 0; j < NM1; ++j) s_oidx[j * kWTP + sw(i)] = ok ? p.oidx[j][t0 + i] : 0u;
@@ -1156,10 +1195,62 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
   }
   // neighbours for the tile-level continuation tests (issued with the staging)
   uint32_t prev_row = kNone, next_row = kNone;
-  if (lane == 0 && t0 > 0) prev_row = p.out_idx[t0 - 1];
-  if (lane == 1 && t0 + cnt < p.nnz) next_row = p.out_idx[t0 + cnt];
-  prev_row = __shfl_sync(0xffffffffu, prev_row, 0);
-  next_row = __shfl_sync(0xffffffffu, next_row, 1);
+  uint32_t f_lo = 0;
+  if constexpr (!FIBER) {
+    if (lane == 0 && t0 > 0) prev_row = p.out_idx[t0 - 1];
+    if (lane == 1 && t0 + cnt < p.nnz) next_row = p.out_idx[t0 + cnt];
+    prev_row = __shfl_sync(0xffffffffu, prev_row, 0);
+    next_row = __shfl_sync(0xffffffffu, next_row, 1);
+  } else {
+    // TTM: rows are fiber ids. Head tuples of the tile's entries, the fptr
+    // slice of the fibers touching it, head flags, and each entry's fiber.
+    for (uint32_t j = 0; j + 1 < p.N; ++j)
+      for (int i = lane; i < kWT; i += 32)
+        s_hid[j * kWTP + sw(i)] = i < cnt ? p.hnm[j][t0 + i] : 0u;
+    f_lo = __ldg(p.tile_fiber + tile);
+    reinterpret_cast<uint2*>(s_hd)[lane] = make_uint2(0u, 0u);
+    __syncwarp();
+    const uint64_t t_end = t0 + cnt;
+    uint64_t next_start = ~0ull;
+#pragma unroll
+    for (int r = 0; r < (kWT + 2 + 31) / 32; ++r) {
+      const uint32_t i = lane + 32 * r;
+      const uint64_t f = (uint64_t)f_lo + i;
+      if (f > p.rows || i >= kWT + 4) continue;
+      const uint32_t st = __ldg(p.fptr + f);
+      s_fp[i] = st;
+      if (st >= t0 && st < t_end) s_hd[st - t0] = 1;
+      if (st >= t_end && st < next_start) next_start = st;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t v = __shfl_xor_sync(0xffffffffu, next_start, o);
+      next_start = v < next_start ? v : next_start;
+    }
+    __syncwarp();
+    constexpr int kPer = kWT / 32;
+    int nh = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) nh += (lane * kPer + q < cnt && s_hd[lane * kPer + q]) ? 1 : 0;
+    int incl = nh;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int head0 = __shfl_sync(0xffffffffu, (int)s_hd[0], 0);
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int hc = incl - nh;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int e = lane * kPer + q;
+      hc += (e < cnt && s_hd[e]) ? 1 : 0;
+      s_out[sw(e)] = e < cnt ? f_lo + (uint32_t)(hc - head0) : 0u;
+    }
+    const uint32_t last_fiber = f_lo + (uint32_t)(total - head0);
+    if (tile > 0) prev_row = head0 ? f_lo - 1 : f_lo;
+    if (t_end < p.nnz) next_row = next_start == t_end ? last_fiber + 1 : last_fiber;
+  }
   __syncwarp();
 
   // ---- per-group segmented accumulation (as in mttkrp_seg_kernel)
@@ -1247,6 +1338,7 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
 #pragma unroll
           for (int k = 0; k < VEC; ++k) o[k] = (float)acc[k];
           Vec<VEC>::store(p.out + (size_t)run_row * p.R + col, o);
+          if constexpr (FIBER) wt_emit_idx<VEC>(p, s_fp[run_row - f_lo], run_row, col, s_hid, t0);
         }
         if (row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
       }
@@ -1294,6 +1386,7 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
 #pragma unroll
             for (int k = 0; k < VEC; ++k) o[k] = (float)w_acc[k];
             Vec<VEC>::store(p.out + (size_t)w_cur * p.R + col, o);
+            if constexpr (FIBER) wt_emit_idx<VEC>(p, s_fp[w_cur - f_lo], w_cur, col, s_hid, t0);
           }
           if (g != cur_g && row > w_cur + 1 && writer)
             zero_rows<VEC>(p.out, w_cur + 1, row, p.R, col, true);
@@ -1382,12 +1475,14 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
 #pragma unroll
       for (int k = 0; k < VEC; ++k) o[k] = (float)(carry[k] + head_acc[k]);
       Vec<VEC>::store(p.out + (size_t)head_row * p.R + col, o);
+      if constexpr (FIBER) wt_emit_idx<VEC>(p, s_fp[head_row - f_lo], head_row, col, s_hid, t0);
     }
     if (boundary && !cont_next) {
       float o[VEC];
 #pragma unroll
       for (int k = 0; k < VEC; ++k) o[k] = (float)tail_acc[k];
       Vec<VEC>::store(p.out + (size_t)tail_row * p.R + col, o);
+      if constexpr (FIBER) wt_emit_idx<VEC>(p, s_fp[tail_row - f_lo], tail_row, col, s_hid, t0);
     }
   }
 }
@@ -1561,18 +1656,34 @@ struct TtmVariant {
   int G, VEC;
   KernelFn fn;
   size_t smem;
+  KernelFn wt;  // warp-tile TTM (same G/VEC)
 };
 
 TtmVariant choose_ttm(uint32_t R, bool aligned) {
+#define SPT_TTM_V(g, v) \
+  { g, v, mttkrp_seg_kernel<1, g, v, true>, ttm_smem<g, v>(), mttkrp_wt_kernel<1, g, v, true> }
   if (R % 4 == 0 && aligned) {
     const uint32_t q = R / 4;
-    if (q <= 2) return {2, 4, mttkrp_seg_kernel<1, 2, 4, true>, ttm_smem<2, 4>()};
-    if (q <= 4) return {4, 4, mttkrp_seg_kernel<1, 4, 4, true>, ttm_smem<4, 4>()};
-    if (q <= 8) return {8, 4, mttkrp_seg_kernel<1, 8, 4, true>, ttm_smem<8, 4>()};
-    if (q <= 16) return {16, 4, mttkrp_seg_kernel<1, 16, 4, true>, ttm_smem<16, 4>()};
-    return {32, 4, mttkrp_seg_kernel<1, 32, 4, true>, ttm_smem<32, 4>()};
+    if (q <= 2) return SPT_TTM_V(2, 4);
+    if (q <= 4) return SPT_TTM_V(4, 4);
+    if (q <= 8) return SPT_TTM_V(8, 4);
+    if (q <= 16) return SPT_TTM_V(16, 4);
+    return SPT_TTM_V(32, 4);
   }
-  return {32, 1, mttkrp_seg_kernel<1, 32, 1, true>, ttm_smem<32, 1>()};
+  return SPT_TTM_V(32, 1);
+#undef SPT_TTM_V
+}
+
+size_t ttm_wt_smem(int G, int VEC, uint32_t n_modes) {
+  const auto slice = [&](size_t s) { return (s + 15) & ~size_t(15); };
+  switch (VEC * 100 + G) {
+    case 402: return kWarps * slice(wt_slice<1, 2, 4, true>(n_modes));
+    case 404: return kWarps * slice(wt_slice<1, 4, 4, true>(n_modes));
+    case 408: return kWarps * slice(wt_slice<1, 8, 4, true>(n_modes));
+    case 416: return kWarps * slice(wt_slice<1, 16, 4, true>(n_modes));
+    case 432: return kWarps * slice(wt_slice<1, 32, 4, true>(n_modes));
+    default: return kWarps * slice(wt_slice<1, 32, 1, true>(n_modes));
+  }
 }
 
 }  // namespace
@@ -1623,10 +1734,16 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
   for (uint32_t d = 0; d < N; ++d) aligned = aligned && spt::aligned16(z->idx[d]);
   const TtmVariant v = choose_ttm(R, aligned);
   const uint32_t CB = v.G * v.VEC;
-  const uint64_t ntiles = (x->nnz + kTile - 1) / kTile;
+#ifndef SPT_TTM_WARP_TILES
+#define SPT_TTM_WARP_TILES 1
+#endif
+  // warp tiles (no CTA barrier) by default; per-CTA tiles kept for A/B
+  const bool wt = SPT_TTM_WARP_TILES != 0;
+  const uint32_t tile_entries = wt ? kWT : kTile;
+  const uint64_t ntiles = (x->nnz + tile_entries - 1) / tile_entries;
   uint32_t* map;
   SPT_TRY(spt::ctx_scratch(ctx, ntiles * sizeof(uint32_t), reinterpret_cast<void**>(&map)));
-  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), kTile,
+  SPT_TRY(spt::build_tile_fiber_map(ctx, d_fptr, static_cast<uint32_t>(nfibs), tile_entries,
                                     static_cast<uint32_t>(ntiles), map, st));
 
   MttkrpParams p{};
@@ -1650,8 +1767,12 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
   }
   p.N = N;
   p.mode = mode;
-  const size_t smem = v.smem + (size_t)(N - 1) * kTileP * sizeof(uint32_t);
-  SPT_CUDA(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const KernelFn fn = wt ? v.wt : v.fn;
+  const size_t smem = wt ? ttm_wt_smem(v.G, v.VEC, N)
+                         : v.smem + (size_t)(N - 1) * kTileP * sizeof(uint32_t);
+  const unsigned grid = wt ? static_cast<unsigned>((ntiles + kWarps - 1) / kWarps)
+                           : static_cast<unsigned>(ntiles);
+  SPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   for (uint32_t c0 = 0; c0 < R; c0 += CB) {
     uint32_t epoch;
@@ -1662,7 +1783,7 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
     p.epoch = epoch;
     p.c0 = c0;
     p.ncols = std::min<uint32_t>(CB, R - c0);
-    v.fn<<<static_cast<unsigned>(ntiles), kThreads, smem, st>>>(p);
+    fn<<<grid, kThreads, smem, st>>>(p);
     SPT_LAUNCHED(ctx);
   }
   (void)flags;
