@@ -62,7 +62,7 @@ def within_tol(got, y64, yabs, tol=TOL):
 
 def rand_tensor(rng, dims, nnz, lo=0.0, hi=1.0, sort=None):
     cap = int(np.prod([float(d) for d in dims]))
-    if cap < 4 * nnz:
+    if cap < 16 * nnz:
         lin = rng.choice(cap, size=nnz, replace=False)
     else:
         lin = np.unique(np.concatenate([
@@ -73,7 +73,8 @@ def rand_tensor(rng, dims, nnz, lo=0.0, hi=1.0, sort=None):
     for d in reversed(dims):
         idx.append((lin % d).astype(np.uint32))
         lin = lin // d
-    t = HostTensor(dims, idx[::-1], rng.uniform(lo, hi, nnz).astype(np.float32), None, True)
+    t = HostTensor(dims, idx[::-1], rng.uniform(lo, hi, len(idx[0])).astype(np.float32), None,
+                   True)
     if sort is not None:
         O.sort_lexicographic(t, sort)
     return t
@@ -427,3 +428,51 @@ def test_tew_matches_at_tile_edges(sp, nnz):
         got = host(ops.tew(dev(sp, x), dev(sp, y2), op))
         want, _ = O.tew(x.copy(), y2.copy(), op)
         assert same(got, want), ("identical", nnz, op)
+
+
+@pytest.mark.parametrize("offset", [0, 1])
+@pytest.mark.parametrize("strat", ["cta", "warp"])
+def test_mttkrp_tile_shapes_and_alignment(sp, offset, strat):
+    """The persistent CTA-tile kernel (aligned inputs), its per-CTA fallback
+    (unaligned views) and the warp-tile kernel, on partial tiles, rows that
+    cross many tiles and 4th-order Zipf-like rows."""
+    ops = sp[0]
+    s = {"cta": ops.MTTKRP_SEGMENTED_CTA, "warp": ops.MTTKRP_SEGMENTED_WARP}[strat]
+    rng = np.random.default_rng(17 + offset)
+    for dims, nnz, R in (([50, 40, 30, 20], 70_001, 32), ([7, 3000, 3000], 123_457, 12),
+                         ([2, 500, 400], 99_999, 16)):
+        x = rand_tensor(rng, dims, nnz)
+        fs = [rng.uniform(0, 1, (d, R)).astype(np.float32) for d in dims]
+        for mode in (0, len(dims) - 1):
+            xs = x.copy()
+            O.sort_lexicographic(xs, [mode] + [d for d in range(len(dims)) if d != mode])
+            _, o64, oab = O.mttkrp(xs, fs, mode)
+            out = ops.mttkrp(dev(sp, xs, offset), [torch.from_numpy(f).cuda() for f in fs], mode,
+                             s).cpu().numpy()
+            ok, worst = within_tol(out, o64, oab)
+            assert ok, (dims, mode, worst)
+
+
+@pytest.mark.parametrize("R", [3, 8, 20, 64])
+def test_ttv_ttm_warp_tiles_orders(sp, R):
+    """Warp-tile TTV/TTM at orders 2-4, ragged warp tiles, fibers of every
+    length from 1 to thousands, and R that is not a multiple of 4."""
+    ops = sp[0]
+    rng = np.random.default_rng(R + 101)
+    for dims, nnz in (([3000, 40], 50_003), ([30, 40, 2000], 77_777), ([9, 8, 7, 600], 123_001)):
+        x = rand_tensor(rng, dims, nnz, -1, 1)
+        N = len(dims)
+        for mode in range(N):
+            xs = x.copy()
+            O.sort_lexicographic(xs, [d for d in range(N) if d != mode] + [mode])
+            dx = dev(sp, xs)
+            v = rng.uniform(-1, 1, dims[mode]).astype(np.float32)
+            zt, y64, yab = O.ttv(xs, v, mode)
+            g = host(ops.ttv(dx, torch.from_numpy(v).cuda(), mode))
+            assert same(HostTensor(g.dims, g.indices, zt.values, g.sort_order, g.coalesced), zt)
+            assert within_tol(g.values, y64, yab)[0], (dims, mode)
+            u = rng.uniform(-1, 1, (dims[mode], R)).astype(np.float32)
+            zm, y64, yab = O.ttm(xs, u, mode)
+            g = host(ops.ttm(dx, torch.from_numpy(u).cuda(), mode))
+            assert same(HostTensor(g.dims, g.indices, zm.values, g.sort_order, g.coalesced), zm)
+            assert within_tol(g.values, y64, yab)[0], (dims, mode, R)
