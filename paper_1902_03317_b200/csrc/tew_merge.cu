@@ -296,7 +296,10 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(MergeParams p) {
 // entry; indices are unpacked from the key on emission. u64 smem arrays get
 // one pad element per 16 so the ~4-apart merge positions of a half-warp hit
 // distinct banks.
-__device__ __forceinline__ int pad64(int i) { return i + (i >> 4); }
+// Packed keys: one pad slot per 32 (measured best of 8/16/32/64/XOR for the
+// data-dependent merge-path positions).
+constexpr int kPad64Shift = 5;
+__device__ __forceinline__ int pad64(int i) { return i + (i >> kPad64Shift); }
 
 // ---------------------------------------------------------------------------
 // Persistent, pipelined, warp-specialised merge (packed u64 keys).
@@ -349,7 +352,7 @@ struct StageInfo {
 // at nxt, y keys at [nxt+1, nxt+1+nyt), a sentinel slot after them whose value
 // is the first y after the tile. Clamped head reads land on the sentinels, so
 // the merge loop has no bounds branches.
-constexpr int kSK = (kTile + 2 + (kTile + 2) / 16 + 4) & ~3;  // >= pad64(kTile + 1) + 1
+constexpr int kSK = (kTile + 2 + ((kTile + 2) >> kPad64Shift) + 4) & ~3;  // >= pad64(kTile+1)+1
 constexpr int kSV = (kTile + 2 + (kTile + 2) / 32 + 8) & ~3;  // >= pad(kTile + 2) + 1, 16B multiple
 // smem: stages [kStages][(N+1) * kSeg] u32 | sk [kSK] u64 | ek [2][kEK] u64 |
 //       sv [kSV] u32 | ev [2][kEV] u32 | info [kStages] | barriers | scalars
