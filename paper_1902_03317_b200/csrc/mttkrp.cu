@@ -1906,8 +1906,13 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
 #ifndef SPT_MTTKRP_PF
 #define SPT_MTTKRP_PF 1
 #endif
-  if (SPT_MTTKRP_PF && p.vec_ok) {
-    // persistent CTAs with the asynchronous tile fold
+  // Persistent CTAs with the asynchronous tile fold win up to a few 10M nnz
+  // (10M uniform: 160 vs 209 us; C4 shape at 20M: 615 vs 655 us). At 100M+
+  // with Zipf rows spanning thousands of tiles, the one fold warp that sums
+  // such a row's chain stalls its CTA (and the tickets it holds); the
+  // per-CTA kernel, which sums chains with all 256 threads, is faster there
+  // (C4 mode 3 at 100M: 2.71 vs 3.12 ms).
+  if (SPT_MTTKRP_PF && p.vec_ok && x->nnz <= (32ull << 20)) {
     const PfVariant pv = choose_pf(v.G, v.VEC, nm1);
     SPT_CUDA(cudaFuncSetAttribute(pv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(pv.smem)));
