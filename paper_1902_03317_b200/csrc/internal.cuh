@@ -135,6 +135,10 @@ __device__ __forceinline__ void st_release64(unsigned long long* p, unsigned lon
 __device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Release-only fence (MEMBAR.ALL.GPU): orders this thread's payload writes
+// before a later flag store, without the L1 invalidation (CCTL.IVALL) that
+// __threadfence() adds -- which would evict the L1-resident factor rows.
+__device__ __forceinline__ void fence_release() { asm volatile("fence.release.gpu;" ::: "memory"); }
 // Relaxed polling loads (no L1 invalidation per poll, unlike ld.acquire).
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;

@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
     // Inclusive partial of the tail row is known without predecessors.
     if (c < CB) {
       p.payP[(size_t)tile * CB + c] = boundary ? tail_acc : head_acc;
-      __threadfence();
+      spt::fence_release();
     }
     __syncthreads();
     if (tid == 0) spt::st_release(p.status + tile, tag | kFlagP);
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
     // Single-row tile continuing both ways: publish the aggregate first.
     if (c < CB) {
       p.payA[(size_t)tile * CB + c] = head_acc;
-      __threadfence();
+      spt::fence_release();
     }
     __syncthreads();
     if (tid == 0) spt::st_release(p.status + tile, tag | kFlagA);
@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(kPfThreads, 3) mttkrp_pf_kernel(MttkrpParams p
         }
       }
       if (cont_next) {
-        __threadfence();
+        spt::fence_release();
         __syncwarp();
         if (lane == 0)
           spt::st_release(p.status + tile,
@@ -1446,7 +1446,7 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
     if (gw == 0) {
 #pragma unroll
       for (int k = 0; k < VEC; ++k) pay[lcol + k] = pub[k];
-      __threadfence();
+      spt::fence_release();
     }
     __syncwarp();
     if (lane == 0) spt::st_release(p.status + tile, tag | (inclusive ? kFlagP : kFlagA));

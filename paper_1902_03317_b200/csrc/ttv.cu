@@ -177,11 +177,9 @@ __global__ void __launch_bounds__(kThreads, SPT_TTV_MINB) ttv_kernel(TtvParams p
   if (cont_next && tid == 0) {
     if (!single || !cont_prev) {
       p.payP[tile] = block_agg.v;
-      __threadfence();
       spt::st_release(p.status + tile, tag | kFlagP);
     } else {
       p.payA[tile] = block_agg.v;
-      __threadfence();
       spt::st_release(p.status + tile, tag | kFlagA);
     }
   }
@@ -416,11 +414,9 @@ __global__ void __launch_bounds__(kThreads, SPT_TTV_WT_MINB) ttv_wt_kernel(TtvPa
   if (cont_nx && lane == 0) {
     if (!single || !cont_prev) {
       p.payP[wt] = tile_tail;
-      __threadfence();
       spt::st_release(p.status + wt, tag | kFlagP);
     } else {
       p.payA[wt] = tile_tail;
-      __threadfence();
       spt::st_release(p.status + wt, tag | kFlagA);
     }
   }
