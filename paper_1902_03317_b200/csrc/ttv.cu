@@ -267,7 +267,7 @@ __global__ void tile_fiber_kernel(const uint32_t* fptr, uint32_t nfibs, uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// Warp-tile TTV: every warp owns a tile of kWT = 256 consecutive entries (8
+// Warp-tile TTV: every warp owns a tile of kWT = 128 or 256 consecutive entries (4 or 8
 // per lane) and does everything itself -- head flags from its slice of fptr,
 // fp32 terms, an fp64 segmented warp scan, staging of its fibers' outputs in
 // its own shared-memory slice, coalesced stores -- so no warp ever waits at a
@@ -275,19 +275,19 @@ __global__ void tile_fiber_kernel(const uint32_t* fptr, uint32_t nfibs, uint32_t
 // holding its last entry through the same epoch-tagged decoupled look-back
 // (scalar fp64 payloads); C3's short fibers rarely cross one. A CTA draws one
 // ticket for its 8 consecutive warp tiles, so predecessors are resident.
-constexpr int kWT = 256;
-constexpr int kWE = kWT / 32;  // entries per lane (blocked)
 
-template <int NO>
+template <int NO, int kWT>
 constexpr size_t ttv_wt_slice() {
   return (size_t)(kWT + 8) + (size_t)(kWT + 1) * 4 * (1 + NO);  // heads | zv | zi[NO]
 }
 
-template <int NO>
-#ifndef SPT_TTV_WT_MINB
-#define SPT_TTV_WT_MINB 4
-#endif
-__global__ void __launch_bounds__(kThreads, SPT_TTV_WT_MINB) ttv_wt_kernel(TtvParams p) {
+// kWT entries per warp tile (128 or 256); 128-entry tiles hold half the
+// registers (8 CTAs per SM instead of 4) and win when fibers are ~1 entry
+// long (C3 mode 0: 202 vs 232 us at 20M), 256 wins once fibers are longer
+// (fewer tiles split a fiber: mode 2 239 vs 249 us).
+template <int NO, int kWT>
+__global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(TtvParams p) {
+  constexpr int kWE = kWT / 32;  // entries per lane (blocked)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_ticket;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, SPT_TTV_WT_MINB) ttv_wt_kernel(TtvPa
   __syncthreads();  // the only CTA barrier
   const uint32_t wt = s_ticket * (kThreads / 32) + warp;
   if (wt >= p.ntiles) return;
-  unsigned char* base = smem_raw + warp * ((ttv_wt_slice<NO>() + 15) & ~size_t(15));
+  unsigned char* base = smem_raw + warp * ((ttv_wt_slice<NO, kWT>() + 15) & ~size_t(15));
   uint8_t* s_head = base;                                             // [kWT + 8]
   float* s_zv = reinterpret_cast<float*>(base + kWT + 8);             // [kWT + 1]
   uint32_t* s_zi = reinterpret_cast<uint32_t*>(s_zv + (kWT + 1));      // [NO][kWT + 1]
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, SPT_TTV_WT_MINB) ttv_wt_kernel(TtvPa
   }
 
   // ---- head flags from fptr[f_lo ...]: at most kWT + 2 fiber starts matter
-  reinterpret_cast<uint2*>(s_head)[lane] = make_uint2(0u, 0u);
+  for (int i = lane; i < kWT / 4; i += 32) reinterpret_cast<uint32_t*>(s_head)[i] = 0u;
   __syncwarp();
   const uint64_t t_end = t0 + cnt;
   uint64_t next_start = ~0ull;  // first fiber start >= t_end (this lane's share)
@@ -457,15 +457,20 @@ __global__ void __launch_bounds__(kThreads, SPT_TTV_WT_MINB) ttv_wt_kernel(TtvPa
       spt::st_stream(p.zidx[d] + f_lo + o, s_zi[d * (kWT + 1) + o]);
 }
 
-template <int NO>
+template <int NO, int kWT>
 int launch_ttv_wt(spt_ctx* ctx, const TtvParams& p, cudaStream_t st) {
-  const size_t smem = (size_t)(kThreads / 32) * ((ttv_wt_slice<NO>() + 15) & ~size_t(15));
-  SPT_CUDA(cudaFuncSetAttribute(ttv_wt_kernel<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = (size_t)(kThreads / 32) * ((ttv_wt_slice<NO, kWT>() + 15) & ~size_t(15));
+  SPT_CUDA(cudaFuncSetAttribute(ttv_wt_kernel<NO, kWT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   const unsigned grid = static_cast<unsigned>((p.ntiles + kThreads / 32 - 1) / (kThreads / 32));
-  ttv_wt_kernel<NO><<<grid, kThreads, smem, st>>>(p);
+  ttv_wt_kernel<NO, kWT><<<grid, kThreads, smem, st>>>(p);
   SPT_LAUNCHED(ctx);
   return SPT_OK;
+}
+
+template <int NO>
+int launch_ttv_wt_any(spt_ctx* ctx, const TtvParams& p, cudaStream_t st, uint32_t wt_entries) {
+  return wt_entries == 128 ? launch_ttv_wt<NO, 128>(ctx, p, st) : launch_ttv_wt<NO, 256>(ctx, p, st);
 }
 
 template <int NO>
@@ -539,7 +544,9 @@ extern "C" int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uin
 #ifndef SPT_TTV_WARP_TILES
 #define SPT_TTV_WARP_TILES 1
 #endif
-  const uint32_t tile_entries = SPT_TTV_WARP_TILES ? kWT : kTile;
+  // warp tiles of 128 entries for ~1-entry fibers, 256 otherwise
+  const uint32_t wt_entries = x->nnz <= nfibs + nfibs / 2 ? 128u : 256u;
+  const uint32_t tile_entries = SPT_TTV_WARP_TILES ? wt_entries : kTile;
   const uint64_t ntiles = (x->nnz + tile_entries - 1) / tile_entries;
   uint32_t* map;
   SPT_TRY(spt::ctx_scratch(ctx, ntiles * sizeof(uint32_t), reinterpret_cast<void**>(&map)));
@@ -574,13 +581,13 @@ extern "C" int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uin
   p.vec_ok = p.vec_ok && spt::aligned16(x->val);
   if (SPT_TTV_WARP_TILES) {
     switch (N - 1) {
-      case 1: SPT_TRY(launch_ttv_wt<1>(ctx, p, st)); break;
-      case 2: SPT_TRY(launch_ttv_wt<2>(ctx, p, st)); break;
-      case 3: SPT_TRY(launch_ttv_wt<3>(ctx, p, st)); break;
-      case 4: SPT_TRY(launch_ttv_wt<4>(ctx, p, st)); break;
-      case 5: SPT_TRY(launch_ttv_wt<5>(ctx, p, st)); break;
-      case 6: SPT_TRY(launch_ttv_wt<6>(ctx, p, st)); break;
-      default: SPT_TRY(launch_ttv_wt<7>(ctx, p, st)); break;
+      case 1: SPT_TRY(launch_ttv_wt_any<1>(ctx, p, st, wt_entries)); break;
+      case 2: SPT_TRY(launch_ttv_wt_any<2>(ctx, p, st, wt_entries)); break;
+      case 3: SPT_TRY(launch_ttv_wt_any<3>(ctx, p, st, wt_entries)); break;
+      case 4: SPT_TRY(launch_ttv_wt_any<4>(ctx, p, st, wt_entries)); break;
+      case 5: SPT_TRY(launch_ttv_wt_any<5>(ctx, p, st, wt_entries)); break;
+      case 6: SPT_TRY(launch_ttv_wt_any<6>(ctx, p, st, wt_entries)); break;
+      default: SPT_TRY(launch_ttv_wt_any<7>(ctx, p, st, wt_entries)); break;
     }
     (void)flags;
     return SPT_OK;
