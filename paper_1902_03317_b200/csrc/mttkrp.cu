@@ -65,6 +65,7 @@ struct MttkrpParams {
   unsigned long long* tile_ctr;
   unsigned long long* err;
   int vec_ok;  // per-entry arrays 16-byte aligned (vector staging)
+  int bid_tiles;  // warp tiles: the grid fits in one wave, so tile = blockIdx (no ticket)
   // TTM (FIBER=true): output rows are fibers of an x sorted with `mode` last.
   const uint32_t* fptr;
   const uint32_t* tile_fiber;
@@ -1099,7 +1100,10 @@ __global__ void __launch_bounds__(kPfThreads, 3) mttkrp_pf_kernel(MttkrpParams p
 // warp that meets many short (Zipf) rows never stalls the other seven, and the
 // CTA-level fold disappears. A CTA draws one ticket for its 8 consecutive warp
 // tiles, so predecessors are always resident.
-constexpr int kWT = 256;
+#ifndef SPT_MTTKRP_WT
+#define SPT_MTTKRP_WT 256
+#endif
+constexpr int kWT = SPT_MTTKRP_WT;
 constexpr int kWTP = kWT + kWT / 8;  // padded (sw layout)
 
 // TTM output index tuples of fiber `row` (head entry h) for NCOL columns at
@@ -1132,12 +1136,30 @@ __device__ __forceinline__ void wt_emit_idx(const MttkrpParams& p, uint32_t h, u
 // per-warp shared-memory slice of the warp-tile kernels
 template <int NM1, int G, int VEC, bool FIBER>
 __host__ __device__ constexpr size_t wt_slice(uint32_t n_modes) {
-  return (size_t)2 * (32 / G) * G * VEC * sizeof(double) + (size_t)(2 + NM1) * kWTP * 4 +
-         (FIBER ? (size_t)(kWT + 4) * 4 + (size_t)(n_modes - 1) * kWTP * 4 + (kWT + 16) : 0);
+  // group slots; TTM adds the staged entries, fiber offsets, head tuples and
+  // head flags (MTTKRP reads its entries through L1)
+  return (size_t)2 * (32 / G) * G * VEC * sizeof(double) +
+         (FIBER ? (size_t)(2 + NM1) * kWTP * 4 + (size_t)(kWT + 4) * 4 +
+                      (size_t)(n_modes - 1) * kWTP * 4 + (kWT + 16)
+                : 0);
 }
 
+#ifdef SPT_WT_TRACE
+__device__ unsigned long long g_wt_trace[16384 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define WT_TR(k) do { if (lane == 0 && tile < 16384) g_wt_trace[tile * 8 + (k)] = gtime(); } while (0)
+#else
+#define WT_TR(k) do {} while (0)
+#endif
+#ifndef SPT_WT_MINB
+#define SPT_WT_MINB 4
+#endif
 template <int NM1, int G, int VEC, bool FIBER = false>
-__global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) {
+__global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(MttkrpParams p) {
   constexpr int P = 32 / G;
   constexpr int EG = kWT / P;
   constexpr int CB = G * VEC;
@@ -1156,21 +1178,44 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
   uint8_t* s_hd = reinterpret_cast<uint8_t*>(s_hid + (FIBER ? (p.N - 1) * kWTP : 0));
   __shared__ uint32_t s_ticket;
   __shared__ uint32_t s_grow_all[kWarps][64];
+#ifdef SPT_WT_TRACE
+  const unsigned long long t_entry = gtime();
+#endif
 
-  if (tid == 0) {
-    const unsigned long long t = atomicAdd(p.tile_ctr, 1ull);
-    if (t == gridDim.x - 1) atomicExch(p.tile_ctr, 0ull);
-    s_ticket = static_cast<uint32_t>(t);
+  uint32_t cta_tile;
+  if (p.bid_tiles) {
+    // every CTA of the grid is resident at once, so predecessors always make
+    // progress without in-order tickets
+    cta_tile = blockIdx.x;
+  } else {
+    if (tid == 0) {
+      const unsigned long long t = atomicAdd(p.tile_ctr, 1ull);
+      if (t == gridDim.x - 1) atomicExch(p.tile_ctr, 0ull);
+      s_ticket = static_cast<uint32_t>(t);
+    }
+    __syncthreads();  // the only CTA barrier
+    cta_tile = s_ticket;
   }
-  __syncthreads();  // the only CTA barrier
-  const uint32_t tile = s_ticket * kWarps + warp;
+  const uint32_t tile = cta_tile * kWarps + warp;
   if (tile >= p.ntiles) return;
+  WT_TR(0);
   const uint64_t t0 = (uint64_t)tile * kWT;
   const int cnt = (p.nnz - t0 < (uint64_t)kWT) ? static_cast<int>(p.nnz - t0) : kWT;
   uint32_t* my_grow = s_grow_all[warp];
 
-  // ---- stage (vector loads when the warp tile is full and aligned)
-  if (cnt == kWT && p.vec_ok) {
+  // ---- stage. MTTKRP: no shared-memory copy -- each lane touches one 32-byte
+  // sector of every entry array (one warp = the tile's 4*32 sectors), so the
+  // groups' batch loads below hit L1, and the smem left free goes to L1 for
+  // the factor rows. TTM: staged copy (vector loads when full and aligned).
+  if constexpr (!FIBER) {
+    const uint64_t e8 = t0 + 8u * lane;
+    if (e8 < p.nnz) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p.out_idx + e8));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p.val + e8));
+#pragma unroll
+      for (int j = 0; j < NM1; ++j) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.oidx[j] + e8));
+    }
+  } else if (cnt == kWT && p.vec_ok) {
 #pragma unroll
     for (int r = 0; r < kWT / 128; ++r) {
       const int i = lane + 32 * r;  // uint4 chunk
@@ -1252,6 +1297,7 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
     if (t_end < p.nnz) next_row = next_start == t_end ? last_fiber + 1 : last_fiber;
   }
   __syncwarp();
+  WT_TR(1);
 
   // ---- per-group segmented accumulation (as in mttkrp_seg_kernel)
   const int gw = lane / G, gl = lane % G;
@@ -1278,12 +1324,32 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
   for (int e = e_begin; e < e_end; e += kU) {
     uint32_t rr[kU], ix[NM1][kU];
     float vv[kU];
-    ld_batch<kU>(s_out + sw(e), rr);
-    ld_batch<kU>(reinterpret_cast<const uint32_t*>(s_val) + sw(e),
-                 reinterpret_cast<uint32_t(&)[kU]>(vv));
-#pragma unroll
-    for (int j = 0; j < NM1; ++j) ld_batch<kU>(s_oidx + j * kWTP + sw(e), ix[j]);
     const bool full = e + kU <= e_end;
+    if constexpr (!FIBER) {
+      if (full && p.vec_ok) {
+        ld_batch<kU>(p.out_idx + t0 + e, rr);
+        ld_batch<kU>(reinterpret_cast<const uint32_t*>(p.val) + t0 + e,
+                     reinterpret_cast<uint32_t(&)[kU]>(vv));
+#pragma unroll
+        for (int j = 0; j < NM1; ++j) ld_batch<kU>(p.oidx[j] + t0 + e, ix[j]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const bool ok = e + u < e_end;
+          const uint64_t m = t0 + e + u;
+          rr[u] = ok ? p.out_idx[m] : 0u;
+          vv[u] = ok ? p.val[m] : 0.0f;
+#pragma unroll
+          for (int j = 0; j < NM1; ++j) ix[j][u] = ok ? p.oidx[j][m] : 0u;
+        }
+      }
+    } else {
+      ld_batch<kU>(s_out + sw(e), rr);
+      ld_batch<kU>(reinterpret_cast<const uint32_t*>(s_val) + sw(e),
+                   reinterpret_cast<uint32_t(&)[kU]>(vv));
+#pragma unroll
+      for (int j = 0; j < NM1; ++j) ld_batch<kU>(s_oidx + j * kWTP + sw(e), ix[j]);
+    }
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       if (e + u >= e_end) rr[u] = kNone;
@@ -1354,6 +1420,7 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
     for (int k = 0; k < VEC; ++k) s_gslot[sl * CB + lcol + k] = acc[k];
   }
   __syncwarp();
+  WT_TR(2);
 
   // ---- warp fold over the P groups' boundary runs -> tile head / tail
   uint32_t w_cur = kNone, h_row = kNone;
@@ -1421,6 +1488,7 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
     if (tail_row + 1 < stop) zero_rows<VEC>(p.out, tail_row + 1, stop, p.R, col, true);
   }
 
+  WT_TR(3);
   // ---- publish / look-back (warp-level)
   const uint32_t tag = p.epoch << 3;
   if (cont_next) {
@@ -1468,6 +1536,7 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
       for (int k = 0; k < VEC; ++k) carry[k] += __shfl_xor_sync(0xffffffffu, carry[k], o);
   }
 
+  WT_TR(4);
   // ---- rows completed by this tile
   if (writer) {
     if (boundary || !cont_next) {
@@ -1485,12 +1554,21 @@ __global__ void __launch_bounds__(kThreads, 4) mttkrp_wt_kernel(MttkrpParams p) 
       if constexpr (FIBER) wt_emit_idx<VEC>(p, s_fp[tail_row - f_lo], tail_row, col, s_hid, t0);
     }
   }
+  WT_TR(5);
+#ifdef SPT_WT_TRACE
+  if (lane == 0 && tile < 16384) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    g_wt_trace[tile * 8 + 6] = sm;
+    g_wt_trace[tile * 8 + 7] = t_entry;
+  }
+#endif
 }
 
 template <int G, int VEC>
 size_t wt_smem(int nm1) {
-  return (size_t)kWarps * ((size_t)2 * (32 / G) * G * VEC * sizeof(double) +
-                           (size_t)(2 + nm1) * kWTP * 4);
+  (void)nm1;
+  return (size_t)kWarps * ((size_t)2 * (32 / G) * G * VEC * sizeof(double));
 }
 
 using KernelFnT = void (*)(MttkrpParams);
@@ -1886,6 +1964,15 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
     p.ntiles = static_cast<uint32_t>(ntiles);
     SPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
+#ifndef SPT_WT_CARVEOUT
+#define SPT_WT_CARVEOUT 40  // ~100 KB smem per SM: 4 CTAs, the rest of the 256 KB is L1
+#endif
+    SPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  SPT_WT_CARVEOUT));
+    int per_sm = 0;
+    SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+    const uint64_t grid = (ntiles + kWarps - 1) / kWarps;
+    p.bid_tiles = grid <= (uint64_t)per_sm * ctx->num_sms ? 1 : 0;
     for (uint32_t c0 = 0; c0 < R; c0 += CB) {
       uint32_t epoch;
       SPT_TRY(spt::ctx_lookback(ctx, ntiles, 2 * ntiles * CB, &epoch));
@@ -1895,7 +1982,7 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
       p.epoch = epoch;
       p.c0 = c0;
       p.ncols = static_cast<uint32_t>(std::min<uint64_t>(CB, R - c0));
-      fn<<<static_cast<unsigned>((ntiles + kWarps - 1) / kWarps), kThreads, smem, st>>>(p);
+      fn<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(p);
       SPT_LAUNCHED(ctx);
     }
     if (flags & SPT_FLAG_ASYNC) return SPT_OK;
@@ -1952,3 +2039,9 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
   if (flags & SPT_FLAG_ASYNC) return SPT_OK;
   return spt::sync_and_check(ctx, st);
 }
+
+#ifdef SPT_WT_TRACE
+extern "C" __attribute__((visibility("default"))) int spt_debug_wt_trace(void* dst) {
+  return cudaMemcpyFromSymbol(dst, g_wt_trace, sizeof(g_wt_trace)) == cudaSuccess ? 0 : 5;
+}
+#endif
