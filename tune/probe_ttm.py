@@ -6,7 +6,7 @@ ctx = _lib.Context.get(0); lib = _lib.load(); st = torch.cuda.current_stream().c
 dims, nnz, R = [50000, 20000, 100000], int(os.environ.get("NNZ", 20_000_000)), 16
 base = generate.coo(dims, nnz, 1, [1.1, 0, 0], 0, 1, None)
 res = []
-for mode in (0, 2):
+for mode in [int(m) for m in os.environ.get("MODES", "0,2").split(",")]:
     xs = base.clone(); ops.sort_lexicographic(xs, ops.mode_last_order(3, mode))
     fib = ops.build_fiber_index(xs, mode)
     U = generate.uniform((dims[mode], R), 1, 5, -1, 1)
