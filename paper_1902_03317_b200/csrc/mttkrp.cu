@@ -1108,27 +1108,48 @@ constexpr int kWTP = kWT + kWT / 8;  // padded (sw layout)
 
 // TTM output index tuples of fiber `row` (head entry h) for NCOL columns at
 // col, head indices from the warp's staged copy when h lies in its tile.
-template <int NCOL>
+// NT > 0: the order is a compile-time constant (unrolled, the mode test is a
+// select); NT = 0: any order.
+template <int NCOL, int NT>
 __device__ __forceinline__ void wt_emit_idx(const MttkrpParams& p, uint32_t h, uint32_t row,
                                             uint32_t col, const uint32_t* s_hid, uint64_t t0) {
   const size_t base = (size_t)row * p.R + col;
-  int j = 0;
-  for (uint32_t d = 0; d < p.N; ++d) {
-    uint32_t w[NCOL];
-    if (d == p.mode) {
-#pragma unroll
-      for (int k = 0; k < NCOL; ++k) w[k] = col + k;
-    } else {
-      const uint32_t hv = h >= t0 ? s_hid[j * kWTP + sw(static_cast<int>(h - t0))] : p.hidx[d][h];
-      ++j;
-#pragma unroll
-      for (int k = 0; k < NCOL; ++k) w[k] = hv;
-    }
+  const bool staged = h >= t0;
+  const int hs = staged ? sw(static_cast<int>(h - t0)) : 0;
+  auto put = [&](uint32_t d, const uint32_t (&w)[NCOL]) {
     if constexpr (NCOL == 4) {
       __stcs(reinterpret_cast<uint4*>(p.zidx[d] + base), make_uint4(w[0], w[1], w[2], w[3]));
     } else {
 #pragma unroll
       for (int k = 0; k < NCOL; ++k) __stcs(p.zidx[d] + base + k, w[k]);
+    }
+  };
+  if constexpr (NT > 0) {
+    const int mode = static_cast<int>(p.mode);
+#pragma unroll
+    for (int d = 0; d < NT; ++d) {
+      const int j = d < mode ? d : d - 1;  // position among the non-mode dims
+      uint32_t hv = 0;
+      if (d != mode) hv = staged ? s_hid[j * kWTP + hs] : p.hidx[d][h];
+      uint32_t w[NCOL];
+#pragma unroll
+      for (int k = 0; k < NCOL; ++k) w[k] = d == mode ? col + k : hv;
+      put(d, w);
+    }
+  } else {
+    int j = 0;
+    for (uint32_t d = 0; d < p.N; ++d) {
+      uint32_t w[NCOL];
+      if (d == p.mode) {
+#pragma unroll
+        for (int k = 0; k < NCOL; ++k) w[k] = col + k;
+      } else {
+        const uint32_t hv = staged ? s_hid[j * kWTP + hs] : p.hidx[d][h];
+        ++j;
+#pragma unroll
+        for (int k = 0; k < NCOL; ++k) w[k] = hv;
+      }
+      put(d, w);
     }
   }
 }
@@ -1158,7 +1179,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 #ifndef SPT_WT_MINB
 #define SPT_WT_MINB 4
 #endif
-template <int NM1, int G, int VEC, bool FIBER = false>
+template <int NM1, int G, int VEC, bool FIBER = false, int NT = 0>
 __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(MttkrpParams p) {
   constexpr int P = 32 / G;
   constexpr int EG = kWT / P;
@@ -1393,7 +1414,9 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
         continue;
       }
       if (run_row != kNone) {
-        if (row < run_row && gl == 0) atomicMin(p.err + 2, (unsigned long long)(t0 + e + u));
+        // fiber ids increase by construction (TTM): only MTTKRP checks its input
+        if (!FIBER && row < run_row && gl == 0)
+          atomicMin(p.err + 2, (unsigned long long)(t0 + e + u));
         if (first_run) {
           if (gl == 0) my_grow[2 * gw] = run_row;
 #pragma unroll
@@ -1404,7 +1427,7 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
 #pragma unroll
           for (int k = 0; k < VEC; ++k) o[k] = (float)acc[k];
           Vec<VEC>::store(p.out + (size_t)run_row * p.R + col, o);
-          if constexpr (FIBER) wt_emit_idx<VEC>(p, s_fp[run_row - f_lo], run_row, col, s_hid, t0);
+          if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[run_row - f_lo], run_row, col, s_hid, t0);
         }
         if (row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
       }
@@ -1453,7 +1476,7 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
 #pragma unroll
             for (int k = 0; k < VEC; ++k) o[k] = (float)w_acc[k];
             Vec<VEC>::store(p.out + (size_t)w_cur * p.R + col, o);
-            if constexpr (FIBER) wt_emit_idx<VEC>(p, s_fp[w_cur - f_lo], w_cur, col, s_hid, t0);
+            if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[w_cur - f_lo], w_cur, col, s_hid, t0);
           }
           if (g != cur_g && row > w_cur + 1 && writer)
             zero_rows<VEC>(p.out, w_cur + 1, row, p.R, col, true);
@@ -1544,14 +1567,14 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
 #pragma unroll
       for (int k = 0; k < VEC; ++k) o[k] = (float)(carry[k] + head_acc[k]);
       Vec<VEC>::store(p.out + (size_t)head_row * p.R + col, o);
-      if constexpr (FIBER) wt_emit_idx<VEC>(p, s_fp[head_row - f_lo], head_row, col, s_hid, t0);
+      if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[head_row - f_lo], head_row, col, s_hid, t0);
     }
     if (boundary && !cont_next) {
       float o[VEC];
 #pragma unroll
       for (int k = 0; k < VEC; ++k) o[k] = (float)tail_acc[k];
       Vec<VEC>::store(p.out + (size_t)tail_row * p.R + col, o);
-      if constexpr (FIBER) wt_emit_idx<VEC>(p, s_fp[tail_row - f_lo], tail_row, col, s_hid, t0);
+      if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[tail_row - f_lo], tail_row, col, s_hid, t0);
     }
   }
   WT_TR(5);
@@ -1737,9 +1760,18 @@ struct TtmVariant {
   KernelFn wt;  // warp-tile TTM (same G/VEC)
 };
 
-TtmVariant choose_ttm(uint32_t R, bool aligned) {
+template <int G, int VEC>
+KernelFn pick_ttm_wt(uint32_t N) {
+  switch (N) {
+    case 3: return mttkrp_wt_kernel<1, G, VEC, true, 3>;
+    case 4: return mttkrp_wt_kernel<1, G, VEC, true, 4>;
+    default: return mttkrp_wt_kernel<1, G, VEC, true>;
+  }
+}
+
+TtmVariant choose_ttm(uint32_t R, bool aligned, uint32_t N) {
 #define SPT_TTM_V(g, v) \
-  { g, v, mttkrp_seg_kernel<1, g, v, true>, ttm_smem<g, v>(), mttkrp_wt_kernel<1, g, v, true> }
+  { g, v, mttkrp_seg_kernel<1, g, v, true>, ttm_smem<g, v>(), pick_ttm_wt<g, v>(N) }
   if (R % 4 == 0 && aligned) {
     const uint32_t q = R / 4;
     if (q <= 2) return SPT_TTM_V(2, 4);
@@ -1810,7 +1842,7 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
 
   bool aligned = spt::aligned16(d_u) && spt::aligned16(z->val);
   for (uint32_t d = 0; d < N; ++d) aligned = aligned && spt::aligned16(z->idx[d]);
-  const TtmVariant v = choose_ttm(R, aligned);
+  const TtmVariant v = choose_ttm(R, aligned, N);
   const uint32_t CB = v.G * v.VEC;
 #ifndef SPT_TTM_WARP_TILES
 #define SPT_TTM_WARP_TILES 1
