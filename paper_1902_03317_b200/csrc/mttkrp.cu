@@ -1126,14 +1126,24 @@ __device__ __forceinline__ void wt_emit_idx(const MttkrpParams& p, uint32_t h, u
   };
   if constexpr (NT > 0) {
     const int mode = static_cast<int>(p.mode);
+    uint32_t hv[NT];
+    if (staged) {
+      // head tuple from the warp's staged copy (the usual case)
+      const uint32_t* src = s_hid + hs;
+#pragma unroll
+      for (int d = 0; d < NT; ++d) {
+        const int j = d < mode ? d : d - 1;  // position among the non-mode dims
+        hv[d] = d == mode ? 0u : src[j * kWTP];
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < NT; ++d) hv[d] = d == mode ? 0u : p.hidx[d][h];
+    }
 #pragma unroll
     for (int d = 0; d < NT; ++d) {
-      const int j = d < mode ? d : d - 1;  // position among the non-mode dims
-      uint32_t hv = 0;
-      if (d != mode) hv = staged ? s_hid[j * kWTP + hs] : p.hidx[d][h];
       uint32_t w[NCOL];
 #pragma unroll
-      for (int k = 0; k < NCOL; ++k) w[k] = d == mode ? col + k : hv;
+      for (int k = 0; k < NCOL; ++k) w[k] = d == mode ? col + k : hv[d];
       put(d, w);
     }
   } else {
