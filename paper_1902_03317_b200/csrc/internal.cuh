@@ -62,7 +62,7 @@ int sync_and_check(spt_ctx* ctx, cudaStream_t stream);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+__host__ __device__ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 inline unsigned grid_for(uint64_t work_items, unsigned block, unsigned max_blocks) {
   uint64_t g = (work_items + block - 1) / block;

@@ -1280,10 +1280,20 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
   } else {
     // TTM: rows are fiber ids. Head tuples of the tile's entries, the fptr
     // slice of the fibers touching it, head flags, and each entry's fiber.
-    for (uint32_t j = 0; j + 1 < p.N; ++j)
-      for (int i = lane; i < kWT; i += 32)
-        s_hid[j * kWTP + sw(i)] = i < cnt ? p.hnm[j][t0 + i] : 0u;
     f_lo = __ldg(p.tile_fiber + tile);
+    for (uint32_t j = 0; j + 1 < p.N; ++j) {
+      if (cnt == kWT && spt::aligned16(p.hnm[j])) {
+#pragma unroll
+        for (int r = 0; r < kWT / 128; ++r) {
+          const int i = lane + 32 * r;  // uint4 chunk
+          reinterpret_cast<uint4*>(s_hid + j * kWTP)[i + (i >> 3)] =
+              spt::ld_stream(reinterpret_cast<const uint4*>(p.hnm[j] + t0) + i);
+        }
+      } else {
+        for (int i = lane; i < kWT; i += 32)
+          s_hid[j * kWTP + sw(i)] = i < cnt ? p.hnm[j][t0 + i] : 0u;
+      }
+    }
     reinterpret_cast<uint2*>(s_hd)[lane] = make_uint2(0u, 0u);
     __syncwarp();
     const uint64_t t_end = t0 + cnt;
