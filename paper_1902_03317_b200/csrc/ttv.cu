@@ -26,6 +26,9 @@ constexpr int kThreads = 256;
 #ifndef SPT_TTV_EPT
 #define SPT_TTV_EPT 8
 #endif
+#ifndef SPT_TTV_TICKET
+#define SPT_TTV_TICKET 0
+#endif
 #ifndef SPT_TTV_MINB
 #define SPT_TTV_MINB 4
 #endif
@@ -289,15 +292,22 @@ template <int NO, int kWT>
 __global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(TtvParams p) {
   constexpr int kWE = kWT / 32;  // entries per lane (blocked)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ uint32_t s_ticket;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#if SPT_TTV_TICKET
+  __shared__ uint32_t s_ticket;
   if (tid == 0) {
     const unsigned long long t = atomicAdd(p.tile_ctr, 1ull);
     if (t == gridDim.x - 1) atomicExch(p.tile_ctr, 0ull);
     s_ticket = static_cast<uint32_t>(t);
   }
-  __syncthreads();  // the only CTA barrier
-  const uint32_t wt = s_ticket * (kThreads / 32) + warp;
+  __syncthreads();
+  const uint32_t cta = s_ticket;
+#else
+  // tiles in launch order (as CUB's single-pass scans do): CTAs are dispatched
+  // in blockIdx order, so a tile's predecessors are resident or done
+  const uint32_t cta = blockIdx.x;
+#endif
+  const uint32_t wt = cta * (kThreads / 32) + warp;
   if (wt >= p.ntiles) return;
   unsigned char* base = smem_raw + warp * ((ttv_wt_slice<NO, kWT>() + 15) & ~size_t(15));
   uint8_t* s_head = base;                                             // [kWT + 8]
@@ -336,24 +346,48 @@ __global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(Tt
     }
   }
 
-  // ---- head flags from fptr[f_lo ...]: at most kWT + 2 fiber starts matter
-  for (int i = lane; i < kWT / 4; i += 32) reinterpret_cast<uint32_t*>(s_head)[i] = 0u;
-  __syncwarp();
+  // ---- head flags. x is coalesced and sorted with `mode` last, so a fiber
+  // starts exactly where a non-mode index changes (build_fiber_index,
+  // P/src/tensor.cpp:92-120): compare each entry's tuple with its
+  // predecessor's (previous lane by shuffle, entry t0-1 / t_end loaded by
+  // lanes 0 / 31) -- no fptr reads on the tile's critical path.
   const uint64_t t_end = t0 + cnt;
-  uint64_t next_start = ~0ull;  // first fiber start >= t_end (this lane's share)
+  uint32_t prv[NO], nxt[NO];
 #pragma unroll
-  for (int r = 0; r < (kWT + 2 + 31) / 32; ++r) {
-    const uint64_t f = (uint64_t)f_lo + lane + 32 * r;
-    if (f > p.nfibs) continue;
-    const uint64_t s = __ldg(p.fptr + f);
-    if (s >= t0 && s < t_end) s_head[s - t0] = 1;
-    if (s >= t_end && s < next_start) next_start = s;
+  for (int d = 0; d < NO; ++d) {
+    prv[d] = (lane == 0 && t0 > 0) ? p.hidx[d][t0 - 1] : 0u;
+    nxt[d] = (lane == 31 && t_end < p.nnz) ? p.hidx[d][t_end] : 0u;
   }
+  bool hd[kWE];
+  {
+    bool diff0 = (lane == 0 && t0 == 0);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t v = __shfl_xor_sync(0xffffffffu, next_start, o);
-    next_start = v < next_start ? v : next_start;
+    for (int d = 0; d < NO; ++d) {
+      const uint32_t up = __shfl_up_sync(0xffffffffu, oi[d][kWE - 1], 1);
+      const uint32_t before = lane == 0 ? prv[d] : up;
+      diff0 = diff0 || oi[d][0] != before;
+    }
+    hd[0] = diff0;
+#pragma unroll
+    for (int i = 1; i < kWE; ++i) {
+      bool df = false;
+#pragma unroll
+      for (int d = 0; d < NO; ++d) df = df || oi[d][i] != oi[d][i - 1];
+      hd[i] = df;
+    }
   }
+  // does the tile's last fiber go on past t_end?
+  bool cont_nx_l = false;
+  if (lane == 31 && t_end < p.nnz) {
+    // entry t_end - 1 is lane 31's last valid entry only for full tiles; the
+    // partial tile is the last one (t_end == nnz), so this branch sees a full tile
+    cont_nx_l = true;
+#pragma unroll
+    for (int d = 0; d < NO; ++d) cont_nx_l = cont_nx_l && nxt[d] == oi[d][kWE - 1];
+  }
+  const bool cont_nx = __shfl_sync(0xffffffffu, cont_nx_l ? 1 : 0, 31) != 0;
+#pragma unroll
+  for (int i = 0; i < kWE; ++i) s_head[e0 + i] = (e0 + i < cnt && hd[i]) ? 1 : 0;
   __syncwarp();
 
   // ---- terms, segmented warp scan (fp64), local fiber ids
@@ -402,7 +436,6 @@ __global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(Tt
   }
   const bool head0 = __shfl_sync(0xffffffffu, head[0] ? 1 : 0, 0) != 0;  // entry t0 starts a fiber
   const bool cont_prev = !head0;
-  const bool cont_nx = next_start != t_end;  // the last fiber goes on past this tile
   const int hc0 = head0 ? 1 : 0;
   const int total_h = __shfl_sync(0xffffffffu, hx, 31);
   const int last_lf = total_h - hc0;  // local id of the tile's last fiber
