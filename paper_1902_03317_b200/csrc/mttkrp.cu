@@ -156,6 +156,9 @@ __device__ __forceinline__ void zero_rows(float* out, uint32_t r0, uint32_t r1, 
 #ifndef SPT_MTTKRP_UNROLL
 #define SPT_MTTKRP_UNROLL 4
 #endif
+#ifndef SPT_SEG_TICKET
+#define SPT_SEG_TICKET 0
+#endif
 #ifndef SPT_MTTKRP_MINB
 #define SPT_MTTKRP_MINB 3  // <= 85 registers: 3 CTAs (24 warps) per SM
 #endif
@@ -182,10 +185,12 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
   uint32_t* s_hid = reinterpret_cast<uint32_t*>(s_gslot + 2 * GROUPS * CB);
   __shared__ uint32_t s_grow[2 * GROUPS];
   __shared__ uint32_t s_slot_row[NSLOT];
-  __shared__ uint32_t s_tile, s_flag;
+  __shared__ uint32_t s_flag;
   __shared__ uint32_t s_meta[4];
 
   const int tid = threadIdx.x;
+#if SPT_SEG_TICKET
+  __shared__ uint32_t s_tile;
   if (tid == 0) {
     const unsigned long long t = atomicAdd(p.tile_ctr, 1ull);
     if (t == p.ntiles - 1) atomicExch(p.tile_ctr, 0ull);  // last increment of this launch
@@ -193,6 +198,11 @@ __global__ void __launch_bounds__(kThreads, SPT_MTTKRP_MINB) mttkrp_seg_kernel(M
   }
   __syncthreads();
   const uint32_t tile = s_tile;
+#else
+  // tiles in launch order (CTAs are dispatched in blockIdx order, as CUB's
+  // single-pass scans assume): no ticket round trip
+  const uint32_t tile = blockIdx.x;
+#endif
   const uint64_t t0 = (uint64_t)tile * kTile;
   const int cnt = (p.nnz - t0 < (uint64_t)kTile) ? static_cast<int>(p.nnz - t0) : kTile;
 
@@ -1104,6 +1114,10 @@ __global__ void __launch_bounds__(kPfThreads, 3) mttkrp_pf_kernel(MttkrpParams p
 #define SPT_MTTKRP_WT 256
 #endif
 constexpr int kWT = SPT_MTTKRP_WT;
+// warp tiles in launch order (blockIdx) instead of in-order tickets
+#ifndef SPT_WT_BID
+#define SPT_WT_BID 1
+#endif
 constexpr int kWTP = kWT + kWT / 8;  // padded (sw layout)
 
 // TTM output index tuples of fiber `row` (head entry h) for NCOL columns at
@@ -1897,6 +1911,7 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
   }
   p.N = N;
   p.mode = mode;
+  p.bid_tiles = SPT_WT_BID;
   const KernelFn fn = wt ? v.wt : v.fn;
   const size_t smem = wt ? ttm_wt_smem(v.G, v.VEC, N)
                          : v.smem + (size_t)(N - 1) * kTileP * sizeof(uint32_t);
@@ -2024,7 +2039,7 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
     int per_sm = 0;
     SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
     const uint64_t grid = (ntiles + kWarps - 1) / kWarps;
-    p.bid_tiles = grid <= (uint64_t)per_sm * ctx->num_sms ? 1 : 0;
+    p.bid_tiles = SPT_WT_BID || grid <= (uint64_t)per_sm * ctx->num_sms ? 1 : 0;
     for (uint32_t c0 = 0; c0 < R; c0 += CB) {
       uint32_t epoch;
       SPT_TRY(spt::ctx_lookback(ctx, ntiles, 2 * ntiles * CB, &epoch));
