@@ -301,6 +301,73 @@ class C2(Workload):
         return self.cpu_units
 
 
+# ---------------------------------------------------------------------------
+# Reference CPU legs (oracle/_ref = the reference library, par:: kernels with
+# every host thread) shared by the workloads' cpu_setup / cpu_step.
+
+
+def _host_sample(t, k):
+    """The first k entries of a device tensor as a HostTensor (a prefix of a
+    sorted, coalesced tensor is sorted and coalesced, and its fibers are whole
+    except possibly the last)."""
+    from oracle.oracle import HostTensor
+    k = min(k, t.nnz)
+    return HostTensor(list(t.dims), [ix[:k].cpu().numpy().view(np.uint32).copy()
+                                     for ix in t.indices],
+                      t.values[:k].cpu().numpy().copy(),
+                      None if t.sort_order is None else list(t.sort_order), t.coalesced)
+
+
+class _RefCalls:
+    """Handles for the reference's par:: kernels on fixed inputs."""
+
+    def __init__(self, ref):
+        import ctypes
+        self.ref, self.lib, self.ct = ref, ref.lib, ctypes
+        self.keep = []
+
+    def coo(self, ht):
+        h = self.ref.coo(ht)
+        self.keep.append(("coo", h))
+        return h
+
+    def matrix(self, a):
+        import numpy as np
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        self.keep.append(("arr", a))
+        f32p = self.ct.POINTER(self.ct.c_float)
+        return self.lib.ref_matrix_new(a.ctypes.data_as(f32p), a.shape[0], a.shape[1])
+
+    def vector(self, a):
+        import numpy as np
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        self.keep.append(("arr", a))
+        f32p = self.ct.POINTER(self.ct.c_float)
+        return self.lib.ref_vector_new(a.ctypes.data_as(f32p), a.shape[0])
+
+    def factors(self, hx, mats):
+        """One reference factor vector (the matrices are copied into it, so the
+        temporaries go at once -- C5's factors are 1.28 GB each)."""
+        import numpy as np
+        f32p = self.ct.POINTER(self.ct.c_float)
+        hs = (self.ct.c_void_p * len(mats))()
+        for d, m in enumerate(mats):
+            a = np.ascontiguousarray(m, dtype=np.float32)
+            hs[d] = self.lib.ref_matrix_new(a.ctypes.data_as(f32p), a.shape[0], a.shape[1])
+        fv = self.lib.ref_factors_new(hx, hs)
+        for h in hs:
+            self.lib.ref_matrix_free(h)
+        return fv
+
+    def run(self, fn, *args, kind="coo"):
+        out = self.ct.c_void_p()
+        self.ref._check(fn(*args, self.ct.byref(out)))
+        (self.lib.ref_matrix_free if kind == "matrix" else self.lib.ref_coo_free)(out.value)
+
+    def mttkrp(self, hx, fv, mode, nt):  # privatize: the strategy the paper reports
+        self.run(self.lib.ref_mttkrp_fv, hx, fv, mode, 1, nt, 0, kind="matrix")
+
+
 class C1(Workload):
     """BASELINE configs[0]: MTTKRP mode 0 (R=16) + TS add/mul by 2.5, 1M nnz."""
 
@@ -331,6 +398,20 @@ class C1(Workload):
     def config(self):
         return {"workload": self.name, "baseline_config": "configs[0] (C1)", "dims": self.dims,
                 "nnz": self.nnz, "R": self.R, "mttkrp_input": "sorted (0,1,2) (mode-0 leading)"}
+
+    def cpu_setup(self, ref, sample_nnz=None):
+        c = self.cr = _RefCalls(ref)
+        self.hx = c.coo(_host_sample(self.x, self.nnz))
+        self.fv = c.factors(self.hx, [f.cpu().numpy() for f in self.f])
+        self.cpu_units = 3 * self.nnz
+        return f"full C1 workload: mttkrp mode 0 (privatize) + ts add/mul on {self.nnz} nnz, par::"
+
+    def cpu_step(self, ref, nthreads):
+        c = self.cr
+        c.mttkrp(self.hx, self.fv, 0, nthreads)
+        for op in (0, 1):
+            c.run(c.lib.ref_ts, self.hx, 2.5, op, 1, nthreads)
+        return self.cpu_units
 
 
 class C3(Workload):
@@ -385,6 +466,27 @@ class C3(Workload):
                 "nnz": self.nnz, "R": self.R, "nfibs": [f.nfibs for f in self.fib],
                 "mode0": "Zipf(1.1) over a seeded id permutation; modes 1,2 uniform"}
 
+    def cpu_setup(self, ref, sample_nnz=1_000_000):
+        c = self.cr = _RefCalls(ref)
+        self.cpu_in = []
+        k = min(sample_nnz, self.nnz)
+        for m in range(3):
+            hx = c.coo(_host_sample(self.xs[m], k))
+            fib = ref.lib.ref_fiber_new(hx, m)  # preprocessing, untimed (P/src/bench.cpp:363-368)
+            c.keep.append(("fib", fib))
+            self.cpu_in.append((hx, fib, c.vector(self.v[m].cpu().numpy()),
+                                c.matrix(self.u[m].cpu().numpy())))
+        self.cpu_units = 6 * k
+        return f"ttv + ttm (R={self.R}) along every mode on the first {k} entries of each " \
+               "mode-last sorted copy, par::"
+
+    def cpu_step(self, ref, nthreads):
+        c = self.cr
+        for m, (hx, fib, hv, hu) in enumerate(self.cpu_in):
+            c.run(c.lib.ref_ttv_fib, hx, hv, m, fib, 1, nthreads)
+            c.run(c.lib.ref_ttm_fib, hx, hu, m, fib, 1, nthreads)
+        return self.cpu_units
+
 
 class C4(Workload):
     """configs[3]: MTTKRP every mode, R=32, 4th order, 100M nnz, Zipf(1.2) modes."""
@@ -419,6 +521,23 @@ class C4(Workload):
         return {"workload": self.name, "baseline_config": "configs[3] (C4)", "dims": self.dims,
                 "nnz": self.nnz, "R": self.R, "dist": "every mode Zipf(1.2), shuffled ids",
                 "mttkrp_input": "one mode-leading sorted copy per mode (preprocessing)"}
+
+    def cpu_setup(self, ref, sample_nnz=1_000_000):
+        c = self.cr = _RefCalls(ref)
+        k = min(sample_nnz, self.nnz)
+        self.cpu_in = []
+        for m in range(4):
+            self.cpu_in.append((c.coo(_host_sample(self.xs[m], k)), None))
+        fv = c.factors(self.cpu_in[0][0], [f.cpu().numpy() for f in self.f])
+        self.cpu_in = [(hx, fv) for hx, _ in self.cpu_in]
+        self.cpu_units = 4 * k
+        return f"mttkrp (R={self.R}, privatize) along every mode on the first {k} entries of " \
+               "each mode-leading sorted copy (full-size factors), par::"
+
+    def cpu_step(self, ref, nthreads):
+        for m, (hx, fv) in enumerate(self.cpu_in):
+            self.cr.mttkrp(hx, fv, m, nthreads)
+        return self.cpu_units
 
 
 class C5(Workload):
@@ -471,6 +590,30 @@ class C5(Workload):
                 "nnz": self.nnz, "R": self.R, "dist": "every mode Zipf(1.1), shuffled ids",
                 "mttkrp_input": "one mode-leading sorted copy per mode (preprocessing)",
                 "tew_eq": "mul against the same pattern, y U[0.5,1.5)"}
+
+    def cpu_setup(self, ref, sample_nnz=1_000_000):
+        c = self.cr = _RefCalls(ref)
+        k = min(sample_nnz, self.nnz)
+        self.cpu_in = []
+        for m in range(3):
+            self.cpu_in.append((c.coo(_host_sample(self.xs[m], k)), None))
+        fv = c.factors(self.cpu_in[0][0], [f.cpu().numpy() for f in self.f])
+        self.cpu_in = [(hx, fv) for hx, _ in self.cpu_in]
+        from oracle.oracle import HostTensor
+        hx0 = _host_sample(self.xs[0], k)
+        hy = HostTensor(hx0.dims, hx0.indices, self.y.values[:k].cpu().numpy(), hx0.sort_order,
+                        hx0.coalesced)
+        self.eq = (c.coo(hx0), c.coo(hy))
+        self.cpu_units = 4 * k
+        return f"mttkrp (R={self.R}, privatize) modes 0-2 on the first {k} entries of each " \
+               f"mode-leading copy (full 10M-row factors) + tew_eq mul on {k} entries, par::"
+
+    def cpu_step(self, ref, nthreads):
+        c = self.cr
+        for m, (hx, fv) in enumerate(self.cpu_in):
+            c.mttkrp(hx, fv, m, nthreads)
+        c.run(c.lib.ref_tew_eq, self.eq[0], self.eq[1], 2, 1, nthreads)
+        return self.cpu_units
 
 
 class Pre(Workload):
