@@ -388,6 +388,19 @@ __device__ __forceinline__ uint32_t word_phase(const uint32_t* p) {
   return (static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p)) >> 2) & 3u;
 }
 
+// Per-tile phase timeline for tune/probe_merge_trace.py (-DSPT_MERGE_TRACE).
+#ifdef SPT_MERGE_TRACE
+__device__ unsigned long long g_mtrace[16384 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define MT_TR(tile, k) do { if ((tile) < 16384) g_mtrace[(tile) * 8 + (k)] = gtime(); } while (0)
+#else
+#define MT_TR(tile, k) do {} while (0)
+#endif
+
 template <int N, int OP>
 __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, uint32_t nctas) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -449,7 +462,9 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
         a0 = p.split[t];
         a1 = p.split[t + 1];
       }
+      if (lane == 0 && t < p.ntiles) MT_TR(t, 0);
       if (it >= kStages) spt::mbar_wait(empty + s, ((it / kStages) - 1) & 1u);
+      if (lane == 0 && t < p.ntiles) MT_TR(t, 1);
       StageInfo& inf = info[s];
       if (t >= p.ntiles) {
         if (lane == 0) inf.tile = kDone;
@@ -578,9 +593,18 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
   };
   for (uint32_t it = 0;; ++it) {
     const int s = it % kStages;
+#ifdef SPT_MERGE_TRACE
+    const unsigned long long tw0 = gtime();
+#endif
     spt::mbar_wait(full + s, (it / kStages) & 1u);
     const StageInfo& inf = info[s];
     const uint32_t tile = inf.tile;
+#ifdef SPT_MERGE_TRACE
+    if (tid == 0 && tile != kDone && tile < 16384) {
+      g_mtrace[tile * 8 + 2] = tw0;
+      MT_TR(tile, 3);
+    }
+#endif
     const int r = it % kSlots;
     if (tile == kDone) {
       if (it > 0) flush(it - 1);
@@ -626,6 +650,7 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
     __syncwarp();
     if (lane == 0) spt::mbar_arrive(empty + s);  // this warp is done with the stage
     bar_sync(1, kThreads);
+    if (tid == 0) MT_TR(tile, 4);
 
     const int dg = std::min(tid * kIPT, len);
     int lo = std::max(0, dg - nyt), hi = std::min(dg, nxt);
@@ -688,6 +713,7 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
       tile_total += v;
     }
     const uint32_t excl = wpre + incl - cnt;
+    if (tid == 0) MT_TR(tile, 5);
     if (tid == 0) {
       spt::st_relaxed64(p.status + ((size_t)tile << kSS),
                         tag | ((tile == 0 ? kFlagP : kFlagA) << 32) | tile_total);
@@ -699,6 +725,7 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
       spt::mbar_arrive(lbfull + r);
     }
     if (it > 0) flush(it - 1);
+    if (tid == 0) MT_TR(tile, 6);
 #pragma unroll
     for (int k = 0; k < kIPT; ++k) {
       pkey[k] = key[k];
@@ -877,3 +904,9 @@ extern "C" int spt_tew_f32(spt_ctx* ctx, const spt_coo* x, const spt_coo* y, int
   }
   return SPT_OK;
 }
+
+#ifdef SPT_MERGE_TRACE
+extern "C" __attribute__((visibility("default"))) int spt_debug_merge_trace(void* dst) {
+  return cudaMemcpyFromSymbol(dst, g_mtrace, sizeof(g_mtrace)) == cudaSuccess ? 0 : 5;
+}
+#endif
