@@ -1463,7 +1463,8 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
           Vec<VEC>::store(p.out + (size_t)run_row * p.R + col, o);
           if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[run_row - f_lo], run_row, col, s_hid, t0);
         }
-        if (row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
+        // TTM rows are consecutive fibers: no gaps to zero
+        if (!FIBER && row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
       }
       run_row = row;
 #pragma unroll
@@ -1512,7 +1513,7 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
             Vec<VEC>::store(p.out + (size_t)w_cur * p.R + col, o);
             if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[w_cur - f_lo], w_cur, col, s_hid, t0);
           }
-          if (g != cur_g && row > w_cur + 1 && writer)
+          if (!FIBER && g != cur_g && row > w_cur + 1 && writer)
             zero_rows<VEC>(p.out, w_cur + 1, row, p.R, col, true);
         }
         w_cur = row;
@@ -1532,14 +1533,17 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
     head_acc[k] = boundary ? h_acc[k] : w_acc[k];
     tail_acc[k] = w_acc[k];
   }
-  if (prev_row != kNone && prev_row > head_row && lane == 0) atomicMin(p.err + 2, (unsigned long long)t0);
-  if (next_row != kNone && next_row < tail_row && lane == 0)
-    atomicMin(p.err + 2, (unsigned long long)(t0 + cnt));
+  if constexpr (!FIBER) {
+    if (prev_row != kNone && prev_row > head_row && lane == 0)
+      atomicMin(p.err + 2, (unsigned long long)t0);
+    if (next_row != kNone && next_row < tail_row && lane == 0)
+      atomicMin(p.err + 2, (unsigned long long)(t0 + cnt));
+  }
   const bool cont_prev = prev_row == head_row;
   const bool cont_next = next_row == tail_row;
 
-  // ---- inter-tile zero fill
-  if (writer) {
+  // ---- inter-tile zero fill (MTTKRP: rows without entries)
+  if (!FIBER && writer) {
     if (tile == 0) zero_rows<VEC>(p.out, 0, head_row, p.R, col, true);
     const uint32_t stop = next_row == kNone ? p.rows : next_row;
     if (tail_row + 1 < stop) zero_rows<VEC>(p.out, tail_row + 1, stop, p.R, col, true);
