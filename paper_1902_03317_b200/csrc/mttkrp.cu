@@ -1292,40 +1292,73 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
     prev_row = __shfl_sync(0xffffffffu, prev_row, 0);
     next_row = __shfl_sync(0xffffffffu, next_row, 1);
   } else {
-    // TTM: rows are fiber ids. Head tuples of the tile's entries, the fptr
-    // slice of the fibers touching it, head flags, and each entry's fiber.
+    // TTM: rows are fiber ids. Head tuples of the tile's entries and the head
+    // flags: a fiber starts where the non-mode tuple changes (x is coalesced
+    // and sorted with `mode` last -- build_fiber_index's definition,
+    // P/src/tensor.cpp:92-120), compared in registers as the tuples are
+    // staged, so no fptr slice sits behind the tile map on the critical path.
+    // Each entry's fiber = the tile's first fiber (map) + heads so far.
     f_lo = __ldg(p.tile_fiber + tile);
-    for (uint32_t j = 0; j + 1 < p.N; ++j) {
-      if (cnt == kWT && spt::aligned16(p.hnm[j])) {
-#pragma unroll
-        for (int r = 0; r < kWT / 128; ++r) {
-          const int i = lane + 32 * r;  // uint4 chunk
-          reinterpret_cast<uint4*>(s_hid + j * kWTP)[i + (i >> 3)] =
-              spt::ld_stream(reinterpret_cast<const uint4*>(p.hnm[j] + t0) + i);
-        }
-      } else {
-        for (int i = lane; i < kWT; i += 32)
-          s_hid[j * kWTP + sw(i)] = i < cnt ? p.hnm[j][t0 + i] : 0u;
-      }
-    }
-    reinterpret_cast<uint2*>(s_hd)[lane] = make_uint2(0u, 0u);
-    __syncwarp();
     const uint64_t t_end = t0 + cnt;
-    uint64_t next_start = ~0ull;
+    const uint32_t nhd = p.N - 1;  // non-mode dims
+    uint32_t nb = 0;  // lane j: hnm[j][t0 - 1]; lane 16 + j: hnm[j][t_end]
+    if (lane < nhd && t0 > 0) nb = p.hnm[lane][t0 - 1];
+    if (lane >= 16 && lane - 16 < nhd && t_end < p.nnz) nb = p.hnm[lane - 16][t_end];
+    bool vec = cnt == kWT;
+    for (uint32_t j = 0; j < nhd; ++j) vec = vec && spt::aligned16(p.hnm[j]);
+    bool eq_next = t_end < p.nnz;
+    if (vec) {
+      constexpr int kR = kWT / 128;  // uint4 chunks per lane: entries 128 r + 4 lane + q
+      uint32_t dm[kR];
 #pragma unroll
-    for (int r = 0; r < (kWT + 2 + 31) / 32; ++r) {
-      const uint32_t i = lane + 32 * r;
-      const uint64_t f = (uint64_t)f_lo + i;
-      if (f > p.rows || i >= kWT + 4) continue;
-      const uint32_t st = __ldg(p.fptr + f);
-      s_fp[i] = st;
-      if (st >= t0 && st < t_end) s_hd[st - t0] = 1;
-      if (st >= t_end && st < next_start) next_start = st;
-    }
+      for (int r = 0; r < kR; ++r) dm[r] = 0;
+      for (uint32_t j = 0; j < nhd; ++j) {
+        uint4 c[kR];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t v = __shfl_xor_sync(0xffffffffu, next_start, o);
-      next_start = v < next_start ? v : next_start;
+        for (int r = 0; r < kR; ++r) {
+          const int i = lane + 32 * r;
+          c[r] = spt::ld_stream(reinterpret_cast<const uint4*>(p.hnm[j] + t0) + i);
+          reinterpret_cast<uint4*>(s_hid + j * kWTP)[i + (i >> 3)] = c[r];
+        }
+        const uint32_t pv = __shfl_sync(0xffffffffu, nb, j);
+        const uint32_t nv = __shfl_sync(0xffffffffu, nb, 16 + j);
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          const uint32_t up = __shfl_up_sync(0xffffffffu, c[r].w, 1);
+          const uint32_t wrap = __shfl_sync(0xffffffffu, c[r > 0 ? r - 1 : 0].w, 31);
+          const uint32_t before = lane ? up : (r == 0 ? pv : wrap);
+          dm[r] |= (c[r].x != before ? 1u : 0u) | (c[r].y != c[r].x ? 2u : 0u) |
+                   (c[r].z != c[r].y ? 4u : 0u) | (c[r].w != c[r].z ? 8u : 0u);
+        }
+        eq_next = eq_next && __shfl_sync(0xffffffffu, c[kR - 1].w, 31) == nv;
+      }
+      if (t0 == 0 && lane == 0) dm[0] |= 1u;  // the tensor's first entry
+#pragma unroll
+      for (int r = 0; r < kR; ++r)
+        reinterpret_cast<uint32_t*>(s_hd)[32 * r + lane] =
+            (dm[r] & 1u) | ((dm[r] >> 1) & 1u) << 8 | ((dm[r] >> 2) & 1u) << 16 |
+            ((dm[r] >> 3) & 1u) << 24;
+    } else {
+      for (uint32_t j = 0; j < nhd; ++j)
+        for (int i = lane; i < kWT; i += 32) s_hid[j * kWTP + sw(i)] = i < cnt ? p.hnm[j][t0 + i] : 0u;
+      __syncwarp();
+      for (uint32_t j = 0; j < nhd; ++j) {
+        const uint32_t nv = __shfl_sync(0xffffffffu, nb, 16 + j);
+        eq_next = eq_next && s_hid[j * kWTP + sw(cnt - 1)] == nv;
+      }
+      bool first_diff = t0 == 0;
+      for (uint32_t j = 0; j < nhd; ++j)
+        first_diff = first_diff || s_hid[j * kWTP + sw(0)] != __shfl_sync(0xffffffffu, nb, j);
+      for (int e = lane; e < kWT; e += 32) {
+        bool h = false;
+        if (e == 0) {
+          h = first_diff;
+        } else if (e < cnt) {
+          for (uint32_t j = 0; j < nhd; ++j)
+            h = h || s_hid[j * kWTP + sw(e)] != s_hid[j * kWTP + sw(e - 1)];
+        }
+        s_hd[e] = h ? 1 : 0;
+      }
     }
     __syncwarp();
     constexpr int kPer = kWT / 32;
@@ -1341,15 +1374,22 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
     const int head0 = __shfl_sync(0xffffffffu, (int)s_hd[0], 0);
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     int hc = incl - nh;
+    // s_fp[local fiber] = an entry of that fiber in this tile (its head, or
+    // entry t0 for the fiber continuing into the tile): any entry carries the
+    // fiber's non-mode tuple, which is all the emission reads from it
+    if (lane == 0 && !head0) s_fp[0] = static_cast<uint32_t>(t0);
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const int e = lane * kPer + q;
-      hc += (e < cnt && s_hd[e]) ? 1 : 0;
+      if (e < cnt && s_hd[e]) {
+        ++hc;
+        s_fp[hc - head0] = static_cast<uint32_t>(t0 + e);
+      }
       s_out[sw(e)] = e < cnt ? f_lo + (uint32_t)(hc - head0) : 0u;
     }
     const uint32_t last_fiber = f_lo + (uint32_t)(total - head0);
     if (tile > 0) prev_row = head0 ? f_lo - 1 : f_lo;
-    if (t_end < p.nnz) next_row = next_start == t_end ? last_fiber + 1 : last_fiber;
+    if (t_end < p.nnz) next_row = eq_next ? last_fiber : last_fiber + 1;
   }
   __syncwarp();
   WT_TR(1);
