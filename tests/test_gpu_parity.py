@@ -453,10 +453,12 @@ def test_mttkrp_tile_shapes_and_alignment(sp, offset, strat):
             assert ok, (dims, mode, worst)
 
 
+@pytest.mark.parametrize("offset", [0, 1])
 @pytest.mark.parametrize("R", [3, 8, 20, 64])
-def test_ttv_ttm_warp_tiles_orders(sp, R):
+def test_ttv_ttm_warp_tiles_orders(sp, R, offset):
     """Warp-tile TTV/TTM at orders 2-4, ragged warp tiles, fibers of every
-    length from 1 to thousands, and R that is not a multiple of 4."""
+    length from 1 to thousands, R that is not a multiple of 4, and unaligned
+    index/value views (scalar staging and head-flag paths)."""
     ops = sp[0]
     rng = np.random.default_rng(R + 101)
     for dims, nnz in (([3000, 40], 50_003), ([30, 40, 2000], 77_777), ([9, 8, 7, 600], 123_001)):
@@ -465,7 +467,7 @@ def test_ttv_ttm_warp_tiles_orders(sp, R):
         for mode in range(N):
             xs = x.copy()
             O.sort_lexicographic(xs, [d for d in range(N) if d != mode] + [mode])
-            dx = dev(sp, xs)
+            dx = dev(sp, xs, offset)
             v = rng.uniform(-1, 1, dims[mode]).astype(np.float32)
             zt, y64, yab = O.ttv(xs, v, mode)
             g = host(ops.ttv(dx, torch.from_numpy(v).cuda(), mode))
