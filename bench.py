@@ -47,6 +47,11 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def _measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
 # ---------------------------------------------------------------------------
 # clocks sampler
 
@@ -806,12 +811,27 @@ def main():
                             "alg_bytes": int(by), "GB_s": round(gbs, 1),
                             "frac": round(gbs / hbm, 4), "nnz_s": op.units / (mean_ms / 1e3),
                             "launches_per_call": op.launches / args.steps}
+    # MTTKRP's second floor: every gathered factor row costs at least one L1
+    # wavefront (<= 128 B) per SM-cycle whether it hits L1, L2 or smem
+    # ("Gather floor")
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    sm_hz = float(_measured_peaks().get("sm_max_mhz", 1965.0)) * 1e6
+    for op in wl.ops:
+        if op.name.startswith("mttkrp"):
+            N, R = len(wl.dims), wl.R
+            wf = wl.nnz * (N - 1) * -(-4 * R // 128)
+            floor_ms = wf / (props.multi_processor_count * sm_hz) * 1e3
+            ops_out[op.name]["gather_floor_ms"] = round(floor_ms, 5)
+            ops_out[op.name]["gather_floor_frac"] = round(floor_ms / ops_out[op.name]["ms"], 4)
     dom = max(wl.ops, key=lambda o: sum(o.times))
     d = ops_out[dom.name]
     roofline = {"bound": "hbm", "achieved": d["GB_s"], "peak": hbm, "unit": "GB/s",
                 "frac": d["frac"], "traffic": None, "kernel": dom.name,
                 "alg_bytes_per_launch": d["alg_bytes"], "peak_source": peak_src,
                 "time_share": round(sum(dom.times) / sum(step_ms), 3)}
+    if "gather_floor_ms" in d:
+        roofline["gather_floor"] = {"ms": d["gather_floor_ms"], "frac": d["gather_floor_frac"],
+                                    "model": "nnz*(N-1)*ceil(4R/128) L1 wavefronts / (SMs * SM clock)"}
     tr = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tr):
         roofline["traffic"] = json.load(open(tr)).get(dom.name)
