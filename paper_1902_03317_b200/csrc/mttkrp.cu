@@ -1184,7 +1184,7 @@ __host__ __device__ constexpr size_t wt_slice(uint32_t n_modes) {
   // group slots; TTM adds the staged entries, fiber offsets, head tuples and
   // head flags (MTTKRP reads its entries through L1)
   return (size_t)2 * (32 / G) * G * VEC * sizeof(double) +
-         (FIBER ? (size_t)(2 + NM1) * kWTP * 4 + (size_t)(kWT + 4) * 4 +
+         (FIBER ? (size_t)(2 + NM1) * kWTP * 4 + (size_t)(kWTP + 4) * 4 +
                       (size_t)(n_modes - 1) * kWTP * 4 + (kWT + 16)
                 : 0);
 }
@@ -1218,8 +1218,8 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
   uint32_t* s_out = reinterpret_cast<uint32_t*>(s_gslot + 2 * P * CB);
   float* s_val = reinterpret_cast<float*>(s_out + kWTP);
   uint32_t* s_oidx = reinterpret_cast<uint32_t*>(s_val + kWTP);
-  uint32_t* s_fp = s_oidx + NM1 * kWTP;           // FIBER: fptr[f_lo + i]
-  uint32_t* s_hid = s_fp + (kWT + 4);              // FIBER: [N-1][kWTP]
+  uint32_t* s_fp = s_oidx + NM1 * kWTP;           // FIBER: [sw(local fiber)] an entry of it
+  uint32_t* s_hid = s_fp + (kWTP + 4);             // FIBER: [N-1][kWTP]
   uint8_t* s_hd = reinterpret_cast<uint8_t*>(s_hid + (FIBER ? (p.N - 1) * kWTP : 0));
   __shared__ uint32_t s_ticket;
   __shared__ uint32_t s_grow_all[kWarps][64];
@@ -1377,13 +1377,13 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
     // s_fp[local fiber] = an entry of that fiber in this tile (its head, or
     // entry t0 for the fiber continuing into the tile): any entry carries the
     // fiber's non-mode tuple, which is all the emission reads from it
-    if (lane == 0 && !head0) s_fp[0] = static_cast<uint32_t>(t0);
+    if (lane == 0 && !head0) s_fp[sw(0)] = static_cast<uint32_t>(t0);
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const int e = lane * kPer + q;
       if (e < cnt && s_hd[e]) {
         ++hc;
-        s_fp[hc - head0] = static_cast<uint32_t>(t0 + e);
+        s_fp[sw(hc - head0)] = static_cast<uint32_t>(t0 + e);
       }
       s_out[sw(e)] = e < cnt ? f_lo + (uint32_t)(hc - head0) : 0u;
     }
@@ -1501,7 +1501,7 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
 #pragma unroll
           for (int k = 0; k < VEC; ++k) o[k] = (float)acc[k];
           Vec<VEC>::store(p.out + (size_t)run_row * p.R + col, o);
-          if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[run_row - f_lo], run_row, col, s_hid, t0);
+          if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[sw(static_cast<int>(run_row - f_lo))], run_row, col, s_hid, t0);
         }
         // TTM rows are consecutive fibers: no gaps to zero
         if (!FIBER && row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
@@ -1551,7 +1551,7 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
 #pragma unroll
             for (int k = 0; k < VEC; ++k) o[k] = (float)w_acc[k];
             Vec<VEC>::store(p.out + (size_t)w_cur * p.R + col, o);
-            if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[w_cur - f_lo], w_cur, col, s_hid, t0);
+            if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[sw(static_cast<int>(w_cur - f_lo))], w_cur, col, s_hid, t0);
           }
           if (!FIBER && g != cur_g && row > w_cur + 1 && writer)
             zero_rows<VEC>(p.out, w_cur + 1, row, p.R, col, true);
@@ -1645,14 +1645,14 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
 #pragma unroll
       for (int k = 0; k < VEC; ++k) o[k] = (float)(carry[k] + head_acc[k]);
       Vec<VEC>::store(p.out + (size_t)head_row * p.R + col, o);
-      if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[head_row - f_lo], head_row, col, s_hid, t0);
+      if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[sw(static_cast<int>(head_row - f_lo))], head_row, col, s_hid, t0);
     }
     if (boundary && !cont_next) {
       float o[VEC];
 #pragma unroll
       for (int k = 0; k < VEC; ++k) o[k] = (float)tail_acc[k];
       Vec<VEC>::store(p.out + (size_t)tail_row * p.R + col, o);
-      if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[tail_row - f_lo], tail_row, col, s_hid, t0);
+      if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[sw(static_cast<int>(tail_row - f_lo))], tail_row, col, s_hid, t0);
     }
   }
   WT_TR(5);
