@@ -553,6 +553,9 @@ class C5(Workload):
     all-reduce of the I_n x R partials."""
 
     name = "c5-mttkrp-tew_eq"
+    # BASELINE configs[4] shards ONE 1B-nnz tensor over the GPUs: every rank
+    # builds the same tensor (same seed) and keeps its shards
+    STRONG = True
 
     def __init__(self, seed, device, scale=1.0):
         from paper_1902_03317_b200 import generate, ops
@@ -577,18 +580,48 @@ class C5(Workload):
         self.y = DeviceCOO(list(self.dims), [i.clone() for i in x.indices],
                            generate.uniform(self.nnz, seed, 77, 0.5, 1.5, device),
                            list(x.sort_order), x.coalesced)
-        self.z = DeviceCOO.empty(self.dims, self.nnz, device)
         self.out = [torch.empty((d, self.R), dtype=torch.float32, device=dev) for d in self.dims]
         n, N, R = self.nnz, 3, self.R
-        self.ops = [Op(f"mttkrp_m{m}",
-                       lambda m=m: allreduce(ops.mttkrp(self.xs[m], self.f, m,
-                                                        ops.MTTKRP_SEGMENTED, out=self.out[m],
-                                                        sync=False)),
-                       n, lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims))
+        world = DIST.get_world_size() if DIST is not None else 1
+        if world == 1:
+            self.z = DeviceCOO.empty(self.dims, self.nnz, device)
+            self.ops = [Op(f"mttkrp_m{m}",
+                           lambda m=m: ops.mttkrp(self.xs[m], self.f, m, ops.MTTKRP_SEGMENTED,
+                                                  out=self.out[m], sync=False),
+                           n, lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims))
+                        for m in range(3)]
+            self.ops.append(Op("tew_eq_mul",
+                               lambda: ops.tew_eq(x, self.y, ops.MUL, out=self.z, sync=False),
+                               n, lambda: 3 * tensor_bytes(n, N)))
+            return
+        # N > 1: MTTKRP on row-aligned nnz shards of each
+        # mode-leading copy, the owned row blocks all-gathered over NCCL (half
+        # the all-reduce's volume); TEW-eq on contiguous nnz shards, no exchange.
+        # Units per rank = nnz / world, so `value` is the whole tensor's nnz/s.
+        from paper_1902_03317_b200 import parallel
+        me = DIST.get_rank()
+        self.blocks = []
+        for m in range(3):
+            rr = parallel.row_aligned_ranges(self.xs[m].indices[m], world)
+            self.blocks.append(parallel.row_blocks(self.xs[m].indices[m], rr, self.dims[m]))
+            self.xs[m] = parallel.slice_coo(self.xs[m], *rr[me])
+        lo, hi = parallel.shard_range(self.nnz, world, me)
+        xe = parallel.slice_coo(x, lo, hi)
+        self.y = parallel.slice_coo(self.y, lo, hi)
+        self.z = DeviceCOO.empty(self.dims, hi - lo, device)
+        share = n / world
+
+        def mt(m):
+            part = lambda s, f, mm: ops.mttkrp(s, f, mm, ops.MTTKRP_SEGMENTED, out=self.out[mm],
+                                               sync=False)
+            return parallel.mttkrp_row_allgather(self.xs[m], self.f, m, self.dims[m], R,
+                                                 self.blocks[m], part)
+        self.ops = [Op(f"mttkrp_m{m}", lambda m=m: mt(m), share,
+                       lambda: (tensor_bytes(n, N) + 4 * R * sum(self.dims)) / world)
                     for m in range(3)]
         self.ops.append(Op("tew_eq_mul",
-                           lambda: ops.tew_eq(x, self.y, ops.MUL, out=self.z, sync=False),
-                           n, lambda: 3 * tensor_bytes(n, N)))
+                           lambda: ops.tew_eq(xe, self.y, ops.MUL, out=self.z, sync=False),
+                           share, lambda: 3 * tensor_bytes(n, N) / world))
 
     def config(self):
         return {"workload": self.name, "baseline_config": "configs[4] (C5)", "dims": self.dims,
@@ -731,7 +764,10 @@ def main():
         DIST = dist
 
     from paper_1902_03317_b200 import _lib
-    wl = WORKLOADS[args.workload](args.seed + 1009 * rank, local, args.scale)
+    W = WORKLOADS[args.workload]
+    # weak scaling: an independent instance per rank; strong (C5): one tensor
+    wl = W(args.seed if getattr(W, "STRONG", False) else args.seed + 1009 * rank, local,
+           args.scale)
     hbm, peak_src = peaks()
 
     if args.impl == "reference":
@@ -869,7 +905,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "scaling": "strong" if getattr(wl, "STRONG", False) else "weak",
+                "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded Philox, BASELINE config shapes; public datasets "
                         "unavailable offline)",
                 "config": {**wl.config(), "l2": "inputs > L2 and L2 flushed before every op",

@@ -7,6 +7,10 @@ SURVEY.md section 8(e):
     come out zero-filled), and the partials are summed with an all-reduce --
     NCCL over NVLink/NVSwitch on the B200 box (the reference's only analogue
     is the private-buffer reduction of par::mttkrp, P/src/kernels_par.cpp:290-319).
+    A row-aligned variant (mttkrp_row_allgather) cuts the shards at row
+    starts instead, so every output row is owned by exactly one rank and the
+    exchange is an all-gather of the owners' row blocks: (G-1)/G of the output
+    per rank instead of the all-reduce's 2(G-1)/G.
   * TEW-eq and TS shard with no communication (contiguous nnz ranges; the
     output stays sharded, rank order = global order).
   * TEW (merge) shards by key range, the distributed form of
@@ -79,3 +83,93 @@ def tew_key_ranges(x_keys: np.ndarray, y_keys: np.ndarray, world: int) -> list:
                   for c in cuts_x[1:-1]]
     cuts_y = [0] + [int(np.searchsorted(y_keys, k, side="left")) for k in split_keys] + [len(y_keys)]
     return [((cuts_x[r], cuts_x[r + 1]), (cuts_y[r], cuts_y[r + 1])) for r in range(world)]
+
+
+def _row_at(rows):
+    """rows[i] as a Python int (u32 values stored in int32 device arrays)."""
+    if isinstance(rows, torch.Tensor):
+        return lambda i: int(rows[i].item()) & 0xFFFFFFFF
+    a = np.asarray(rows)
+    return lambda i: int(a[i]) & 0xFFFFFFFF
+
+
+def _row_search(rows):
+    """(i, right) -> first / one-past-last position of row rows[i]; device
+    arrays are searched in place (1B-entry tensors stay on the GPU)."""
+    if isinstance(rows, torch.Tensor):
+        def f(i, right):
+            v = rows[i:i + 1]
+            if rows.dtype == torch.int32 and int(v.item()) < 0:
+                raise OverflowError("row ids >= 2^31 in an int32 device array: search on the host")
+            return int(torch.searchsorted(rows, v, right=right).item())
+        return f
+    a = np.asarray(rows)
+    a = a.view(np.uint32) if a.dtype == np.int32 else a
+    return lambda i, right: int(np.searchsorted(a, a[i], side="right" if right else "left"))
+
+
+def row_aligned_ranges(rows, world: int) -> list:
+    """Per-rank [lo, hi) entry ranges of a tensor sorted with the output mode
+    leading (`rows` = its mode-n index array, non-decreasing), cut at the row
+    start nearest below each equal-nnz point, so no row is split: a rank owns
+    the rows its entries start. A row longer than nnz/world makes the cut fall
+    back to that row's end (ranks may then be empty)."""
+    find = _row_search(rows)
+    n = len(rows)
+    cuts = [0]
+    for r in range(1, world):
+        t = shard_range(n, world, r)[0]
+        c = n if t >= n else find(t, False)
+        if c <= cuts[-1]:  # the row at t started before the previous cut
+            c = n if t >= n else find(t, True)
+        cuts.append(max(c, cuts[-1]))
+    cuts.append(n)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def row_blocks(rows, ranges: Sequence, n_rows: int) -> list:
+    """Output row block [row_lo, row_hi) owned by each rank: from the first row
+    of its entries to the first row of the next non-empty rank (rows without
+    entries in between belong to the block that precedes them; they are zero
+    in its partial)."""
+    at = _row_at(rows)
+    starts = [at(lo) if hi > lo else None for lo, hi in ranges]
+    blocks, nxt = [None] * len(ranges), n_rows
+    for r in range(len(ranges) - 1, -1, -1):
+        if starts[r] is None:
+            blocks[r] = (nxt, nxt)
+        else:
+            blocks[r] = (starts[r], nxt)
+            nxt = starts[r]
+    first = next((r for r in range(len(ranges)) if starts[r] is not None), None)
+    if first is not None:
+        blocks[first] = (0, blocks[first][1])
+    return blocks
+
+
+def mttkrp_row_allgather(x_shard, factors: Sequence, mode: int, rows: int, rank_R: int,
+                         blocks: Sequence, partial_fn: Optional[Callable] = None,
+                         group=None) -> torch.Tensor:
+    """MTTKRP over row-aligned shards: each rank's partial is exact on the rows
+    it owns (`blocks[rank]`, from row_blocks), and one all-gather of the owned
+    blocks (padded to the largest) assembles the full rows x R result on every
+    rank. Same arithmetic per row as the single-process kernel (no cross-rank
+    sums), half the all-reduce's exchange volume."""
+    if partial_fn is None:
+        from . import ops
+        partial_fn = lambda xs, fs, m: ops.mttkrp(xs, fs, m, ops.MTTKRP_AUTO)  # noqa: E731
+    part = partial_fn(x_shard, factors, mode)
+    assert tuple(part.shape) == (rows, rank_R)
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return part
+    world, me = dist.get_world_size(group), dist.get_rank(group)
+    B = max(1, max(hi - lo for lo, hi in blocks))
+    lo, hi = blocks[me]
+    send = torch.zeros((B, rank_R), dtype=part.dtype, device=part.device)
+    send[: hi - lo] = part[lo:hi]
+    recv = torch.empty((world * B, rank_R), dtype=part.dtype, device=part.device)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    out = torch.empty_like(part)
+    for r, (a, b) in enumerate(blocks):
+        out[a:b] = recv[r * B: r * B + (b - a)]
+    return out

@@ -53,6 +53,12 @@ def _worker(rank, world, port, q):
             part_fn = lambda s, f, m: torch.from_numpy(O.mttkrp(s, f, m)[1].copy())  # fp64 partial
             got = parallel.mttkrp_allreduce(shard, fs, mode, dims[mode], R, part_fn)
             out[f"mttkrp{mode}"] = got.numpy()
+            # row-aligned shards + all-gather of the owned row blocks
+            rr = parallel.row_aligned_ranges(xs.indices[mode], world)
+            blocks = parallel.row_blocks(xs.indices[mode], rr, dims[mode])
+            shard = parallel.slice_coo(xs, *rr[rank])
+            got = parallel.mttkrp_row_allgather(shard, fs, mode, dims[mode], R, blocks, part_fn)
+            out[f"mttkrp_ag{mode}"] = got.numpy()
         # TS / TEW-eq: no communication, shards concatenate in rank order
         lo, hi = parallel.shard_range(x.nnz, world, rank)
         z = O.ts(parallel.slice_coo(x, lo, hi), 2.5, 1)
@@ -97,6 +103,11 @@ def test_two_rank_sharding_matches_single_process():
         _, want, absum = O.mttkrp(x, fs, mode)
         got = out[f"mttkrp{mode}"]
         assert np.all(np.abs(got - want) <= 1e-12 * np.maximum(absum, 1e-300))
+        # row-aligned: every row is computed whole, in the same entry order, on
+        # one rank -> identical to one process on the same mode-sorted tensor
+        xs = x.copy()
+        O.sort_lexicographic(xs, [mode] + [d for d in range(3) if d != mode])
+        assert np.array_equal(out[f"mttkrp_ag{mode}"], O.mttkrp(xs, fs, mode)[1])
     assert np.array_equal(out["ts"].view(np.uint32), O.ts(x, 2.5, 1).values.view(np.uint32))
     y = _tensor(5, dims, 15000)
     z, _ = O.tew(x.copy(), y.copy(), 0)
@@ -113,3 +124,25 @@ def test_shard_range_partitions():
             assert r[0][0] == 0 and r[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
             assert max(h - l for l, h in r) - min(h - l for l, h in r) <= 1
+
+
+def test_row_aligned_ranges_and_blocks():
+    from paper_1902_03317_b200.parallel import row_aligned_ranges, row_blocks
+    rng = np.random.default_rng(7)
+    for n_rows, nnz, world in ((50, 1000, 2), (50, 1000, 8), (1000, 37, 4), (5, 300, 8)):
+        rows = np.sort(rng.zipf(1.3, nnz) % n_rows).astype(np.uint32)
+        rr = row_aligned_ranges(rows, world)
+        assert rr[0][0] == 0 and rr[-1][1] == nnz
+        assert all(a[1] == b[0] for a, b in zip(rr, rr[1:]))
+        for lo, hi in rr:  # no row split across ranks
+            if lo > 0 and lo < nnz:
+                assert rows[lo] != rows[lo - 1]
+        bl = row_blocks(rows, rr, n_rows)
+        assert bl[0][0] == 0 and max(b for _, b in bl) == n_rows
+        covered = sorted(b for b in bl if b[1] > b[0])
+        assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
+        for (lo, hi), (a, b) in zip(rr, bl):  # every entry's row lies in its rank's block
+            assert np.all((rows[lo:hi] >= a) & (rows[lo:hi] < b))
+        # the in-place tensor search (device arrays) gives the same cuts
+        t = torch.from_numpy(rows.astype(np.int32))
+        assert row_aligned_ranges(t, world) == rr and row_blocks(t, rr, n_rows) == bl
