@@ -1,0 +1,184 @@
+"""Parity at BASELINE.json's full sizes (the oracle-sized cases live in
+test_gpu_parity.py). Too large for the CPU oracle, so each check is a
+size-independent property or an on-device recomputation:
+
+* TS, TEW-eq: bit-exact against one IEEE fp32 torch op per stored value
+  (the reference's apply_scalar / apply_elem, P/src/kernel_detail.hpp:19-32),
+  indices identical to x's;
+* TEW merge (C2b, 10M + 10M independent patterns): output keys strictly
+  increasing (sorted, coalesced), the key set equals the union (add) /
+  intersection (mul) of the input key sets, matched values bit-exact x op y,
+  unmatched values copied bit-exactly;
+* sort: non-decreasing keys and the same multiset of tuples (sorted keys equal);
+* MTTKRP (C4, 100M nnz, R=32), TTV (C3, 50M), TTM (C3 mode 2): per output
+  entry within TOL = 1e-5 of an fp64 recomputation (chunked torch index_add
+  over the same fp32 inputs), |y - y64| <= TOL * max(|y64|, sum|terms|).
+"""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+CHUNK = 4_000_000
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1902_03317_b200 import _lib, generate, ops
+    assert _lib.missing_symbols() == []
+    return ops, generate
+
+
+def u32(t):
+    return t.to(torch.int64) & 0xFFFFFFFF
+
+
+def keys(t, order=None):
+    """Linearised tuples (int64; the configs' index spaces fit 63 bits)."""
+    order = order if order is not None else list(range(len(t.dims)))
+    k = torch.zeros(t.nnz, dtype=torch.int64, device=t.values.device)
+    for d in order:
+        k = k * int(t.dims[d]) + u32(t.indices[d][: t.nnz])
+    return k
+
+
+def bits(v):
+    return v.contiguous().view(torch.int32)
+
+
+def test_c1_ts_full(lib):
+    ops, gen = lib
+    x = gen.config_tensor("c1", seed=11, sort_order=[0, 1, 2])
+    s = torch.tensor(2.5, dtype=torch.float32, device="cuda")
+    for op, ref in ((ops.SCALAR_ADD, x.values + s), (ops.SCALAR_MUL, x.values * s)):
+        z = ops.ts(x, 2.5, op)
+        assert torch.equal(bits(z.values), bits(ref))
+        assert all(torch.equal(a, b) for a, b in zip(z.indices, x.indices))
+
+
+def test_c2_tew_eq_full(lib):
+    ops, gen = lib
+    x = gen.config_tensor("c2", seed=21, sort_order=[0, 1, 2])
+    y = x.clone()
+    y.values = gen.uniform(x.nnz, 22, 7, 0.5, 1.5)
+    for op, f in ((ops.ADD, torch.add), (ops.SUB, torch.sub), (ops.MUL, torch.mul),
+                  (ops.DIV, torch.div)):
+        z = ops.tew_eq(x, y, op)
+        assert torch.equal(bits(z.values), bits(f(x.values, y.values))), op
+        assert all(torch.equal(a, b) for a, b in zip(z.indices, x.indices))
+
+
+def test_c2_tew_merge_full(lib):
+    ops, gen = lib
+    x = gen.config_tensor("c2", seed=31, sort_order=[0, 1, 2])
+    y = gen.config_tensor("c2", seed=32, sort_order=[0, 1, 2])
+    kx, ky = keys(x), keys(y)  # independent patterns: ~100 tuples match by chance
+    for op in (ops.ADD, ops.MUL):
+        z = ops.tew(x, y, op)
+        kz = keys(z)
+        assert bool((kz[1:] > kz[:-1]).all()), "output keys strictly increasing"
+        inter = kx[torch.isin(kx, ky)]
+        if op == ops.ADD:
+            assert z.nnz == x.nnz + y.nnz - inter.numel()
+        else:
+            assert z.nnz == inter.numel() and torch.equal(kz, inter)
+        # values: locate each output key in x and y
+        ix = torch.searchsorted(kx, kz).clamp(max=x.nnz - 1)
+        iy = torch.searchsorted(ky, kz).clamp(max=y.nnz - 1)
+        inx, iny = kx[ix] == kz, ky[iy] == kz
+        assert bool((inx | iny).all())
+        xv, yv = x.values[ix], y.values[iy]
+        both = inx & iny
+        want = torch.where(both, xv + yv if op == ops.ADD else xv * yv,
+                           torch.where(inx, xv, yv))
+        assert torch.equal(bits(z.values[: z.nnz]), bits(want)), op
+
+
+def test_c2_sort_full(lib):
+    ops, gen = lib
+    x = gen.config_tensor("c2", seed=41)  # draw order
+    k0 = keys(x)
+    ops.sort_lexicographic(x, [2, 0, 1])
+    k = keys(x, [2, 0, 1])
+    assert bool((k[1:] >= k[:-1]).all())
+    k0p = keys(x)  # the same multiset of tuples as before the sort
+    assert int(k0.sum()) == int(k0p.sum())
+    assert torch.equal(torch.sort(k0).values, torch.sort(k0p).values)
+
+
+def _mttkrp64(x, fs, mode):
+    """fp64 out(i, :) += val * prod_{d != mode} F_d(i_d, :), in chunks; also
+    the sum of |terms| (equal to out for these all-positive inputs)."""
+    R = fs[0].shape[1]
+    out = torch.zeros((x.dims[mode], R), dtype=torch.float64, device="cuda")
+    for a in range(0, x.nnz, CHUNK):
+        b = min(x.nnz, a + CHUNK)
+        t = x.values[a:b].to(torch.float64)[:, None].expand(-1, R).clone()
+        for d in range(len(x.dims)):
+            if d != mode:
+                t *= fs[d][u32(x.indices[d][a:b])].to(torch.float64)
+        out.index_add_(0, u32(x.indices[mode][a:b]), t)
+    return out
+
+
+@pytest.mark.parametrize("mode", [0, 3])
+def test_c4_mttkrp_full(lib, mode):
+    ops, gen = lib
+    c = gen.CONFIGS["c4"]
+    x = gen.config_tensor("c4", seed=51, sort_order=[mode] + [d for d in range(4) if d != mode])
+    fs = [gen.uniform((d, c["R"]), 51, 100 + k, 0.0, 1.0) for k, d in enumerate(c["dims"])]
+    got = ops.mttkrp(x, fs, mode).to(torch.float64)
+    want = _mttkrp64(x, fs, mode)
+    assert bool(((got - want).abs() <= TOL * want.abs()).all())
+
+
+def _fiber_ids(x, fib):
+    f = torch.arange(fib.nfibs, device="cuda", dtype=torch.int64)
+    fptr = u32(fib.fptr)
+    return torch.repeat_interleave(f, fptr[1:] - fptr[:-1], output_size=x.nnz)
+
+
+def test_c3_ttv_full(lib):
+    ops, gen = lib
+    c = gen.CONFIGS["c3"]
+    base = gen.config_tensor("c3", seed=61)
+    for mode in range(3):
+        x = base.clone()
+        ops.sort_lexicographic(x, ops.mode_last_order(3, mode))
+        fib = ops.build_fiber_index(x, mode)
+        v = gen.uniform(c["dims"][mode], 61, 200 + mode, -1.0, 1.0)
+        z = ops.ttv(x, v, mode, fib)
+        fid = _fiber_ids(x, fib)
+        term = x.values.to(torch.float64) * v[u32(x.indices[mode])].to(torch.float64)
+        y64 = torch.zeros(fib.nfibs, dtype=torch.float64, device="cuda").index_add_(0, fid, term)
+        yab = torch.zeros_like(y64).index_add_(0, fid, term.abs())
+        err = (z.values[: fib.nfibs].to(torch.float64) - y64).abs()
+        assert bool((err <= TOL * torch.maximum(y64.abs(), yab)).all()), mode
+        heads = u32(fib.fptr[:-1])
+        others = [d for d in range(3) if d != mode]
+        for j, d in enumerate(others):  # output tuple = the fiber head's non-mode indices
+            assert torch.equal(z.indices[j][: fib.nfibs], x.indices[d][heads]), (mode, d)
+
+
+def test_c3_ttm_full_mode2(lib):
+    ops, gen = lib
+    c = gen.CONFIGS["c3"]
+    mode, R = 2, c["R"]
+    x = gen.config_tensor("c3", seed=71)
+    ops.sort_lexicographic(x, ops.mode_last_order(3, mode))
+    fib = ops.build_fiber_index(x, mode)
+    u = gen.uniform((c["dims"][mode], R), 71, 300, -1.0, 1.0)
+    z = ops.ttm(x, u, mode, fib)
+    fid = _fiber_ids(x, fib)
+    y64 = torch.zeros((fib.nfibs, R), dtype=torch.float64, device="cuda")
+    yab = torch.zeros_like(y64)
+    for a in range(0, x.nnz, CHUNK):
+        b = min(x.nnz, a + CHUNK)
+        t = x.values[a:b].to(torch.float64)[:, None] * u[u32(x.indices[mode][a:b])].to(torch.float64)
+        y64.index_add_(0, fid[a:b], t)
+        yab.index_add_(0, fid[a:b], t.abs())
+    got = z.values[: fib.nfibs * R].view(fib.nfibs, R).to(torch.float64)
+    assert bool(((got - y64).abs() <= TOL * torch.maximum(y64.abs(), yab)).all())
+    r = torch.arange(R, device="cuda", dtype=torch.int32).repeat(fib.nfibs)
+    assert torch.equal(z.indices[mode][: fib.nfibs * R], r)  # mode index = column
