@@ -2110,7 +2110,10 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
   // such a row's chain stalls its CTA (and the tickets it holds); the
   // per-CTA kernel, which sums chains with all 256 threads, is faster there
   // (C4 mode 3 at 100M: 2.71 vs 3.12 ms).
-  if (SPT_MTTKRP_PF && p.vec_ok && x->nnz <= (32ull << 20)) {
+#ifndef SPT_PF_MAX_NNZ
+#define SPT_PF_MAX_NNZ (32ull << 20)
+#endif
+  if (SPT_MTTKRP_PF && p.vec_ok && x->nnz <= SPT_PF_MAX_NNZ) {
     const PfVariant pv = choose_pf(v.G, v.VEC, nm1);
     SPT_CUDA(cudaFuncSetAttribute(pv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(pv.smem)));
