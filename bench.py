@@ -404,6 +404,62 @@ class C1(Workload):
         return {"workload": self.name, "baseline_config": "configs[0] (C1)", "dims": self.dims,
                 "nnz": self.nnz, "R": self.R, "mttkrp_input": "sorted (0,1,2) (mode-0 leading)"}
 
+    # e2e through the C-ABI with host buffers
+    E2E_CHUNKS = 4
+    E2E_PATH = ("ops.* -> C-ABI; pinned host buffers; x uploaded in 4 chunks (TS of each chunk "
+                "and its download overlap the next chunk's upload), factors up, MTTKRP on the "
+                "whole tensor, its I x R result and both TS outputs down")
+
+    def e2e_host(self, device=0):
+        from paper_1902_03317_b200.coo import DeviceCOO
+        from paper_1902_03317_b200.staging import PinnedCOO, Pipeline
+        dev = torch.device(device) if not isinstance(device, int) else torch.device("cuda", device)
+        n = self.nnz
+        return {"pipe": Pipeline(dev),
+                "px": PinnedCOO.from_host(self.x.to_host()),
+                "pf": [f.cpu().pin_memory() for f in self.f],
+                "dx": DeviceCOO(list(self.dims), [torch.empty(n, dtype=torch.int32, device=dev)
+                                                  for _ in self.dims],
+                                torch.empty(n, dtype=torch.float32, device=dev), [0, 1, 2], True),
+                "df": [torch.empty_like(f) for f in self.f],
+                "dz": [DeviceCOO.empty(self.dims, n, dev) for _ in range(2)],
+                "dout": torch.empty((self.dims[0], self.R), dtype=torch.float32, device=dev),
+                "out_ts": [PinnedCOO(self.dims, n) for _ in range(2)],
+                "out_m": torch.empty((self.dims[0], self.R), dtype=torch.float32).pin_memory()}
+
+    def e2e_step(self, host, device):
+        """Pinned host inputs -> MTTKRP + TS add/mul -> pinned host outputs.
+        Returns (h2d, d2h) bytes."""
+        from paper_1902_03317_b200 import ops
+        from paper_1902_03317_b200.staging import Pipeline, chunk_bounds, view
+        pl, px, dx = host["pipe"], host["px"], host["dx"]
+        h2d = d2h = 0
+        pl.begin()
+        with torch.cuda.stream(pl.h2d):
+            for a, b in zip(host["df"], host["pf"]):
+                a.copy_(b, non_blocking=True)
+                h2d += b.numel() * 4
+        b = chunk_bounds(self.nnz, self.E2E_CHUNKS)
+        ev_in = []
+        for lo, hi in zip(b[:-1], b[1:]):
+            h2d += px.upload(dx, lo, hi, pl.h2d)
+            ev_in.append(Pipeline.mark(pl.h2d))
+        with torch.cuda.stream(pl.cmp):
+            for c, (lo, hi) in enumerate(zip(b[:-1], b[1:])):
+                pl.cmp.wait_event(ev_in[c])
+                for k, op in enumerate((ops.SCALAR_ADD, ops.SCALAR_MUL)):
+                    z = ops.ts(view(dx, lo, hi), 2.5, op, out=view(host["dz"][k], lo, hi),
+                               sync=False)
+                    pl.d2h.wait_event(Pipeline.mark(pl.cmp))
+                    d2h += host["out_ts"][k].download(z, pl.d2h, at=lo)
+            ops.mttkrp(dx, host["df"], 0, ops.MTTKRP_SEGMENTED, out=host["dout"], sync=False)
+            pl.d2h.wait_event(Pipeline.mark(pl.cmp))
+        with torch.cuda.stream(pl.d2h):
+            host["out_m"].copy_(host["dout"], non_blocking=True)
+            d2h += host["out_m"].numel() * 4
+        pl.end()
+        return h2d, d2h
+
     def cpu_setup(self, ref, sample_nnz=None):
         c = self.cr = _RefCalls(ref)
         self.hx = c.coo(_host_sample(self.x, self.nnz))

@@ -45,3 +45,29 @@ def test_c2_pipelined_e2e_matches_oracle(scale):
         assert same(_ht(got), ref), op
         n_out += ref.nnz
     assert d2h == (4 * wl.nnz + n_out) * 16
+
+
+@pytest.mark.parametrize("scale", [0.01, 1.0])
+def test_c1_pipelined_e2e_matches_oracle(scale):
+    """C1's host-buffer path (chunked x upload, TS per chunk, MTTKRP on the
+    whole tensor) returns what the oracle computes from the same host data."""
+    import bench
+    wl = bench.C1(20190210, 0, scale)
+    host = wl.e2e_host(0)
+    for _ in range(2):
+        for o in host["out_ts"]:
+            o.val.fill_(np.nan)
+            o.nnz = 0
+        host["out_m"].fill_(np.nan)
+        h2d, d2h = wl.e2e_step(host, "cuda:0")
+        torch.cuda.synchronize()
+    n = wl.nnz
+    assert h2d == n * 16 + sum(f.numel() * 4 for f in wl.f)
+    assert d2h == 2 * n * 16 + host["out_m"].numel() * 4
+    hx = _ht(wl.x.to_host())
+    O = Oracle()
+    for k, op in enumerate((0, 1)):
+        assert same(_ht(host["out_ts"][k].to_host()), O.ts(hx, 2.5, op)), op
+    _, y64, yab = O.mttkrp(hx, [f.cpu().numpy() for f in wl.f], 0)
+    got = host["out_m"].numpy()
+    assert np.all(np.abs(got - y64) <= 1e-5 * np.maximum(np.abs(y64), yab))
