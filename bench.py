@@ -929,7 +929,9 @@ def main():
         roofline["traffic"] = json.load(open(tr)).get(dom.name)
 
     e2e = None
-    if not args.no_e2e and hasattr(wl, "e2e_step") and rank == 0:
+    if not args.no_e2e and hasattr(wl, "e2e_step"):
+        # every rank runs its own host-buffer pipeline (its own PCIe link);
+        # whole-job throughput over the slowest rank, like `value`
         host = wl.e2e_host(local)
         wl.e2e_step(host, f"cuda:{local}")
         torch.cuda.synchronize()
@@ -937,6 +939,8 @@ def main():
         for _ in range(max(2, min(args.steps, 5))):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
+            if dist:
+                dist.barrier()
             torch.cuda.synchronize()
             a.record(stream)
             h2d, d2h = wl.e2e_step(host, f"cuda:{local}")
@@ -944,9 +948,15 @@ def main():
             torch.cuda.synchronize()
             times.append(a.elapsed_time(b))
         ms = statistics.mean(times)
-        e2e = {"value": units_per_step / (ms / 1e3), "unit": "nnz/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        e2e = {"value": world * units_per_step / (ms / 1e3), "unit": "nnz/s",
+               "h2d_bytes_per_step": world * h2d, "d2h_bytes_per_step": world * d2h,
+               "ms_per_step": ms,
                "path": getattr(wl, "E2E_PATH", "ops.* -> C-ABI with pinned host buffers")}
+        del host
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1 and hasattr(wl, "cpu_setup"):
