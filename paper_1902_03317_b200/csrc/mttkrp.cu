@@ -2080,9 +2080,10 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
 #endif
     SPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   SPT_WT_CARVEOUT));
-    int per_sm = 0;
-    SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
     const uint64_t grid = (ntiles + kWarps - 1) / kWarps;
+    int per_sm = 0;
+    if (!SPT_WT_BID)  // tickets unless the grid fits one resident wave
+      SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
     p.bid_tiles = SPT_WT_BID || grid <= (uint64_t)per_sm * ctx->num_sms ? 1 : 0;
     for (uint32_t c0 = 0; c0 < R; c0 += CB) {
       uint32_t epoch;
