@@ -279,6 +279,19 @@ __global__ void tile_fiber_kernel(const uint32_t* fptr, uint32_t nfibs, uint32_t
 // (scalar fp64 payloads); C3's short fibers rarely cross one. A CTA draws one
 // ticket for its 8 consecutive warp tiles, so predecessors are resident.
 
+// Per-tile phase timeline for tune/probe_ttv_trace.py (-DSPT_TTV_TRACE).
+#ifdef SPT_TTV_TRACE
+__device__ unsigned long long g_ttv_trace[65536 * 8];
+__device__ __forceinline__ unsigned long long tgtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TV_TR(k) do { if (lane == 0 && wt < 65536) g_ttv_trace[wt * 8 + (k)] = tgtime(); } while (0)
+#else
+#define TV_TR(k) do {} while (0)
+#endif
+
 template <int NO, int kWT>
 constexpr size_t ttv_wt_slice() {
   return (size_t)(kWT + 8) + (size_t)(kWT + 1) * 4 * (1 + NO);  // heads | zv | zi[NO]
@@ -316,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(Tt
   const uint64_t t0 = (uint64_t)wt * kWT;
   const int cnt = (p.nnz - t0 < (uint64_t)kWT) ? static_cast<int>(p.nnz - t0) : kWT;
   const uint32_t f_lo = __ldg(p.tile_fiber + wt);  // fiber containing entry t0
+  TV_TR(0);
 
   // ---- entries (issued first: the longest round trip)
   const int e0 = lane * kWE;
@@ -346,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(Tt
     }
   }
 
+  TV_TR(1);
   // ---- head flags. x is coalesced and sorted with `mode` last, so a fiber
   // starts exactly where a non-mode index changes (build_fiber_index,
   // P/src/tensor.cpp:92-120): compare each entry's tuple with its
@@ -390,6 +405,7 @@ __global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(Tt
   for (int i = 0; i < kWE; ++i) s_head[e0 + i] = (e0 + i < cnt && hd[i]) ? 1 : 0;
   __syncwarp();
 
+  TV_TR(2);
   // ---- terms, segmented warp scan (fp64), local fiber ids
   float term[kWE];
   bool head[kWE];
@@ -442,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(Tt
   const bool single = last_lf == 0;
   const double tile_tail = __shfl_sync(0xffffffffu, sx, 31);  // sum of the last fiber in this tile
 
+  TV_TR(3);
   // ---- publish the tail partial, then look back for the first fiber's carry
   const uint32_t tag = p.epoch << 3;
   if (cont_nx && lane == 0) {
@@ -462,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(Tt
     for (int o = 16; o > 0; o >>= 1) carry += __shfl_xor_sync(0xffffffffu, carry, o);
   }
 
+  TV_TR(4);
   // ---- stage outputs by local fiber id, then coalesced stores
   int hcount = h_before;
   double run = s_before;
@@ -488,6 +506,7 @@ __global__ void __launch_bounds__(kThreads, kWT == 128 ? 8 : 4) ttv_wt_kernel(Tt
   for (int d = 0; d < NO; ++d)
     for (int o = head_lo + lane; o <= last_lf; o += 32)
       spt::st_stream(p.zidx[d] + f_lo + o, s_zi[d * (kWT + 1) + o]);
+  TV_TR(5);
 }
 
 template <int NO, int kWT>
@@ -638,3 +657,9 @@ extern "C" int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uin
   (void)flags;
   return SPT_OK;
 }
+
+#ifdef SPT_TTV_TRACE
+extern "C" __attribute__((visibility("default"))) int spt_debug_ttv_trace(void* dst) {
+  return cudaMemcpyFromSymbol(dst, g_ttv_trace, sizeof(g_ttv_trace)) == cudaSuccess ? 0 : 5;
+}
+#endif
