@@ -1501,7 +1501,6 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
 #pragma unroll
           for (int k = 0; k < VEC; ++k) o[k] = (float)acc[k];
           Vec<VEC>::store(p.out + (size_t)run_row * p.R + col, o);
-          if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[sw(static_cast<int>(run_row - f_lo))], run_row, col, s_hid, t0);
         }
         // TTM rows are consecutive fibers: no gaps to zero
         if (!FIBER && row > run_row + 1) zero_rows<VEC>(p.out, run_row + 1, row, p.R, col, col_ok);
@@ -1551,7 +1550,6 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
 #pragma unroll
             for (int k = 0; k < VEC; ++k) o[k] = (float)w_acc[k];
             Vec<VEC>::store(p.out + (size_t)w_cur * p.R + col, o);
-            if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[sw(static_cast<int>(w_cur - f_lo))], w_cur, col, s_hid, t0);
           }
           if (!FIBER && g != cur_g && row > w_cur + 1 && writer)
             zero_rows<VEC>(p.out, w_cur + 1, row, p.R, col, true);
@@ -1645,14 +1643,28 @@ __global__ void __launch_bounds__(kThreads, SPT_WT_MINB) mttkrp_wt_kernel(Mttkrp
 #pragma unroll
       for (int k = 0; k < VEC; ++k) o[k] = (float)(carry[k] + head_acc[k]);
       Vec<VEC>::store(p.out + (size_t)head_row * p.R + col, o);
-      if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[sw(static_cast<int>(head_row - f_lo))], head_row, col, s_hid, t0);
     }
     if (boundary && !cont_next) {
       float o[VEC];
 #pragma unroll
       for (int k = 0; k < VEC; ++k) o[k] = (float)tail_acc[k];
       Vec<VEC>::store(p.out + (size_t)tail_row * p.R + col, o);
-      if constexpr (FIBER) wt_emit_idx<VEC, NT>(p, s_fp[sw(static_cast<int>(tail_row - f_lo))], tail_row, col, s_hid, t0);
+    }
+  }
+  if constexpr (FIBER) {
+    // TTM output index rows of every fiber completed in this tile, written by
+    // the whole warp at the end: consecutive lanes cover consecutive
+    // (fiber, column-vector) pairs, so each store instruction fills 512
+    // contiguous bytes (full lines) instead of 8 scattered 64-byte pieces.
+    const bool head_done = boundary || !cont_next;
+    const bool tail_done = boundary ? !cont_next : head_done;
+    const uint32_t fa = head_done ? head_row : head_row + 1;
+    const uint32_t fb = tail_done ? tail_row + 1 : tail_row;  // exclusive
+    const uint32_t per = p.ncols / VEC;  // column vectors per fiber
+    const uint32_t total = fb > fa ? (fb - fa) * per : 0u;
+    for (uint32_t c = lane; c < total; c += 32) {
+      const uint32_t f = fa + c / per, k0 = (c % per) * VEC;
+      wt_emit_idx<VEC, NT>(p, s_fp[sw(static_cast<int>(f - f_lo))], f, p.c0 + k0, s_hid, t0);
     }
   }
   WT_TR(5);
