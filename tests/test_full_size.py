@@ -10,7 +10,7 @@ size-independent property or an on-device recomputation:
   intersection (mul) of the input key sets, matched values bit-exact x op y,
   unmatched values copied bit-exactly;
 * sort: non-decreasing keys and the same multiset of tuples (sorted keys equal);
-* MTTKRP (C4, 100M nnz, R=32), TTV (C3, 50M), TTM (C3 mode 2): per output
+* MTTKRP (C4, 100M nnz, R=32), TTV and TTM (C3, 50M, every mode): per output
   entry within TOL = 1e-5 of an fp64 recomputation (chunked torch index_add
   over the same fp32 inputs), |y - y64| <= TOL * max(|y64|, sum|terms|).
 """
@@ -161,10 +161,11 @@ def test_c3_ttv_full(lib):
             assert torch.equal(z.indices[j][: fib.nfibs], x.indices[d][heads]), (mode, d)
 
 
-def test_c3_ttm_full_mode2(lib):
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_c3_ttm_full(lib, mode):
     ops, gen = lib
     c = gen.CONFIGS["c3"]
-    mode, R = 2, c["R"]
+    R = c["R"]
     x = gen.config_tensor("c3", seed=71)
     ops.sort_lexicographic(x, ops.mode_last_order(3, mode))
     fib = ops.build_fiber_index(x, mode)
@@ -182,3 +183,8 @@ def test_c3_ttm_full_mode2(lib):
     assert bool(((got - y64).abs() <= TOL * torch.maximum(y64.abs(), yab)).all())
     r = torch.arange(R, device="cuda", dtype=torch.int32).repeat(fib.nfibs)
     assert torch.equal(z.indices[mode][: fib.nfibs * R], r)  # mode index = column
+    heads = u32(fib.fptr[:-1])
+    for d in range(3):  # other index rows: the fiber head's index, repeated R times
+        if d != mode:
+            want = x.indices[d][heads].repeat_interleave(R)
+            assert torch.equal(z.indices[d][: fib.nfibs * R], want), (mode, d)
