@@ -478,3 +478,27 @@ def test_ttv_ttm_warp_tiles_orders(sp, R, offset):
             g = host(ops.ttm(dx, torch.from_numpy(u).cuda(), mode))
             assert same(HostTensor(g.dims, g.indices, zm.values, g.sort_order, g.coalesced), zm)
             assert within_tol(g.values, y64, yab)[0], (dims, mode, R)
+
+
+@pytest.mark.parametrize("R", [130, 200])
+def test_ttm_mttkrp_many_column_blocks(sp, R):
+    """R beyond one launch's column block (float4 lanes: 128 columns, scalar
+    lanes: 32): several launches, each emitting its own column slice of the
+    values and of the TTM index rows."""
+    ops = sp[0]
+    rng = np.random.default_rng(R)
+    x = rand_tensor(rng, [50, 40, 300], 20_000, -1, 1)
+    for mode in range(3):
+        xs = x.copy()
+        O.sort_lexicographic(xs, [d for d in range(3) if d != mode] + [mode])
+        u = rng.uniform(-1, 1, (x.dims[mode], R)).astype(np.float32)
+        zm, y64, yab = O.ttm(xs, u, mode)
+        g = host(ops.ttm(dev(sp, xs), torch.from_numpy(u).cuda(), mode))
+        assert same(HostTensor(g.dims, g.indices, zm.values, g.sort_order, g.coalesced), zm)
+        assert within_tol(g.values, y64, yab)[0], (R, mode)
+    xs = x.copy()
+    O.sort_lexicographic(xs, [0, 1, 2])
+    fs = [rng.uniform(0, 1, (d, R)).astype(np.float32) for d in x.dims]
+    _, o64, oab = O.mttkrp(xs, fs, 0)
+    out = ops.mttkrp(dev(sp, xs), [torch.from_numpy(f).cuda() for f in fs], 0).cpu().numpy()
+    assert np.all(np.abs(out - o64) <= TOL * np.maximum(np.abs(o64), oab) + 1e-30)
