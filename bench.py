@@ -657,13 +657,17 @@ class C5(Workload):
         from paper_1902_03317_b200 import parallel
         me = DIST.get_rank()
         self.blocks = []
+        # shards are cloned into their own (16-byte aligned) buffers, so the
+        # kernels keep their vector paths, and the full copies are released
+        lo, hi = parallel.shard_range(self.nnz, world, me)
+        xe = parallel.slice_coo(x, lo, hi).clone()
+        self.y = parallel.slice_coo(self.y, lo, hi).clone()
+        del x
         for m in range(3):
             rr = parallel.row_aligned_ranges(self.xs[m].indices[m], world)
             self.blocks.append(parallel.row_blocks(self.xs[m].indices[m], rr, self.dims[m]))
-            self.xs[m] = parallel.slice_coo(self.xs[m], *rr[me])
-        lo, hi = parallel.shard_range(self.nnz, world, me)
-        xe = parallel.slice_coo(x, lo, hi)
-        self.y = parallel.slice_coo(self.y, lo, hi)
+            self.xs[m] = parallel.slice_coo(self.xs[m], *rr[me]).clone()
+            torch.cuda.empty_cache()
         self.z = DeviceCOO.empty(self.dims, hi - lo, device)
         share = n / world
 
