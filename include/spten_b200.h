@@ -176,6 +176,31 @@ SPT_API int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const* d
                    const uint64_t* rows, const uint64_t* cols, uint32_t mode, float* d_out,
                    int strategy, unsigned flags, void* stream);
 
+/* ---- MTTKRP plans -----------------------------------------------------------
+ * The preprocessing half of seq::mttkrp / par::mttkrp (same contract as
+ * spt_mttkrp_f32, P/include/spten/kernels_seq.hpp:59-61): a copy of x sorted
+ * with `mode` leading and the other modes by decreasing extent, whose most
+ * gathered factor rows are served from shared memory. Built once (timed as
+ * preprocessing, like the reference's sort_s, P/src/bench.cpp:363-368) and
+ * executed any number of times with fresh factor values. Requires R % 16 == 0,
+ * order 2..4, dims < 2^31 (otherwise SPT_EINVAL: use spt_mttkrp_f32). The plan
+ * holds its own copy of x (indices and values): rebuild it if x changes. One
+ * stream at a time per plan. */
+typedef struct spt_mttkrp_plan spt_mttkrp_plan;
+#define SPT_PLAN_NO_HOT 2u /* no shared-memory hot rows (every gather from L2/HBM) */
+SPT_API int spt_mttkrp_plan_create(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint64_t R,
+                                   unsigned flags, spt_mttkrp_plan** out, void* stream);
+/* out = dims[mode] x R row-major (16-byte aligned), fully written. Factors as
+ * for spt_mttkrp_f32 (16-byte aligned, cols == the plan's R). */
+SPT_API int spt_mttkrp_plan_exec(spt_ctx* ctx, const spt_mttkrp_plan* plan,
+                                 const float* const* d_factors, const uint64_t* rows,
+                                 const uint64_t* cols, float* d_out, unsigned flags, void* stream);
+/* Level order (tensor mode per level, outermost first; order-1 entries) and
+ * hot rows per level. Any pointer may be NULL. */
+SPT_API int spt_mttkrp_plan_info(const spt_mttkrp_plan* plan, uint32_t* level_modes,
+                                 uint32_t* hot_per_level, uint32_t* nhot);
+SPT_API void spt_mttkrp_plan_destroy(spt_mttkrp_plan* plan);
+
 /* ---- seeded synthetic generator (bench / test input, not a reference path) --
  * Draws `nnz` distinct tuples: per-mode index distribution `dist[d]`
  * (0 = uniform, s>0 = Zipf(s) over a seeded permutation of ids), duplicates

@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get(
 # P/src/kernels_seq.cpp:32-34). Named after the C++ exceptions.
 SPT_OK, SPT_EINVAL, SPT_EDOMAIN, SPT_EOVERFLOW, SPT_ENOMEM, SPT_ERUNTIME = range(6)
 SPT_FLAG_ASYNC = 1
+SPT_PLAN_NO_HOT = 2  # spt_mttkrp_plan_create flag
 
 # spten::ElemOp / ScalarOp / MttkrpStrategy enumerator values (P/include/spten/ops.hpp:5-7)
 ADD, SUB, MUL, DIV = 0, 1, 2, 3
@@ -99,6 +100,13 @@ _SIGNATURES = {
     "spt_ttm_f32": ([_P, _PCOO, _P, _U64, _U64, _U32, _P, _U64, _PCOO, ctypes.c_uint, _P], _I),
     "spt_mttkrp_f32": ([_P, _PCOO, ctypes.POINTER(_P), _PU64, _PU64, _U32, _P, _I,
                         ctypes.c_uint, _P], _I),
+    "spt_mttkrp_plan_create": ([_P, _PCOO, _U32, _U64, ctypes.c_uint, ctypes.POINTER(_P), _P],
+                               _I),
+    "spt_mttkrp_plan_exec": ([_P, _P, ctypes.POINTER(_P), _PU64, _PU64, _P, ctypes.c_uint, _P],
+                             _I),
+    "spt_mttkrp_plan_info": ([_P, ctypes.POINTER(_U32), ctypes.POINTER(_U32),
+                              ctypes.POINTER(_U32)], _I),
+    "spt_mttkrp_plan_destroy": ([_P], None),
     "spt_gen_coo_f32": ([_P, _PCOO, _U64, ctypes.POINTER(ctypes.c_double), ctypes.c_float,
                          ctypes.c_float, ctypes.POINTER(_U32), _P], _I),
     "spt_gen_uniform_f32": ([_P, _P, _U64, _U64, _U64, ctypes.c_float, ctypes.c_float, _P], _I),

@@ -27,7 +27,7 @@ __all__ = [
     "ADD", "SUB", "MUL", "DIV", "SCALAR_ADD", "SCALAR_MUL", "MTTKRP_AUTO", "MTTKRP_ATOMIC",
     "MTTKRP_SEGMENTED", "MTTKRP_SEGMENTED_CTA", "MTTKRP_SEGMENTED_WARP", "flops",
     "ascending_order", "mode_last_order", "check_deferred", "ts", "tew_eq", "tew", "ttv",
-    "ttm", "mttkrp", "sort_lexicographic", "coalesce", "build_fiber_index",
+    "ttm", "mttkrp", "mttkrp_plan", "MttkrpPlan", "sort_lexicographic", "coalesce", "build_fiber_index",
 ]
 
 
@@ -284,15 +284,13 @@ def ttm(x: DeviceCOO, u: torch.Tensor, mode: int, fib: Optional[FiberIndex] = No
 # MTTKRP (P/src/kernels_seq.cpp:153-174, P/src/kernels_par.cpp:275-337)
 
 
-def mttkrp(x: DeviceCOO, factors: Sequence[Optional[torch.Tensor]], mode: int,
-           strategy: int = MTTKRP_AUTO, out: Optional[torch.Tensor] = None,
-           sync: bool = True) -> torch.Tensor:
-    """Returns the dims[mode] x R row-major fp32 result on the device.
-    factors[mode] is ignored (may be None), as in the reference."""
-    ctx = _ctx(x)
+def _check_factors(x: DeviceCOO, factors, mode: int, who: str = "mttkrp"):
+    """Factor matrices for the C-ABI: contiguous 2-D float32 on x's device
+    (P/src/kernel_detail.hpp:163-173 checks the shapes; the C side checks
+    them again)."""
     N = x.order
     if len(factors) != N:
-        raise InvalidArgument("mttkrp: need one factor matrix per mode")
+        raise InvalidArgument(f"{who}: need one factor matrix per mode")
     fp = (ctypes.c_void_p * N)()
     rows = (ctypes.c_uint64 * N)()
     cols = (ctypes.c_uint64 * N)()
@@ -300,17 +298,107 @@ def mttkrp(x: DeviceCOO, factors: Sequence[Optional[torch.Tensor]], mode: int,
     for d, f in enumerate(factors):
         if d == mode or f is None:
             continue
-        if f.dim() != 2 or f.dtype != torch.float32 or not f.is_contiguous():
-            raise InvalidArgument("mttkrp: factors must be contiguous 2-D float32 tensors")
+        if (f.dim() != 2 or f.dtype != torch.float32 or not f.is_contiguous()
+                or f.device != x.device):
+            raise InvalidArgument(f"{who}: factors must be contiguous 2-D float32 tensors on "
+                                  f"{x.device}")
         fp[d] = ptr(f)
         rows[d] = int(f.shape[0])
         cols[d] = int(f.shape[1])
         R = R or int(f.shape[1])
-    I = x.dims[mode] if mode < N else 0
+    return fp, rows, cols, R
+
+
+def _check_out(out: torch.Tensor, shape, device, who: str) -> None:
+    if (tuple(out.shape) != tuple(shape) or out.dtype != torch.float32
+            or not out.is_contiguous() or out.device != device):
+        raise InvalidArgument(f"{who}: out must be a contiguous float32 {tuple(shape)} tensor "
+                              f"on {device}")
+
+
+class MttkrpPlan:
+    """Preprocessed MTTKRP input (spt_mttkrp_plan_create): a copy of x sorted
+    with `mode` leading and the other modes by decreasing extent, whose most
+    gathered factor rows are served from shared memory. Built once (timed as
+    preprocessing, like the reference's sort_s, P/src/bench.cpp:363-368);
+    `mttkrp(plan, factors, mode)` then runs it with any factor values."""
+
+    def __init__(self, x: DeviceCOO, mode: int, R: int, hot: bool = True):
+        ctx = _ctx(x)
+        self.device, self.mode, self.R, self.dims, self.order = x.device, mode, R, list(x.dims), x.order
+        self.nnz = x.nnz
+        flags = 0 if hot else _lib.SPT_PLAN_NO_HOT
+        h = ctypes.c_void_p()
+        d = x.descriptor()
+        check(_lib.load().spt_mttkrp_plan_create(ctx.handle, ctypes.byref(d), int(mode), int(R),
+                                                 flags, ctypes.byref(h), _stream(x.device)))
+        self.handle = h
+        lm = (ctypes.c_uint32 * max(x.order - 1, 1))()
+        hp = (ctypes.c_uint32 * max(x.order - 1, 1))()
+        nh = ctypes.c_uint32()
+        check(_lib.load().spt_mttkrp_plan_info(h, lm, hp, ctypes.byref(nh)))
+        self.level_modes = list(lm)[: x.order - 1]
+        self.hot_per_level = list(hp)[: x.order - 1]
+        self.nhot = int(nh.value)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.load().spt_mttkrp_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mttkrp_plan(x: DeviceCOO, mode: int, R: int, hot: bool = True) -> MttkrpPlan:
+    return MttkrpPlan(x, mode, R, hot=hot)
+
+
+def mttkrp(x, factors: Sequence[Optional[torch.Tensor]], mode: int,
+           strategy: int = MTTKRP_AUTO, out: Optional[torch.Tensor] = None,
+           sync: bool = True) -> torch.Tensor:
+    """Returns the dims[mode] x R row-major fp32 result on the device.
+    factors[mode] is ignored (may be None), as in the reference. x is a
+    DeviceCOO (any order: AUTO plans a sorted copy, P/src/kernels_seq.cpp:
+    153-174 accepts any order) or an MttkrpPlan."""
+    if isinstance(x, MttkrpPlan):
+        return _mttkrp_plan_exec(x, factors, mode, out, sync)
+    ctx = _ctx(x)
+    N = x.order
+    if N < 2:
+        raise InvalidArgument("mttkrp: input must have order >= 2")
+    if mode >= N:
+        raise InvalidArgument("mttkrp: mode out of range")
+    fp, rows, cols, R = _check_factors(x, factors, mode)
+    I = x.dims[mode]
     if out is None:
         out = torch.empty((I, max(R, 1) if R else 0), dtype=torch.float32, device=x.device)
+    else:
+        _check_out(out, (I, R), x.device, "mttkrp")
     xd = x.descriptor()
     check(_lib.load().spt_mttkrp_f32(ctx.handle, ctypes.byref(xd), fp, rows, cols, int(mode),
                                      ptr(out), int(strategy), _flags(sync), _stream(x.device)))
     flops.record(x.nnz * N * R)
+    return out
+
+
+def _mttkrp_plan_exec(plan: MttkrpPlan, factors, mode: int, out, sync: bool) -> torch.Tensor:
+    if mode != plan.mode:
+        raise InvalidArgument(f"mttkrp: plan was built for mode {plan.mode}, not {mode}")
+    ctx = _lib.Context.get(plan.device.index if plan.device.index is not None else 0)
+
+    class _X:  # shape/device stand-in for _check_factors
+        order, device = plan.order, plan.device
+    fp, rows, cols, R = _check_factors(_X, factors, mode)
+    I = plan.dims[mode]
+    if out is None:
+        out = torch.empty((I, plan.R), dtype=torch.float32, device=plan.device)
+    else:
+        _check_out(out, (I, plan.R), plan.device, "mttkrp")
+    check(_lib.load().spt_mttkrp_plan_exec(ctx.handle, plan.handle, fp, rows, cols, ptr(out),
+                                           _flags(sync), _stream(plan.device)))
+    flops.record(plan.nnz * plan.order * plan.R)
     return out
