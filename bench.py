@@ -1,55 +1,71 @@
 #!/usr/bin/env python
 """Benchmark of the B200 COO sparse-tensor kernels on the BASELINE.json configs.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2]
-                    [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5]
+                    [--impl ours|reference] [--mttkrp plan|seg]
 
 A step is one pass of the workload's ops over its seeded synthetic inputs
-(already resident in HBM). Default workload = BASELINE.json configs[1] (C2):
-TEW-eq add/sub/mul/div on two 10M-nnz tensors sharing a pattern, plus TEW
-add/mul against an independent 10M-nnz pattern. `value` is nonzeros/s over
-all ranks (TEW merge counts nnz_x + nnz_y), each op timed with CUDA events
-on its stream after an L2 flush (inputs are also > L2). `roofline` is for the
-op with the largest time share: algorithmic bytes per launch
-/ mean event duration vs MEASURED_PEAKS.json hbm_gbs. `e2e` times the same ops
-through the C-ABI with pinned host buffers, H2D of the inputs and D2H of the
-outputs inside the timed region. `cpu_baseline` is the reference's own OpenMP
-path (oracle/_ref, compiled from the reference sources) on this host.
+(already resident in HBM). Default workload = the largest single-GPU config,
+BASELINE.json configs[4] (C5): MTTKRP modes 0/1/2 (R=32) + TEW-eq mul on a
+1B-nnz order-3 tensor with Zipf(1.1) modes. MTTKRP runs on plans (csrc/
+mttkrp_plan.cu) built once per mode as preprocessing, timed apart like the
+reference's sort_s (P/src/bench.cpp:363-368). `value` is nonzeros/s over all
+ranks, each op timed with CUDA events on its stream after an L2 flush (inputs
+are also > L2). `roofline` is for the op with the largest time share:
+algorithmic bytes per launch / mean event duration vs
+MEASURED_PEAKS.json hbm_gbs. `e2e` times the same ops through the public API
+(ops.* -> C-ABI) from pinned host buffers: every step uploads the tensors and
+factors, builds the plans, runs the ops and downloads every result.
+`cpu_baseline` is the reference's own OpenMP path (oracle/_ref, compiled from
+the reference sources) on this host, BASELINE.md section 3 protocol.
 
-Multi-GPU (torchrun): every rank runs its own instance of the workload (the
-ops shard with no communication, "weak" scaling), timing = max over ranks.
+--impl reference runs only that CPU path. Its inputs are made by a separate
+process (`bench.py --prep-cpu DIR`, the GPU generator) and read from files,
+so the reference process loads no library of this repository.
+
+Multi-GPU (torchrun): C5 shards ONE tensor (strong scaling, row-aligned
+MTTKRP shards + one all-gather, TEW-eq nnz shards); the other workloads run
+an independent instance per rank (weak scaling). Timing = max over ranks.
 """
 from __future__ import annotations
 
-import argparse
-import json
 import os
-import statistics
-import subprocess
-import sys
-import threading
-import time
 
-import numpy as np
-import torch
+# the reference's OpenMP threads close-bound to cores.
+# Set before any OpenMP runtime is loaded (torch and the reference library
+# both bring libgomp, which reads these once at load).
+os.environ.setdefault("OMP_PROC_BIND", "close")
+os.environ.setdefault("OMP_PLACES", "cores")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import shutil  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import tempfile  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "nonzeros/sec per COO op (MTTKRP/TTM/TTV/TEW/TS) & achieved HBM GB/s vs peak"
-
-
-def peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
-        d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+DEFAULT_WORKLOAD = "c5"
 
 
 def _measured_peaks() -> dict:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     return json.load(open(p)) if os.path.exists(p) else {}
+
+
+def peaks():
+    d = _measured_peaks()
+    if "hbm_gbs" in d:
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
 # ---------------------------------------------------------------------------
@@ -110,250 +126,76 @@ class Clocks:
                 "samples": len(sm)}
 
 
-# ---------------------------------------------------------------------------
-# workloads
-
-
-class Op:
-    def __init__(self, name, fn, units, bytes_fn, e2e=None, prep=None):
-        self.name, self.fn, self.units, self.bytes_fn = name, fn, units, bytes_fn
-        self.prep = prep  # untimed setup before each call (e.g. restore an unsorted input)
-        self.times = []
-        self.launches = 0
-
-
-def report_rows(wl, ops_list):
-    """Reference-schema rows (variant "gpu") for --report; flops are the
-    sequential reference's counts (P/src/kernels_seq.cpp:37,51,65,99,144,172)."""
-    from paper_1902_03317_b200 import report
-    rows = []
-    N = len(wl.dims)
-    R = getattr(wl, "R", 0)
-    for op in ops_list:
-        name = op.name
-        kind, _, rest = name.rpartition("_") if name.startswith("tew_eq") else name.partition("_")
-        mode = opn = None
-        if name.startswith("tew_eq"):
-            kernel, opn = "tew_eq", name.split("_")[-1]
-            fl = wl.nnz
-        elif name.startswith("tew_"):
-            kernel, opn = "tew", rest
-            nz = wl.nz[opn]
-            fl = 2 * wl.nnz - nz if opn == "add" else nz
-        elif name.startswith("ts_"):
-            kernel, opn, fl = "ts", rest, wl.nnz
-        else:
-            kernel, mode = kind, rest.lstrip("m")
-            fl = {"ttv": 2 * wl.nnz, "ttm": 2 * R * wl.nnz, "mttkrp": N * R * wl.nnz}[kernel]
-        rows.append(report.bench_report(wl.name, wl.dims, wl.nnz, kernel,
-                                        [t / 1e3 for t in op.times], fl, op=opn, mode=mode,
-                                        rank=R if kernel in ("ttm", "mttkrp") else 0))
-    return rows
-
-
 def tensor_bytes(nnz, order):
     return nnz * (4 * order + 4)
 
 
-DIST = None  # torch.distributed when running under torchrun with N > 1
+# ===========================================================================
+# CPU legs: the reference library's own kernels (oracle/_ref/libspten_ref.so)
+# on host arrays. Nothing here imports torch or loads a library of this repo.
 
 
-def allreduce(t):
-    """MTTKRP's one exchange step: every rank holds the
-    dims[n] x R partial of its own nnz shard; NCCL all-reduce over NVLink."""
-    if DIST is not None:
-        DIST.all_reduce(t, op=DIST.ReduceOp.SUM)
-    return t
+def host_record() -> dict:
+    """nproc, lscpu model, free -g."""
+    rec = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                rec["cpu_model"] = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    try:
+        out = subprocess.run(["free", "-g"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Mem:"):
+                rec["mem_total_gb"] = int(ln.split()[1])
+    except (OSError, subprocess.SubprocessError, ValueError, IndexError):
+        pass
+    rec["omp"] = {k: os.environ.get(k) for k in ("OMP_PROC_BIND", "OMP_PLACES")}
+    return rec
 
 
-class Workload:
-    name = ""
-    desc = ""
-
-    def config(self):
-        return {}
-
-
-class C2(Workload):
-    """BASELINE configs[1]: TEW-eq x4 (shared pattern) + TEW add/mul (independent)."""
-
-    name = "c2-tew_eq-tew"
-
-    def __init__(self, seed, device, scale=1.0):
-        from paper_1902_03317_b200 import generate, ops
-        from paper_1902_03317_b200.coo import DeviceCOO
-        c = generate.CONFIGS["c2"]
-        self.dims = c["dims"]
-        self.nnz = int(c["nnz"] * scale)
-        self.x = generate.coo(self.dims, self.nnz, seed, c["zipf"], 0.5, 1.5, [0, 1, 2], device)
-        self.y = DeviceCOO(list(self.dims), [i.clone() for i in self.x.indices],
-                           generate.uniform(self.nnz, seed, 77, 0.5, 1.5, device), [0, 1, 2],
-                           True)
-        self.y2 = generate.coo(self.dims, self.nnz, seed + 7919, c["zipf"], 0.5, 1.5, [0, 1, 2],
-                               device)
-        self.z = DeviceCOO.empty(self.dims, self.nnz, device)
-        self.zu = DeviceCOO.empty(self.dims, 2 * self.nnz, device)
-        self.cnt = torch.zeros(2, dtype=torch.int64, device=f"cuda:{device}")
-        # union / intersection sizes (for the algorithmic byte count)
-        nz_add = ops.tew(self.x, self.y2, ops.ADD).nnz
-        nz_mul = ops.tew(self.x, self.y2, ops.MUL).nnz
-        self.nz = {"add": nz_add, "mul": nz_mul}
-        n, N = self.nnz, 3
-        self.ops = []
-        for opn, op in (("add", ops.ADD), ("sub", ops.SUB), ("mul", ops.MUL), ("div", ops.DIV)):
-            self.ops.append(Op(f"tew_eq_{opn}",
-                               (lambda op=op: ops.tew_eq(self.x, self.y, op, out=self.z,
-                                                         sync=False)),
-                               n, lambda: 3 * tensor_bytes(n, N)))
-        for opn, op, k in (("add", ops.ADD, 0), ("mul", ops.MUL, 1)):
-            nz = self.nz[opn]
-            self.ops.append(Op(f"tew_{opn}",
-                               (lambda op=op, k=k: ops.tew_device(self.x, self.y2, op, self.zu,
-                                                                  self.cnt[k:k + 1])),
-                               2 * n, (lambda nz=nz: tensor_bytes(2 * n + nz, N))))
-
-    def config(self):
-        return {"workload": self.name, "baseline_config": "configs[1] (C2)", "dims": self.dims,
-                "nnz": self.nnz, "order": 3, "values": "U[0.5,1.5)",
-                "pattern": "uniform distinct tuples, sorted (0,1,2)",
-                "tew_second_pattern_nnz": self.nnz, "tew_union": self.nz["add"],
-                "tew_intersection": self.nz["mul"]}
-
-    # e2e through the C-ABI with host buffers
-    def host_inputs(self):
-        hx, hy, hy2 = self.x.to_host(), self.y.to_host(), self.y2.to_host()
-        return [hx, hy, hy2]
-
-    E2E_CHUNKS = 8
-    E2E_PATH = ("ops.* -> C-ABI; pinned host buffers; H2D / kernels / D2H overlapped on three "
-                "streams (staging.Pipeline), x/y uploaded in 8 chunks")
-
-    def e2e_step(self, host, device):
-        """Pinned host inputs -> the 6 ops -> pinned host outputs, pipelined on
-        three streams (staging.Pipeline): x/y go up in chunks and each chunk's
-        four tew_eq results go down while the next chunk computes, y2 goes up
-        under the tew_eq downloads, then the two merges run and their
-        outputs come down. Returns (h2d, d2h) bytes."""
-        from paper_1902_03317_b200 import ops
-        from paper_1902_03317_b200.staging import Pipeline, chunk_bounds, view
-        pl = host["pipe"]
-        (px, py, py2), (dx, dy, dy2) = host["pinned"], host["dev"]
-        h2d = d2h = 0
-        pl.begin()
-        b = chunk_bounds(self.nnz, self.E2E_CHUNKS)
-        ev_in = []
-        for lo, hi in zip(b[:-1], b[1:]):
-            h2d += px.upload(dx, lo, hi, pl.h2d) + py.upload(dy, lo, hi, pl.h2d)
-            ev_in.append(Pipeline.mark(pl.h2d))
-        h2d += py2.upload(dy2, 0, self.nnz, pl.h2d)
-        ev_y2 = Pipeline.mark(pl.h2d)
-        with torch.cuda.stream(pl.cmp):
-            for c, (lo, hi) in enumerate(zip(b[:-1], b[1:])):
-                pl.cmp.wait_event(ev_in[c])
-                for k, op in enumerate((ops.ADD, ops.SUB, ops.MUL, ops.DIV)):
-                    z = ops.tew_eq(view(dx, lo, hi), view(dy, lo, hi), op,
-                                   out=view(host["dz"][k], lo, hi), sync=False)
-                    pl.d2h.wait_event(Pipeline.mark(pl.cmp))
-                    d2h += host["out_eq"][k].download(z, pl.d2h, at=lo)
-            pl.cmp.wait_event(ev_y2)
-            for k, op in enumerate((ops.ADD, ops.MUL)):
-                zu = host["dzu"][k]
-                z = ops.tew(dx, dy2, op, out=view(zu, 0, zu.nnz))  # syncs pl.cmp only; raises
-                # any deferred tew_eq error (sticky device error words)
-                pl.d2h.wait_event(Pipeline.mark(pl.cmp))
-                d2h += host["out_tew"][k].download(z, pl.d2h)
-        pl.end()
-        return h2d, d2h
-
-    def e2e_host(self, device=0):
-        from paper_1902_03317_b200.coo import DeviceCOO
-        from paper_1902_03317_b200.staging import PinnedCOO, Pipeline
-        dev = torch.device(device) if not isinstance(device, int) else torch.device("cuda", device)
-        n = self.nnz
-        return {"pipe": Pipeline(dev),
-                "pinned": [PinnedCOO.from_host(h) for h in self.host_inputs()],
-                "dev": [DeviceCOO(list(self.dims), [torch.empty(n, dtype=torch.int32, device=dev)
-                                                    for _ in self.dims],
-                                  torch.empty(n, dtype=torch.float32, device=dev), [0, 1, 2],
-                                  True) for _ in range(3)],
-                "dz": [DeviceCOO.empty(self.dims, n, dev) for _ in range(4)],
-                "dzu": [DeviceCOO.empty(self.dims, 2 * n, dev),
-                        DeviceCOO.empty(self.dims, n, dev)],
-                "out_eq": [PinnedCOO(self.dims, n) for _ in range(4)],
-                "out_tew": [PinnedCOO(self.dims, 2 * n), PinnedCOO(self.dims, n)]}
-
-    # reference CPU path (oracle/_ref = the reference library)
-    def cpu_setup(self, ref, sample_nnz=None):
-        from oracle.oracle import HostTensor
-        hx, hy, hy2 = self.host_inputs()
-        T = lambda h: HostTensor(h.dims, h.indices, h.values, h.sort_order, h.coalesced)
-        self.h = [ref.coo(T(hx)), ref.coo(T(hy)), ref.coo(T(hy2))]
-        self.cpu_units = 4 * self.nnz + 2 * 2 * self.nnz
-        return f"full C2 workload (4 x tew_eq on {self.nnz} nnz + tew add/mul on " \
-               f"{self.nnz} + {self.nnz} nnz), par:: kernels"
-
-    def cpu_step(self, ref, nthreads):
-        import ctypes
-        hx, hy, hy2 = self.h
-        lib = ref.lib
-        out = ctypes.c_void_p()
-        for op in range(4):
-            ref._check(lib.ref_tew_eq(hx, hy, op, 1, nthreads, ctypes.byref(out)))
-            lib.ref_coo_free(out.value)
-        for op in (0, 2):
-            ref._check(lib.ref_tew(hx, hy2, op, 1, nthreads, ctypes.byref(out)))
-            lib.ref_coo_free(out.value)
-        return self.cpu_units
-
-
-# ---------------------------------------------------------------------------
-# Reference CPU legs (oracle/_ref = the reference library, par:: kernels with
-# every host thread) shared by the workloads' cpu_setup / cpu_step.
-
-
-def _host_sample(t, k):
-    """The first k entries of a device tensor as a HostTensor (a prefix of a
-    sorted, coalesced tensor is sorted and coalesced, and its fibers are whole
-    except possibly the last)."""
+def _host_tensor(arrays, prefix, dims, sort_order, n=None):
     from oracle.oracle import HostTensor
-    k = min(k, t.nnz)
-    return HostTensor(list(t.dims), [ix[:k].cpu().numpy().view(np.uint32).copy()
-                                     for ix in t.indices],
-                      t.values[:k].cpu().numpy().copy(),
-                      None if t.sort_order is None else list(t.sort_order), t.coalesced)
+    N = len(dims)
+    idx = [arrays[f"{prefix}i{d}"][:n] for d in range(N)]
+    return HostTensor(list(dims), [np.ascontiguousarray(a, dtype=np.uint32) for a in idx],
+                      np.ascontiguousarray(arrays[f"{prefix}val"][:n], dtype=np.float32),
+                      None if sort_order is None else list(sort_order), True)
 
 
-class _RefCalls:
-    """Handles for the reference's par:: kernels on fixed inputs."""
+class CpuLeg:
+    """A bounded sample of one workload on the reference's par:: kernels.
+    MTTKRP calls time both strategies once and keep
+    the faster; `seq()` runs the same ops with seq:: on one core."""
 
-    def __init__(self, ref):
+    def __init__(self, ref, nthreads):
         import ctypes
-        self.ref, self.lib, self.ct = ref, ref.lib, ctypes
-        self.keep = []
+        self.ref, self.lib, self.ct, self.nt = ref, ref.lib, ctypes, nthreads
+        self.keep, self.calls, self.strategy = [], [], {}
 
+    # handles
     def coo(self, ht):
         h = self.ref.coo(ht)
-        self.keep.append(("coo", h))
+        self.keep.append(h)
         return h
 
     def matrix(self, a):
-        import numpy as np
         a = np.ascontiguousarray(a, dtype=np.float32)
-        self.keep.append(("arr", a))
-        f32p = self.ct.POINTER(self.ct.c_float)
-        return self.lib.ref_matrix_new(a.ctypes.data_as(f32p), a.shape[0], a.shape[1])
+        self.keep.append(a)
+        return self.lib.ref_matrix_new(a.ctypes.data_as(self.ct.POINTER(self.ct.c_float)),
+                                       a.shape[0], a.shape[1])
 
     def vector(self, a):
-        import numpy as np
         a = np.ascontiguousarray(a, dtype=np.float32)
-        self.keep.append(("arr", a))
-        f32p = self.ct.POINTER(self.ct.c_float)
-        return self.lib.ref_vector_new(a.ctypes.data_as(f32p), a.shape[0])
+        self.keep.append(a)
+        return self.lib.ref_vector_new(a.ctypes.data_as(self.ct.POINTER(self.ct.c_float)),
+                                       a.shape[0])
 
     def factors(self, hx, mats):
-        """One reference factor vector (the matrices are copied into it, so the
-        temporaries go at once -- C5's factors are 1.28 GB each)."""
-        import numpy as np
+        """One reference factor vector (matrices copied in; the temporaries go
+        at once -- C5's factors are 1.28 GB each)."""
         f32p = self.ct.POINTER(self.ct.c_float)
         hs = (self.ct.c_void_p * len(mats))()
         for d, m in enumerate(mats):
@@ -364,36 +206,239 @@ class _RefCalls:
             self.lib.ref_matrix_free(h)
         return fv
 
-    def run(self, fn, *args, kind="coo"):
+    def _run(self, fn, *args, kind="coo"):
         out = self.ct.c_void_p()
         self.ref._check(fn(*args, self.ct.byref(out)))
         (self.lib.ref_matrix_free if kind == "matrix" else self.lib.ref_coo_free)(out.value)
 
-    def mttkrp(self, hx, fv, mode, nt):  # privatize: the strategy the paper reports
-        self.run(self.lib.ref_mttkrp_fv, hx, fv, mode, 1, nt, 0, kind="matrix")
+    # op builders: each call is (name, units, fn(variant, nthreads))
+    def add(self, name, units, fn):
+        self.calls.append((name, units, fn))
+
+    def add_mttkrp(self, name, units, hx, fv, mode):
+        def fn(variant, nt, strat=None):
+            s = self.strategy.get(name, 0) if strat is None else strat
+            self._run(self.lib.ref_mttkrp_fv, hx, fv, mode, variant, nt, s, kind="matrix")
+        self.calls.append((name, units, fn))
+
+    def calibrate(self) -> dict:
+        """Time privatize and atomic once per MTTKRP call; keep the faster."""
+        rec = {}
+        for name, _, fn in self.calls:
+            if not name.startswith("mttkrp"):
+                continue
+            t = {}
+            for s, sname in ((0, "privatize"), (1, "atomic")):
+                t0 = time.perf_counter()
+                fn(1, self.nt, s)
+                t[sname] = time.perf_counter() - t0
+            best = min(t, key=t.get)
+            self.strategy[name] = 0 if best == "privatize" else 1
+            rec[name] = {"privatize_s": round(t["privatize"], 4), "atomic_s": round(t["atomic"], 4),
+                         "chosen": best}
+        return rec
+
+    def units(self) -> int:
+        return sum(u for _, u, _ in self.calls)
+
+    def step(self) -> int:
+        for _, _, fn in self.calls:
+            fn(1, self.nt)
+        return self.units()
+
+
+def _cpu_leg(name, ref, arrays, meta, nthreads):
+    """Build the CpuLeg of workload `name` from host arrays (CPU-only)."""
+    leg = CpuLeg(ref, nthreads)
+    dims = meta["dims"]
+    N = len(dims)
+    if name == "c1":
+        hx = leg.coo(_host_tensor(arrays, "x_", dims, meta["sort_order"]))
+        fv = leg.factors(hx, [arrays[f"f{d}"] for d in range(N)])
+        n = meta["sample_nnz"]
+        leg.add_mttkrp("mttkrp_m0", n, hx, fv, 0)
+        for op, nm in ((0, "ts_add"), (1, "ts_mul")):
+            leg.add(nm, n, lambda v, nt, op=op: leg._run(leg.lib.ref_ts, hx, 2.5, op, v, nt))
+    elif name == "c2":
+        hx = leg.coo(_host_tensor(arrays, "x_", dims, meta["sort_order"]))
+        from oracle.oracle import HostTensor
+        hxt = _host_tensor(arrays, "x_", dims, meta["sort_order"])
+        hy = leg.coo(HostTensor(hxt.dims, hxt.indices, np.ascontiguousarray(arrays["yval"]),
+                                hxt.sort_order, True))
+        hy2 = leg.coo(_host_tensor(arrays, "y2_", dims, meta["sort_order"]))
+        n = meta["sample_nnz"]
+        for op, nm in ((0, "tew_eq_add"), (1, "tew_eq_sub"), (2, "tew_eq_mul"), (3, "tew_eq_div")):
+            leg.add(nm, n, lambda v, nt, op=op: leg._run(leg.lib.ref_tew_eq, hx, hy, op, v, nt))
+        for op, nm in ((0, "tew_add"), (2, "tew_mul")):
+            leg.add(nm, 2 * n, lambda v, nt, op=op: leg._run(leg.lib.ref_tew, hx, hy2, op, v, nt))
+    elif name == "c3":
+        for m in range(N):
+            hx = leg.coo(_host_tensor(arrays, f"m{m}_", dims, meta["sort_orders"][m]))
+            fib = leg.lib.ref_fiber_new(hx, m)  # preprocessing, untimed (P/src/bench.cpp:363-368)
+            leg.keep.append(("fib", fib))
+            hv, hu = leg.vector(arrays[f"v{m}"]), leg.matrix(arrays[f"u{m}"])
+            n = meta["sample_nnz"]
+            leg.add(f"ttv_m{m}", n, lambda v, nt, hx=hx, hv=hv, m=m, fib=fib:
+                    leg._run(leg.lib.ref_ttv_fib, hx, hv, m, fib, v, nt))
+            leg.add(f"ttm_m{m}", n, lambda v, nt, hx=hx, hu=hu, m=m, fib=fib:
+                    leg._run(leg.lib.ref_ttm_fib, hx, hu, m, fib, v, nt))
+    elif name in ("c4", "c5"):
+        fv = None
+        for m in range(N):
+            hx = leg.coo(_host_tensor(arrays, f"m{m}_", dims, meta["sort_orders"][m]))
+            if fv is None:
+                fv = leg.factors(hx, [arrays[f"f{d}"] for d in range(N)])
+                leg.keep.append(("fv", fv))
+            leg.add_mttkrp(f"mttkrp_m{m}", meta["sample_nnz"], hx, fv, m)
+        if name == "c5":
+            from oracle.oracle import HostTensor
+            hxt = _host_tensor(arrays, "eq_", dims, meta["eq_sort_order"])
+            hx = leg.coo(hxt)
+            hy = leg.coo(HostTensor(hxt.dims, hxt.indices, np.ascontiguousarray(arrays["eq_yval"]),
+                                    hxt.sort_order, True))
+            leg.add("tew_eq_mul", meta["sample_nnz"],
+                    lambda v, nt: leg._run(leg.lib.ref_tew_eq, hx, hy, 2, v, nt))
+    elif name == "pre":
+        from oracle.oracle import HostTensor
+        t = _host_tensor(arrays, "x_", dims, None)
+        n = meta["sample_nnz"]
+
+        def sort_once(v, nt):
+            leg.ref.sort_lexicographic(HostTensor(t.dims, [a.copy() for a in t.indices],
+                                                  t.values.copy(), None, True), [0, 1, 2])
+        leg.add("sort_lexicographic", n, sort_once)
+    else:
+        raise ValueError(name)
+    return leg
+
+
+def run_cpu_leg(name, arrays, meta, steps, warmup, seq=True) -> dict:
+    """BASELINE.md section 3: par:: with every host thread, both MTTKRP
+    strategies, `warmup` untimed + `steps` timed runs (mean and median), and
+    one seq:: pass on one core."""
+    from oracle.oracle import Ref
+    ref = Ref()
+    nthreads = os.cpu_count() or 1
+    leg = _cpu_leg(name, ref, arrays, meta, nthreads)
+    strategies = leg.calibrate()
+    for _ in range(warmup):
+        leg.step()
+    t = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        leg.step()
+        t.append(time.perf_counter() - t0)
+    units = leg.units()
+    res = {"value": units / statistics.mean(t), "unit": "nnz/s", "cores": nthreads,
+           "kind": "reference", "sample": meta["sample"], "step_s_mean": statistics.mean(t),
+           "step_s_median": statistics.median(t), "value_median": units / statistics.median(t),
+           "protocol": f"{warmup} untimed warm-up + {steps} timed runs, mean (P/src/bench.cpp:"
+                       f"199-209) and median; par:: with nthreads={nthreads}",
+           "mttkrp_strategy": strategies, "host": host_record()}
+    if seq and name != "pre":
+        # seq:: on one core over the same calls (one pass; long calls on a
+        # prefix of the sample when the par:: step is heavy)
+        t0 = time.perf_counter()
+        for nm, _, fn in leg.calls:
+            fn(0, 1) if not nm.startswith("mttkrp") else fn(0, 1, 0)
+        dt = time.perf_counter() - t0
+        res["seq"] = {"value": units / dt, "unit": "nnz/s", "cores": 1,
+                      "note": "spten::seq:: over the same sample, one pass"}
+    return res
+
+
+def save_arrays(d, arrays, meta):
+    os.makedirs(d, exist_ok=True)
+    for k, a in arrays.items():
+        np.save(os.path.join(d, k + ".npy"), a)
+    with open(os.path.join(d, "meta.json"), "w") as fh:
+        json.dump(meta, fh)
+
+
+def load_arrays(d):
+    meta = json.load(open(os.path.join(d, "meta.json")))
+    arrays = {f[:-4]: np.load(os.path.join(d, f)) for f in os.listdir(d) if f.endswith(".npy")}
+    return arrays, meta
+
+
+# ===========================================================================
+# GPU workloads (torch + the C-ABI library)
+
+
+class Op:
+    def __init__(self, name, fn, units, bytes_fn, prep=None):
+        self.name, self.fn, self.units, self.bytes_fn = name, fn, units, bytes_fn
+        self.prep = prep  # untimed setup before each call (e.g. restore an unsorted input)
+        self.times = []
+        self.launches = 0
+
+
+DIST = None  # torch.distributed when running under torchrun with N > 1
+
+
+def allreduce(t):
+    """MTTKRP's exchange for the weak-scaled workloads: every
+    rank holds the dims[n] x R partial of its own instance; NCCL all-reduce."""
+    if DIST is not None:
+        DIST.all_reduce(t, op=DIST.ReduceOp.SUM)
+    return t
+
+
+def _np(t):
+    return t.cpu().numpy()
+
+
+def _idx_np(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _strided(n, k):
+    """Positions of a uniform strided sample of k of n entries (sorted order
+    kept, so a sample of a sorted coalesced tensor is sorted and coalesced)."""
+    s = max(1, n // max(1, k))
+    return slice(0, s * min(k, n), s)
+
+
+class Workload:
+    name = ""
+    STRONG = False
+    preprocess = {}
+
+    def config(self):
+        return {}
 
 
 class C1(Workload):
     """BASELINE configs[0]: MTTKRP mode 0 (R=16) + TS add/mul by 2.5, 1M nnz."""
 
     name = "c1-mttkrp-ts"
+    MTTKRP = "seg"
 
-    def __init__(self, seed, device, scale=1.0):
+    def __init__(self, seed, device, scale=1.0, mttkrp=None):
+        import torch
         from paper_1902_03317_b200 import generate, ops
         from paper_1902_03317_b200.coo import DeviceCOO
         c = generate.CONFIGS["c1"]
         self.dims, self.R = c["dims"], c["R"]
         self.nnz = int(c["nnz"] * scale)
+        self.impl = mttkrp or self.MTTKRP
         self.x = generate.coo(self.dims, self.nnz, seed, c["zipf"], 0.0, 1.0, [0, 1, 2], device)
         self.f = [generate.uniform((d, self.R), seed, 100 + k, 0.0, 1.0, device)
                   for k, d in enumerate(self.dims)]
         self.out = torch.empty((self.dims[0], self.R), dtype=torch.float32, device=f"cuda:{device}")
         self.z = DeviceCOO.empty(self.dims, self.nnz, device)
         n, N, R = self.nnz, 3, self.R
+        if self.impl == "plan":
+            t0 = time.perf_counter()
+            self.plan = ops.mttkrp_plan(self.x, 0, R)
+            self.preprocess = {"mttkrp_m0_plan_s": time.perf_counter() - t0}
+            mt = lambda: ops.mttkrp(self.plan, self.f, 0, out=self.out, sync=False)  # noqa: E731
+        else:
+            mt = lambda: ops.mttkrp(self.x, self.f, 0, ops.MTTKRP_SEGMENTED,  # noqa: E731
+                                    out=self.out, sync=False)
         self.ops = [
-            Op("mttkrp_m0", lambda: allreduce(ops.mttkrp(self.x, self.f, 0, ops.MTTKRP_SEGMENTED,
-                                                         out=self.out, sync=False)),
-               n, lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims)),
+            Op("mttkrp_m0", lambda: allreduce(mt()), n,
+               lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims)),
             Op("ts_add", lambda: ops.ts(self.x, 2.5, ops.SCALAR_ADD, out=self.z, sync=False), n,
                lambda: 2 * tensor_bytes(n, N)),
             Op("ts_mul", lambda: ops.ts(self.x, 2.5, ops.SCALAR_MUL, out=self.z, sync=False), n,
@@ -402,7 +447,16 @@ class C1(Workload):
 
     def config(self):
         return {"workload": self.name, "baseline_config": "configs[0] (C1)", "dims": self.dims,
-                "nnz": self.nnz, "R": self.R, "mttkrp_input": "sorted (0,1,2) (mode-0 leading)"}
+                "nnz": self.nnz, "R": self.R, "mttkrp": self.impl,
+                "mttkrp_input": "sorted (0,1,2) (mode-0 leading)"}
+
+    def cpu_arrays(self):
+        arrays = {f"x_i{d}": _idx_np(self.x.indices[d]) for d in range(3)}
+        arrays["x_val"] = _np(self.x.values)
+        arrays.update({f"f{d}": _np(f) for d, f in enumerate(self.f)})
+        return arrays, {"dims": self.dims, "sort_order": [0, 1, 2], "sample_nnz": self.nnz,
+                        "sample": f"full C1 workload: mttkrp mode 0 (R={self.R}, faster "
+                                  f"strategy) + ts add/mul on {self.nnz} nnz"}
 
     # e2e through the C-ABI with host buffers
     E2E_CHUNKS = 4
@@ -411,9 +465,10 @@ class C1(Workload):
                 "whole tensor, its I x R result and both TS outputs down")
 
     def e2e_host(self, device=0):
+        import torch
         from paper_1902_03317_b200.coo import DeviceCOO
         from paper_1902_03317_b200.staging import PinnedCOO, Pipeline
-        dev = torch.device(device) if not isinstance(device, int) else torch.device("cuda", device)
+        dev = torch.device("cuda", device)
         n = self.nnz
         return {"pipe": Pipeline(dev),
                 "px": PinnedCOO.from_host(self.x.to_host()),
@@ -427,9 +482,10 @@ class C1(Workload):
                 "out_ts": [PinnedCOO(self.dims, n) for _ in range(2)],
                 "out_m": torch.empty((self.dims[0], self.R), dtype=torch.float32).pin_memory()}
 
-    def e2e_step(self, host, device):
+    def e2e_step(self, host):
         """Pinned host inputs -> MTTKRP + TS add/mul -> pinned host outputs.
         Returns (h2d, d2h) bytes."""
+        import torch
         from paper_1902_03317_b200 import ops
         from paper_1902_03317_b200.staging import Pipeline, chunk_bounds, view
         pl, px, dx = host["pipe"], host["px"], host["dx"]
@@ -460,27 +516,125 @@ class C1(Workload):
         pl.end()
         return h2d, d2h
 
-    def cpu_setup(self, ref, sample_nnz=None):
-        c = self.cr = _RefCalls(ref)
-        self.hx = c.coo(_host_sample(self.x, self.nnz))
-        self.fv = c.factors(self.hx, [f.cpu().numpy() for f in self.f])
-        self.cpu_units = 3 * self.nnz
-        return f"full C1 workload: mttkrp mode 0 (privatize) + ts add/mul on {self.nnz} nnz, par::"
 
-    def cpu_step(self, ref, nthreads):
-        c = self.cr
-        c.mttkrp(self.hx, self.fv, 0, nthreads)
-        for op in (0, 1):
-            c.run(c.lib.ref_ts, self.hx, 2.5, op, 1, nthreads)
-        return self.cpu_units
+class C2(Workload):
+    """BASELINE configs[1]: TEW-eq x4 (shared pattern) + TEW add/mul (independent)."""
+
+    name = "c2-tew_eq-tew"
+
+    def __init__(self, seed, device, scale=1.0, mttkrp=None):
+        import torch
+        from paper_1902_03317_b200 import generate, ops
+        from paper_1902_03317_b200.coo import DeviceCOO
+        c = generate.CONFIGS["c2"]
+        self.dims = c["dims"]
+        self.nnz = int(c["nnz"] * scale)
+        self.x = generate.coo(self.dims, self.nnz, seed, c["zipf"], 0.5, 1.5, [0, 1, 2], device)
+        self.y = DeviceCOO(list(self.dims), [i.clone() for i in self.x.indices],
+                           generate.uniform(self.nnz, seed, 77, 0.5, 1.5, device), [0, 1, 2],
+                           True)
+        self.y2 = generate.coo(self.dims, self.nnz, seed + 7919, c["zipf"], 0.5, 1.5, [0, 1, 2],
+                               device)
+        self.z = DeviceCOO.empty(self.dims, self.nnz, device)
+        self.zu = DeviceCOO.empty(self.dims, 2 * self.nnz, device)
+        self.cnt = torch.zeros(2, dtype=torch.int64, device=f"cuda:{device}")
+        nz_add = ops.tew(self.x, self.y2, ops.ADD).nnz
+        nz_mul = ops.tew(self.x, self.y2, ops.MUL).nnz
+        self.nz = {"add": nz_add, "mul": nz_mul}
+        n, N = self.nnz, 3
+        self.ops = []
+        for opn, op in (("add", ops.ADD), ("sub", ops.SUB), ("mul", ops.MUL), ("div", ops.DIV)):
+            self.ops.append(Op(f"tew_eq_{opn}",
+                               (lambda op=op: ops.tew_eq(self.x, self.y, op, out=self.z,
+                                                         sync=False)),
+                               n, lambda: 3 * tensor_bytes(n, N)))
+        for opn, op, k in (("add", ops.ADD, 0), ("mul", ops.MUL, 1)):
+            nz = self.nz[opn]
+            self.ops.append(Op(f"tew_{opn}",
+                               (lambda op=op, k=k: ops.tew_device(self.x, self.y2, op, self.zu,
+                                                                  self.cnt[k:k + 1])),
+                               2 * n, (lambda nz=nz: tensor_bytes(2 * n + nz, N))))
+
+    def config(self):
+        return {"workload": self.name, "baseline_config": "configs[1] (C2)", "dims": self.dims,
+                "nnz": self.nnz, "order": 3, "values": "U[0.5,1.5)",
+                "pattern": "uniform distinct tuples, sorted (0,1,2)",
+                "tew_second_pattern_nnz": self.nnz, "tew_union": self.nz["add"],
+                "tew_intersection": self.nz["mul"]}
+
+    def cpu_arrays(self):
+        arrays = {f"x_i{d}": _idx_np(self.x.indices[d]) for d in range(3)}
+        arrays["x_val"] = _np(self.x.values)
+        arrays["yval"] = _np(self.y.values)
+        arrays.update({f"y2_i{d}": _idx_np(self.y2.indices[d]) for d in range(3)})
+        arrays["y2_val"] = _np(self.y2.values)
+        return arrays, {"dims": self.dims, "sort_order": [0, 1, 2], "sample_nnz": self.nnz,
+                        "sample": f"full C2 workload (4 x tew_eq on {self.nnz} nnz + tew "
+                                  f"add/mul on {self.nnz} + {self.nnz} nnz)"}
+
+    E2E_CHUNKS = 8
+    E2E_PATH = ("ops.* -> C-ABI; pinned host buffers; H2D / kernels / D2H overlapped on three "
+                "streams (staging.Pipeline), x/y uploaded in 8 chunks")
+
+    def e2e_host(self, device=0):
+        import torch
+        from paper_1902_03317_b200.coo import DeviceCOO
+        from paper_1902_03317_b200.staging import PinnedCOO, Pipeline
+        dev = torch.device("cuda", device)
+        n = self.nnz
+        return {"pipe": Pipeline(dev),
+                "pinned": [PinnedCOO.from_host(h) for h in (self.x.to_host(), self.y.to_host(),
+                                                            self.y2.to_host())],
+                "dev": [DeviceCOO(list(self.dims), [torch.empty(n, dtype=torch.int32, device=dev)
+                                                    for _ in self.dims],
+                                  torch.empty(n, dtype=torch.float32, device=dev), [0, 1, 2],
+                                  True) for _ in range(3)],
+                "dz": [DeviceCOO.empty(self.dims, n, dev) for _ in range(4)],
+                "dzu": [DeviceCOO.empty(self.dims, 2 * n, dev),
+                        DeviceCOO.empty(self.dims, n, dev)],
+                "out_eq": [PinnedCOO(self.dims, n) for _ in range(4)],
+                "out_tew": [PinnedCOO(self.dims, 2 * n), PinnedCOO(self.dims, n)]}
+
+    def e2e_step(self, host):
+        import torch
+        from paper_1902_03317_b200 import ops
+        from paper_1902_03317_b200.staging import Pipeline, chunk_bounds, view
+        pl = host["pipe"]
+        (px, py, py2), (dx, dy, dy2) = host["pinned"], host["dev"]
+        h2d = d2h = 0
+        pl.begin()
+        b = chunk_bounds(self.nnz, self.E2E_CHUNKS)
+        ev_in = []
+        for lo, hi in zip(b[:-1], b[1:]):
+            h2d += px.upload(dx, lo, hi, pl.h2d) + py.upload(dy, lo, hi, pl.h2d)
+            ev_in.append(Pipeline.mark(pl.h2d))
+        h2d += py2.upload(dy2, 0, self.nnz, pl.h2d)
+        ev_y2 = Pipeline.mark(pl.h2d)
+        with torch.cuda.stream(pl.cmp):
+            for c, (lo, hi) in enumerate(zip(b[:-1], b[1:])):
+                pl.cmp.wait_event(ev_in[c])
+                for k, op in enumerate((ops.ADD, ops.SUB, ops.MUL, ops.DIV)):
+                    z = ops.tew_eq(view(dx, lo, hi), view(dy, lo, hi), op,
+                                   out=view(host["dz"][k], lo, hi), sync=False)
+                    pl.d2h.wait_event(Pipeline.mark(pl.cmp))
+                    d2h += host["out_eq"][k].download(z, pl.d2h, at=lo)
+            pl.cmp.wait_event(ev_y2)
+            for k, op in enumerate((ops.ADD, ops.MUL)):
+                zu = host["dzu"][k]
+                z = ops.tew(dx, dy2, op, out=view(zu, 0, zu.nnz))
+                pl.d2h.wait_event(Pipeline.mark(pl.cmp))
+                d2h += host["out_tew"][k].download(z, pl.d2h)
+        pl.end()
+        return h2d, d2h
 
 
 class C3(Workload):
     """configs[2]: TTV and TTM (R=16) along every mode, 50M nnz, mode-0 Zipf(1.1)."""
 
     name = "c3-ttv-ttm"
+    CPU_SAMPLE = 2_000_000
 
-    def __init__(self, seed, device, scale=1.0):
+    def __init__(self, seed, device, scale=1.0, mttkrp=None):
         from paper_1902_03317_b200 import generate, ops
         from paper_1902_03317_b200.coo import DeviceCOO
         c = generate.CONFIGS["c3"]
@@ -527,202 +681,327 @@ class C3(Workload):
                 "nnz": self.nnz, "R": self.R, "nfibs": [f.nfibs for f in self.fib],
                 "mode0": "Zipf(1.1) over a seeded id permutation; modes 1,2 uniform"}
 
-    def cpu_setup(self, ref, sample_nnz=1_000_000):
-        c = self.cr = _RefCalls(ref)
-        self.cpu_in = []
-        k = min(sample_nnz, self.nnz)
+    def cpu_arrays(self):
+        # the first k entries of each mode-last sorted copy: whole fibers but
+        # the last
+        k = min(self.CPU_SAMPLE, self.nnz)
+        arrays = {}
         for m in range(3):
-            hx = c.coo(_host_sample(self.xs[m], k))
-            fib = ref.lib.ref_fiber_new(hx, m)  # preprocessing, untimed (P/src/bench.cpp:363-368)
-            c.keep.append(("fib", fib))
-            self.cpu_in.append((hx, fib, c.vector(self.v[m].cpu().numpy()),
-                                c.matrix(self.u[m].cpu().numpy())))
-        self.cpu_units = 6 * k
-        return f"ttv + ttm (R={self.R}) along every mode on the first {k} entries of each " \
-               "mode-last sorted copy, par::"
-
-    def cpu_step(self, ref, nthreads):
-        c = self.cr
-        for m, (hx, fib, hv, hu) in enumerate(self.cpu_in):
-            c.run(c.lib.ref_ttv_fib, hx, hv, m, fib, 1, nthreads)
-            c.run(c.lib.ref_ttm_fib, hx, hu, m, fib, 1, nthreads)
-        return self.cpu_units
+            for d in range(3):
+                arrays[f"m{m}_i{d}"] = _idx_np(self.xs[m].indices[d][:k])
+            arrays[f"m{m}_val"] = _np(self.xs[m].values[:k])
+            arrays[f"v{m}"] = _np(self.v[m])
+            arrays[f"u{m}"] = _np(self.u[m])
+        return arrays, {"dims": self.dims, "sample_nnz": k,
+                        "sort_orders": [list(x.sort_order) for x in self.xs],
+                        "sample": f"ttv + ttm (R={self.R}) along every mode on the first {k} "
+                                  "entries of each mode-last sorted copy"}
 
 
 class C4(Workload):
     """configs[3]: MTTKRP every mode, R=32, 4th order, 100M nnz, Zipf(1.2) modes."""
 
     name = "c4-mttkrp"
+    MTTKRP = "seg"
+    CPU_SAMPLE = 4_000_000
 
-    def __init__(self, seed, device, scale=1.0):
+    def __init__(self, seed, device, scale=1.0, mttkrp=None):
+        import torch
         from paper_1902_03317_b200 import generate, ops
         c = generate.CONFIGS["c4"]
         self.dims, self.R = c["dims"], c["R"]
         self.nnz = int(c["nnz"] * scale)
+        self.impl = mttkrp or self.MTTKRP
         base = generate.coo(self.dims, self.nnz, seed, c["zipf"], 0.0, 1.0, None, device)
         self.f = [generate.uniform((d, self.R), seed, 100 + k, 0.0, 1.0, device)
                   for k, d in enumerate(self.dims)]
-        self.xs = []
+        idx = torch.arange(0, self.nnz, max(1, self.nnz // self.CPU_SAMPLE),
+                           device=base.values.device)[: self.CPU_SAMPLE]
+        from paper_1902_03317_b200.coo import DeviceCOO
+        self.sample = DeviceCOO(list(self.dims), [i[idx] for i in base.indices], base.values[idx],
+                                None, True)
+        self.xs, self.plans, self.preprocess = [], [], {}
         for mode in range(4):
-            xs = base.clone()
-            ops.sort_lexicographic(xs, [mode] + [d for d in range(4) if d != mode])
-            self.xs.append(xs)
+            if self.impl == "plan":
+                t0 = time.perf_counter()
+                self.plans.append(ops.mttkrp_plan(base, mode, self.R))
+                self.preprocess[f"mttkrp_m{mode}_plan_s"] = time.perf_counter() - t0
+            else:
+                xs = base.clone()
+                ops.sort_lexicographic(xs, [mode] + [d for d in range(4) if d != mode])
+                self.xs.append(xs)
         del base
         self.out = [torch.empty((d, self.R), dtype=torch.float32, device=f"cuda:{device}")
                     for d in self.dims]
         n, N, R = self.nnz, 4, self.R
+        src = self.plans if self.impl == "plan" else self.xs
+        strat = {} if self.impl == "plan" else {"strategy": ops.MTTKRP_SEGMENTED}
         self.ops = [Op(f"mttkrp_m{m}",
-                       lambda m=m: allreduce(ops.mttkrp(self.xs[m], self.f, m,
-                                                        ops.MTTKRP_SEGMENTED, out=self.out[m],
-                                                        sync=False)),
+                       lambda m=m: allreduce(ops.mttkrp(src[m], self.f, m, out=self.out[m],
+                                                        sync=False, **strat)),
                        n, lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims))
                     for m in range(4)]
 
     def config(self):
         return {"workload": self.name, "baseline_config": "configs[3] (C4)", "dims": self.dims,
                 "nnz": self.nnz, "R": self.R, "dist": "every mode Zipf(1.2), shuffled ids",
-                "mttkrp_input": "one mode-leading sorted copy per mode (preprocessing)"}
+                "mttkrp": self.impl,
+                "mttkrp_input": ("one plan per mode (preprocessing)" if self.impl == "plan" else
+                                 "one mode-leading sorted copy per mode (preprocessing)")}
 
-    def cpu_setup(self, ref, sample_nnz=1_000_000):
-        c = self.cr = _RefCalls(ref)
-        k = min(sample_nnz, self.nnz)
-        self.cpu_in = []
-        for m in range(4):
-            self.cpu_in.append((c.coo(_host_sample(self.xs[m], k)), None))
-        fv = c.factors(self.cpu_in[0][0], [f.cpu().numpy() for f in self.f])
-        self.cpu_in = [(hx, fv) for hx, _ in self.cpu_in]
-        self.cpu_units = 4 * k
-        return f"mttkrp (R={self.R}, privatize) along every mode on the first {k} entries of " \
-               "each mode-leading sorted copy (full-size factors), par::"
+    def cpu_arrays(self):
+        from paper_1902_03317_b200 import ops
+        return _mode_sorted_sample_arrays(self, ops, 4)
 
-    def cpu_step(self, ref, nthreads):
-        for m, (hx, fv) in enumerate(self.cpu_in):
-            self.cr.mttkrp(hx, fv, m, nthreads)
-        return self.cpu_units
+
+def _mode_sorted_sample_arrays(wl, ops, N):
+    """Uniform strided sample of the tensor (wl.sample, taken on the device),
+    sorted with each mode leading (the order the GPU kernels get), plus the
+    full factors."""
+    arrays, orders = {}, []
+    for m in range(N):
+        s = wl.sample.clone()
+        order = [m] + [d for d in range(N) if d != m]
+        ops.sort_lexicographic(s, order)
+        orders.append(order)
+        for d in range(N):
+            arrays[f"m{m}_i{d}"] = _idx_np(s.indices[d])
+        arrays[f"m{m}_val"] = _np(s.values)
+        del s
+    arrays.update({f"f{d}": _np(f) for d, f in enumerate(wl.f)})
+    k = wl.sample.nnz
+    return arrays, {"dims": wl.dims, "sample_nnz": k, "sort_orders": orders,
+                    "sample": f"mttkrp (R={wl.R}, faster strategy per mode) along every mode "
+                              f"on a uniform strided sample of {k} of the {wl.nnz} entries, "
+                              "sorted with the mode leading, full-size factors"}
 
 
 class C5(Workload):
     """BASELINE configs[4] (C5): MTTKRP modes 0-2 (R=32) + TEW-eq mul on a
     1B-nnz order-3 tensor, every mode Zipf(1.1). One GPU holds the tensor
-    (16 GB), one mode-leading copy per mode and the TEW-eq operand/output;
-    under torchrun every rank runs its own instance and MTTKRP adds the NCCL
-    all-reduce of the I_n x R partials."""
+    (16 GB), one MTTKRP plan per mode (16 GB each) and the TEW-eq operand and
+    output. Under torchrun the tensor is sharded (strong scaling)."""
 
     name = "c5-mttkrp-tew_eq"
-    # BASELINE configs[4] shards ONE 1B-nnz tensor over the GPUs: every rank
-    # builds the same tensor (same seed) and keeps its shards
     STRONG = True
+    MTTKRP = "plan"
+    CPU_SAMPLE = 16_000_000
 
-    def __init__(self, seed, device, scale=1.0):
+    def __init__(self, seed, device, scale=1.0, mttkrp=None):
+        import torch
         from paper_1902_03317_b200 import generate, ops
         from paper_1902_03317_b200.coo import DeviceCOO
         c = generate.CONFIGS["c5"]
         self.dims, self.R = c["dims"], c["R"]
         self.nnz = int(c["nnz"] * scale)
+        self.impl = mttkrp or self.MTTKRP
+        self.seed, self.device = seed, device
         dev = f"cuda:{device}"
-        base = generate.coo(self.dims, self.nnz, seed, c["zipf"], 0.0, 1.0, None, device)
+        x = generate.coo(self.dims, self.nnz, seed, c["zipf"], 0.0, 1.0, [0, 1, 2], device)
         self.f = [generate.uniform((d, self.R), seed, 100 + k, 0.0, 1.0, device)
                   for k, d in enumerate(self.dims)]
-        self.xs = []
-        for mode in range(3):
-            xs = base if mode == 2 else base.clone()
-            ops.sort_lexicographic(xs, [mode] + [d for d in range(3) if d != mode])
-            self.xs.append(xs)
-        del base
-        torch.cuda.empty_cache()
-        x = self.xs[0]
         # TEW-eq operand: same pattern in its own buffers (as SURVEY 8(d) counts
         # the bytes), values U[0.5,1.5)
         self.y = DeviceCOO(list(self.dims), [i.clone() for i in x.indices],
-                           generate.uniform(self.nnz, seed, 77, 0.5, 1.5, device),
-                           list(x.sort_order), x.coalesced)
+                           generate.uniform(self.nnz, seed, 77, 0.5, 1.5, device), [0, 1, 2], True)
+        sl = _strided(self.nnz, self.CPU_SAMPLE)
+        self.sample = DeviceCOO(list(self.dims), [i[sl].clone() for i in x.indices],
+                                x.values[sl].clone(), [0, 1, 2], True)
+        self.sample_y = self.y.values[sl].clone()
         self.out = [torch.empty((d, self.R), dtype=torch.float32, device=dev) for d in self.dims]
         n, N, R = self.nnz, 3, self.R
         world = DIST.get_world_size() if DIST is not None else 1
+        me = DIST.get_rank() if DIST is not None else 0
+        self.preprocess = {}
+        self.x = x
         if world == 1:
+            src = self._mttkrp_inputs(x, None)
             self.z = DeviceCOO.empty(self.dims, self.nnz, device)
-            self.ops = [Op(f"mttkrp_m{m}",
-                           lambda m=m: ops.mttkrp(self.xs[m], self.f, m, ops.MTTKRP_SEGMENTED,
-                                                  out=self.out[m], sync=False),
-                           n, lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims))
+            self.ops = [Op(f"mttkrp_m{m}", lambda m=m: self._mttkrp(src[m], m), n,
+                           lambda: tensor_bytes(n, N) + 4 * R * sum(self.dims))
                         for m in range(3)]
             self.ops.append(Op("tew_eq_mul",
-                               lambda: ops.tew_eq(x, self.y, ops.MUL, out=self.z, sync=False),
+                               lambda: ops.tew_eq(self.x, self.y, ops.MUL, out=self.z, sync=False),
                                n, lambda: 3 * tensor_bytes(n, N)))
             return
         # N > 1 (SURVEY 8(e)): MTTKRP on row-aligned nnz shards of each
-        # mode-leading copy, the owned row blocks all-gathered over NCCL (half
+        # mode-leading order, the owned row blocks all-gathered over NCCL (half
         # the all-reduce's volume); TEW-eq on contiguous nnz shards, no exchange.
         # Units per rank = nnz / world, so `value` is the whole tensor's nnz/s.
         from paper_1902_03317_b200 import parallel
-        me = DIST.get_rank()
         self.blocks = []
-        # shards are cloned into their own (16-byte aligned) buffers, so the
-        # kernels keep their vector paths, and the full copies are released
         lo, hi = parallel.shard_range(self.nnz, world, me)
         xe = parallel.slice_coo(x, lo, hi).clone()
-        self.y = parallel.slice_coo(self.y, lo, hi).clone()
-        del x
+        self.ye = parallel.slice_coo(self.y, lo, hi).clone()
+        del self.y
+        shards = []
         for m in range(3):
-            rr = parallel.row_aligned_ranges(self.xs[m].indices[m], world)
-            self.blocks.append(parallel.row_blocks(self.xs[m].indices[m], rr, self.dims[m]))
-            self.xs[m] = parallel.slice_coo(self.xs[m], *rr[me]).clone()
+            xs = x.clone()
+            if m:
+                ops.sort_lexicographic(xs, [m] + [d for d in range(3) if d != m])
+            rr = parallel.row_aligned_ranges(xs.indices[m], world)
+            self.blocks.append(parallel.row_blocks(xs.indices[m], rr, self.dims[m]))
+            shards.append(parallel.slice_coo(xs, *rr[me]).clone())
+            del xs
             torch.cuda.empty_cache()
+        del x
+        self.x = xe
+        src = self._mttkrp_inputs(None, shards)
+        del shards
+        torch.cuda.empty_cache()
         self.z = DeviceCOO.empty(self.dims, hi - lo, device)
         share = n / world
 
         def mt(m):
-            part = lambda s, f, mm: ops.mttkrp(s, f, mm, ops.MTTKRP_SEGMENTED, out=self.out[mm],
-                                               sync=False)
-            return parallel.mttkrp_row_allgather(self.xs[m], self.f, m, self.dims[m], R,
+            part = lambda s, f, mm: self._mttkrp(s, mm)  # noqa: E731
+            return parallel.mttkrp_row_allgather(src[m], self.f, m, self.dims[m], R,
                                                  self.blocks[m], part)
         self.ops = [Op(f"mttkrp_m{m}", lambda m=m: mt(m), share,
                        lambda: (tensor_bytes(n, N) + 4 * R * sum(self.dims)) / world)
                     for m in range(3)]
         self.ops.append(Op("tew_eq_mul",
-                           lambda: ops.tew_eq(xe, self.y, ops.MUL, out=self.z, sync=False),
+                           lambda: ops.tew_eq(self.x, self.ye, ops.MUL, out=self.z, sync=False),
                            share, lambda: 3 * tensor_bytes(n, N) / world))
+
+    def _mttkrp_inputs(self, x, shards):
+        """Plans (or mode-leading sorted copies for --mttkrp seg) per mode;
+        building them is preprocessing, timed apart."""
+        import torch
+        from paper_1902_03317_b200 import ops
+        src = []
+        for m in range(3):
+            t = x if shards is None else shards[m]
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if self.impl == "plan":
+                src.append(ops.mttkrp_plan(t, m, self.R))
+            else:
+                xs = t.clone() if shards is None else t
+                if shards is None or m:
+                    ops.sort_lexicographic(xs, [m] + [d for d in range(3) if d != m])
+                src.append(xs)
+            torch.cuda.synchronize()
+            self.preprocess[f"mttkrp_m{m}_{'plan' if self.impl == 'plan' else 'sort'}_s"] = \
+                round(time.perf_counter() - t0, 4)
+        return src
+
+    def _mttkrp(self, src, m):
+        from paper_1902_03317_b200 import ops
+        if self.impl == "plan":
+            return ops.mttkrp(src, self.f, m, out=self.out[m], sync=False)
+        return ops.mttkrp(src, self.f, m, ops.MTTKRP_SEGMENTED, out=self.out[m], sync=False)
 
     def config(self):
         return {"workload": self.name, "baseline_config": "configs[4] (C5)", "dims": self.dims,
                 "nnz": self.nnz, "R": self.R, "dist": "every mode Zipf(1.1), shuffled ids",
-                "mttkrp_input": "one mode-leading sorted copy per mode (preprocessing)",
+                "mttkrp": self.impl,
+                "mttkrp_input": ("one plan per mode (mode-leading blocked copy + hot rows; "
+                                 "preprocessing)" if self.impl == "plan" else
+                                 "one mode-leading sorted copy per mode (preprocessing)"),
                 "tew_eq": "mul against the same pattern, y U[0.5,1.5)"}
 
-    def cpu_setup(self, ref, sample_nnz=1_000_000):
-        c = self.cr = _RefCalls(ref)
-        k = min(sample_nnz, self.nnz)
-        self.cpu_in = []
-        for m in range(3):
-            self.cpu_in.append((c.coo(_host_sample(self.xs[m], k)), None))
-        fv = c.factors(self.cpu_in[0][0], [f.cpu().numpy() for f in self.f])
-        self.cpu_in = [(hx, fv) for hx, _ in self.cpu_in]
-        from oracle.oracle import HostTensor
-        hx0 = _host_sample(self.xs[0], k)
-        hy = HostTensor(hx0.dims, hx0.indices, self.y.values[:k].cpu().numpy(), hx0.sort_order,
-                        hx0.coalesced)
-        self.eq = (c.coo(hx0), c.coo(hy))
-        self.cpu_units = 4 * k
-        return f"mttkrp (R={self.R}, privatize) modes 0-2 on the first {k} entries of each " \
-               f"mode-leading copy (full 10M-row factors) + tew_eq mul on {k} entries, par::"
+    def cpu_arrays(self):
+        from paper_1902_03317_b200 import ops
+        arrays, meta = _mode_sorted_sample_arrays(self, ops, 3)
+        for d in range(3):
+            arrays[f"eq_i{d}"] = _idx_np(self.sample.indices[d])
+        arrays["eq_val"] = _np(self.sample.values)
+        arrays["eq_yval"] = _np(self.sample_y)
+        meta["eq_sort_order"] = [0, 1, 2]
+        meta["sample"] += f" + tew_eq mul on the same {meta['sample_nnz']} entries"
+        return arrays, meta
 
-    def cpu_step(self, ref, nthreads):
-        c = self.cr
-        for m, (hx, fv) in enumerate(self.cpu_in):
-            c.mttkrp(hx, fv, m, nthreads)
-        c.run(c.lib.ref_tew_eq, self.eq[0], self.eq[1], 2, 1, nthreads)
-        return self.cpu_units
+    # e2e through the public API from host buffers (the full workload)
+    E2E_PATH = ("ops.* -> C-ABI from pinned host buffers, every step: x (mode-0 sorted, 16 GB), "
+                "y and the three factors uploaded; per mode an MTTKRP plan built (sort + hot "
+                "rows, the preprocessing a host caller pays) and executed, its I x R result "
+                "downloaded while the next plan builds; TEW-eq mul and its full output "
+                "(indices + values) downloaded")
+
+    def e2e_release(self):
+        """Free the device-timed state (e2e needs the memory)."""
+        import torch
+        for k in ("x", "y", "z", "ye", "sample", "sample_y", "ops", "out"):
+            if hasattr(self, k):
+                delattr(self, k)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+    def e2e_host(self, device=0):
+        import torch
+        from paper_1902_03317_b200 import generate
+        from paper_1902_03317_b200.coo import DeviceCOO
+        from paper_1902_03317_b200.staging import PinnedCOO, Pipeline
+        dev = torch.device("cuda", device)
+        n = self.nnz
+        hx = self.x.to_host()
+        hy = self.y.to_host()
+        hf = [f.cpu().pin_memory() for f in self.f]
+        self.e2e_release()
+        host = {"pipe": Pipeline(dev), "px": PinnedCOO.from_host(hx), "py": PinnedCOO.from_host(hy),
+                "pf": hf}
+        del hx, hy
+        host["dx"] = DeviceCOO(list(self.dims), [torch.empty(n, dtype=torch.int32, device=dev)
+                                                 for _ in self.dims],
+                               torch.empty(n, dtype=torch.float32, device=dev), [0, 1, 2], True)
+        host["dy"] = DeviceCOO(list(self.dims), [torch.empty(n, dtype=torch.int32, device=dev)
+                                                 for _ in self.dims],
+                               torch.empty(n, dtype=torch.float32, device=dev), [0, 1, 2], True)
+        host["df"] = [torch.empty(tuple(f.shape), dtype=torch.float32, device=dev) for f in hf]
+        host["dz"] = DeviceCOO.empty(self.dims, n, dev)
+        host["dout"] = [torch.empty((d, self.R), dtype=torch.float32, device=dev)
+                        for d in self.dims]
+        host["out_m"] = [torch.empty((d, self.R), dtype=torch.float32).pin_memory()
+                         for d in self.dims]
+        host["out_eq"] = PinnedCOO(self.dims, n)
+        return host
+
+    def e2e_step(self, host):
+        import torch
+        from paper_1902_03317_b200 import ops
+        from paper_1902_03317_b200.staging import Pipeline, chunk_bounds
+        pl = host["pipe"]
+        h2d = d2h = 0
+        pl.begin()
+        with torch.cuda.stream(pl.h2d):
+            for a, b in zip(host["df"], host["pf"]):
+                a.copy_(b, non_blocking=True)
+                h2d += b.numel() * 4
+        b = chunk_bounds(self.nnz, 8)
+        for lo, hi in zip(b[:-1], b[1:]):
+            h2d += host["px"].upload(host["dx"], lo, hi, pl.h2d)
+        ev_x = Pipeline.mark(pl.h2d)
+        for lo, hi in zip(b[:-1], b[1:]):
+            h2d += host["py"].upload(host["dy"], lo, hi, pl.h2d)
+        ev_y = Pipeline.mark(pl.h2d)
+        with torch.cuda.stream(pl.cmp):
+            pl.cmp.wait_event(ev_x)
+            for m in range(3):
+                plan = ops.mttkrp_plan(host["dx"], m, self.R)
+                ops.mttkrp(plan, host["df"], m, out=host["dout"][m], sync=False)
+                pl.d2h.wait_event(Pipeline.mark(pl.cmp))
+                with torch.cuda.stream(pl.d2h):
+                    host["out_m"][m].copy_(host["dout"][m], non_blocking=True)
+                d2h += host["out_m"][m].numel() * 4
+                torch.cuda.current_stream().synchronize()
+                plan.close()
+            pl.cmp.wait_event(ev_y)
+            z = ops.tew_eq(host["dx"], host["dy"], ops.MUL, out=host["dz"], sync=False)
+            pl.d2h.wait_event(Pipeline.mark(pl.cmp))
+            d2h += host["out_eq"].download(z, pl.d2h)
+        pl.end()
+        return h2d, d2h
 
 
 class Pre(Workload):
     """SURVEY 8(f) "next" row 1: GPU preprocessing at parity and speed --
-    sort_lexicographic (P/src/tensor.cpp:54-64; 4.56 s for 10M on the
-    reference here) and build_fiber_index (:92-120), on C2's 10M tensor in
-    draw (unsorted) order and C3's order for the fiber index."""
+    sort_lexicographic (P/src/tensor.cpp:54-64) and build_fiber_index
+    (:92-120), on C2's 10M tensor in draw (unsorted) order."""
 
     name = "pre-sort-fiber"
+    CPU_SAMPLE = 2_000_000
 
-    def __init__(self, seed, device, scale=1.0):
+    def __init__(self, seed, device, scale=1.0, mttkrp=None):
         from paper_1902_03317_b200 import generate, ops
         c = generate.CONFIGS["c2"]
         self.dims = c["dims"]
@@ -754,70 +1033,108 @@ class Pre(Workload):
                 "fiber_index": "mode 2 on the (0,1,2)-sorted tensor",
                 "note": "preprocessing, timed separately like the reference's sort_s"}
 
-    def cpu_setup(self, ref, sample_nnz=2_000_000):
-        from oracle.oracle import HostTensor
-        h = self.src.to_host()
-        k = min(sample_nnz, self.nnz)
-        self.cpu_t = HostTensor(h.dims, [a[:k] for a in h.indices], h.values[:k], None, True)
-        self.cpu_units = k
-        return f"sort_lexicographic (0,1,2) of the first {k} entries (reference, serial)"
-
-    def cpu_step(self, ref, nthreads):
-        ref.sort_lexicographic(self.cpu_t, [0, 1, 2])
-        return self.cpu_units
+    def cpu_arrays(self):
+        k = min(self.CPU_SAMPLE, self.nnz)
+        arrays = {f"x_i{d}": _idx_np(self.src.indices[d][:k]) for d in range(3)}
+        arrays["x_val"] = _np(self.src.values[:k])
+        return arrays, {"dims": self.dims, "sample_nnz": k,
+                        "sample": f"sort_lexicographic (0,1,2) of the first {k} entries "
+                                  "(the reference's sort is serial)"}
 
 
 WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c5": C5, "pre": Pre}
 
 
-# ---------------------------------------------------------------------------
+def report_rows(wl, ops_list):
+    """Reference-schema rows (variant "gpu") for --report; flops are the
+    sequential reference's counts (P/src/kernels_seq.cpp:37,51,65,99,144,172)."""
+    from paper_1902_03317_b200 import report
+    rows = []
+    N = len(wl.dims)
+    R = getattr(wl, "R", 0)
+    pre = getattr(wl, "preprocess", {}) or {}
+    for op in ops_list:
+        name = op.name
+        mode = opn = None
+        if name.startswith("tew_eq"):
+            kernel, opn = "tew_eq", name.split("_")[-1]
+            fl = wl.nnz
+        elif name.startswith("tew_"):
+            kernel, opn = "tew", name.split("_")[1]
+            nz = wl.nz[opn]
+            fl = 2 * wl.nnz - nz if opn == "add" else nz
+        elif name.startswith("ts_"):
+            kernel, opn, fl = "ts", name.split("_")[1], wl.nnz
+        elif name.startswith(("ttv", "ttm", "mttkrp")):
+            kernel, _, mode = name.partition("_m")
+            fl = {"ttv": 2 * wl.nnz, "ttm": 2 * R * wl.nnz, "mttkrp": N * R * wl.nnz}[kernel]
+        else:
+            kernel, fl = name, 0
+        sort_s = sum(v for k, v in pre.items() if k.startswith(f"{name}_"))
+        rows.append(report.bench_report(wl.name, wl.dims, wl.nnz, kernel,
+                                        [t / 1e3 for t in op.times], fl, op=opn, mode=mode,
+                                        rank=R if kernel in ("ttm", "mttkrp") else 0,
+                                        sort_s=sort_s, preprocess_s=sort_s,
+                                        crosscheck=getattr(wl, "crosscheck", {}).get(name)))
+    return rows
 
 
-def run_cpu_reference(wl, steps, warmup, sample_note=True):
-    from oracle.oracle import Ref
-    ref = Ref()
-    nthreads = os.cpu_count() or 1
-    os.environ.setdefault("OMP_PROC_BIND", "close")
-    sample = wl.cpu_setup(ref)
-    for _ in range(warmup):
-        wl.cpu_step(ref, nthreads)
-    t = []
-    units = 0
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        units = wl.cpu_step(ref, nthreads)
-        t.append(time.perf_counter() - t0)
-    return {"value": units / statistics.mean(t), "unit": "nnz/s", "cores": nthreads,
-            "kind": "reference", "sample": sample, "step_s_mean": statistics.mean(t),
-            "step_s_median": statistics.median(t),
-            "protocol": f"{warmup} untimed warm-up + {steps} timed (mean), as P/src/bench.cpp:199-209"}
+# ===========================================================================
+# entry points
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--seed", type=int, default=20190210)
-    ap.add_argument("--scale", type=float, default=1.0, help="nnz scale (testing only)")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--report", default=None,
-                    help="also write per-op rows in the reference's BenchReport schema "
-                         "(.json or .csv, P/include/spten/report.hpp)")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+def prep_cpu_inputs(args):
+    """Separate process: build the workload on the GPU and write the CPU leg's
+    host arrays (numpy files) for --impl reference."""
+    import torch
+    torch.cuda.set_device(0)
+    W = WORKLOADS[args.workload]
+    wl = W(args.seed, 0, args.scale, getattr(args, "mttkrp", None))
+    arrays, meta = wl.cpu_arrays()
+    meta["config"] = wl.config()  # the reference arm reports the same config
+    save_arrays(args.prep_cpu, arrays, meta)
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference" and rank != 0:
+
+def main_reference(args, world, rank):
+    """The reference's own CPU path on this host, on the workload's bounded
+    sample; inputs from a separate prep process (no repo library loaded here)."""
+    if rank != 0:
         return  # the reference arm runs on rank 0 only (CPU path)
+    base = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    d = tempfile.mkdtemp(prefix="spt_ref_inputs_", dir=base)
+    try:
+        env = dict(os.environ)
+        for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "LOCAL_WORLD_SIZE", "GROUP_RANK",
+                  "ROLE_RANK", "TORCHELASTIC_RUN_ID"):
+            env.pop(k, None)
+        cmd = [sys.executable, os.path.abspath(__file__), "--prep-cpu", d, "--workload",
+               args.workload, "--seed", str(args.seed), "--scale", str(args.scale)]
+        subprocess.run(cmd, check=True, env=env)
+        arrays, meta = load_arrays(d)
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    cb = run_cpu_leg(args.workload, arrays, meta, args.steps, args.warmup)
+    cfg = meta["config"]
+    line = {"metric": METRIC, "value": cb["value"], "unit": "nnz/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["step_s_mean"] * 1e3,
+            "higher_is_better": True,
+            "scaling": "strong" if WORKLOADS[args.workload].STRONG else "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Philox, BASELINE config shapes)", "impl": "reference",
+            "config": cfg,
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_detail": {k: cb[k] for k in cb if k not in ("value", "unit", "cores", "kind",
+                                                             "sample")},
+            "e2e": {"value": cb["value"], "unit": "nnz/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main_ours(args, world, rank, local):
+    import torch
     torch.cuda.set_device(local)
     dist = None
-    if world > 1 and args.impl == "ours":
+    if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         global DIST
@@ -826,24 +1143,8 @@ def main():
     from paper_1902_03317_b200 import _lib
     W = WORKLOADS[args.workload]
     # weak scaling: an independent instance per rank; strong (C5): one tensor
-    wl = W(args.seed if getattr(W, "STRONG", False) else args.seed + 1009 * rank, local,
-           args.scale)
+    wl = W(args.seed if W.STRONG else args.seed + 1009 * rank, local, args.scale, args.mttkrp)
     hbm, peak_src = peaks()
-
-    if args.impl == "reference":
-        cb = run_cpu_reference(wl, args.steps, args.warmup)
-        line = {"metric": METRIC, "value": cb["value"], "unit": "nnz/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": cb["step_s_mean"] * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic (seeded Philox, BASELINE config shapes)", "impl": "reference",
-                "config": wl.config(),
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": cb["value"], "unit": "nnz/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
-        return
-
     ctx = _lib.Context.get(local)
     lib = _lib.load()
     stream = torch.cuda.current_stream()
@@ -903,19 +1204,20 @@ def main():
         mean_ms = statistics.mean(op.times)
         by = op.bytes_fn()
         gbs = by / (mean_ms / 1e3) / 1e9
-        ops_out[op.name] = {"ms": round(mean_ms, 5), "ms_median": round(statistics.median(op.times), 5),
+        ops_out[op.name] = {"ms": round(mean_ms, 5),
+                            "ms_median": round(statistics.median(op.times), 5),
                             "alg_bytes": int(by), "GB_s": round(gbs, 1),
                             "frac": round(gbs / hbm, 4), "nnz_s": op.units / (mean_ms / 1e3),
                             "launches_per_call": op.launches / args.steps}
     # MTTKRP's second floor: every gathered factor row costs at least one L1
     # wavefront (<= 128 B) per SM-cycle whether it hits L1, L2 or smem
-    # ("Gather floor")
+    # ("Gather floor"); per rank's own units
     props = torch.cuda.get_device_properties(torch.cuda.current_device())
     sm_hz = float(_measured_peaks().get("sm_max_mhz", 1965.0)) * 1e6
     for op in wl.ops:
         if op.name.startswith("mttkrp"):
             N, R = len(wl.dims), wl.R
-            wf = wl.nnz * (N - 1) * -(-4 * R // 128)
+            wf = op.units * (N - 1) * -(-4 * R // 128)
             floor_ms = wf / (props.multi_processor_count * sm_hz) * 1e3
             ops_out[op.name]["gather_floor_ms"] = round(floor_ms, 5)
             ops_out[op.name]["gather_floor_frac"] = round(floor_ms / ops_out[op.name]["ms"], 4)
@@ -927,17 +1229,29 @@ def main():
                 "time_share": round(sum(dom.times) / sum(step_ms), 3)}
     if "gather_floor_ms" in d:
         roofline["gather_floor"] = {"ms": d["gather_floor_ms"], "frac": d["gather_floor_frac"],
-                                    "model": "nnz*(N-1)*ceil(4R/128) L1 wavefronts / (SMs * SM clock)"}
+                                    "model": "nnz*(N-1)*ceil(4R/128) L1 wavefronts / "
+                                             "(SMs * SM clock)"}
     tr = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tr):
-        roofline["traffic"] = json.load(open(tr)).get(dom.name)
+        t = json.load(open(tr))
+        if t.get("mttkrp_impl", "seg") == getattr(wl, "impl", "seg") or \
+                not dom.name.startswith("mttkrp"):
+            roofline["traffic"] = t.get(dom.name)
+            roofline["traffic_source"] = t.get("source", os.path.relpath(tr, ROOT))
+
+    # everything that needs the device-timed state before e2e may release it
+    gpu_launches = int(sum(op.launches for op in wl.ops))
+    rows = report_rows(wl, wl.ops) if (args.report and rank == 0) else None
+    cpu_in = None
+    if not args.no_cpu and rank == 0 and world == 1 and hasattr(wl, "cpu_arrays"):
+        cpu_in = wl.cpu_arrays()
 
     e2e = None
     if not args.no_e2e and hasattr(wl, "e2e_step"):
         # every rank runs its own host-buffer pipeline (its own PCIe link);
         # whole-job throughput over the slowest rank, like `value`
         host = wl.e2e_host(local)
-        wl.e2e_step(host, f"cuda:{local}")
+        wl.e2e_step(host)
         torch.cuda.synchronize()
         times = []
         for _ in range(max(2, min(args.steps, 5))):
@@ -947,7 +1261,7 @@ def main():
                 dist.barrier()
             torch.cuda.synchronize()
             a.record(stream)
-            h2d, d2h = wl.e2e_step(host, f"cuda:{local}")
+            h2d, d2h = wl.e2e_step(host)
             b.record(stream)
             torch.cuda.synchronize()
             times.append(a.elapsed_time(b))
@@ -958,15 +1272,15 @@ def main():
             ms = float(t.item())
         e2e = {"value": world * units_per_step / (ms / 1e3), "unit": "nnz/s",
                "h2d_bytes_per_step": world * h2d, "d2h_bytes_per_step": world * d2h,
-               "ms_per_step": ms,
-               "path": getattr(wl, "E2E_PATH", "ops.* -> C-ABI with pinned host buffers")}
+               "ms_per_step": ms, "path": getattr(wl, "E2E_PATH", "ops.* -> C-ABI")}
         del host
 
     cpu = None
-    if not args.no_cpu and rank == 0 and world == 1 and hasattr(wl, "cpu_setup"):
+    if cpu_in is not None:
         try:
-            cb = run_cpu_reference(wl, steps=3, warmup=1)
+            cb = run_cpu_leg(args.workload, cpu_in[0], cpu_in[1], steps=5, warmup=1)
             cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu["detail"] = {k: cb[k] for k in cb if k not in cpu}
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": "nnz/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -975,24 +1289,56 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "strong" if getattr(wl, "STRONG", False) else "weak",
+                "scaling": "strong" if W.STRONG else "weak",
                 "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded Philox, BASELINE config shapes; public datasets "
                         "unavailable offline)",
-                "config": {**wl.config(), "l2": "inputs > L2 and L2 flushed before every op",
-                           "timing": "CUDA events per op on the launch stream, max over ranks"},
+                "config": wl.config(),
+                "timing": {"l2": "inputs > L2 and L2 flushed before every op",
+                           "clock": "CUDA events per op on the launch stream, max over ranks"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": int(sum(op.launches for op in wl.ops)),
-                "clocks": clk, "ops": ops_out}
+                "gpu_launches": gpu_launches,
+                "clocks": clk, "ops": ops_out,
+                "preprocess_s": getattr(wl, "preprocess", {})}
         print(json.dumps(line))
-        if args.report:
+        if rows is not None:
             from paper_1902_03317_b200 import report
-            rows = report_rows(wl, wl.ops)
             with open(args.report, "w") as fh:
                 fh.write(report.emit_csv(rows) if args.report.endswith(".csv")
                          else report.emit_json(rows))
     if dist:
         dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mttkrp", default=None, choices=["plan", "seg"],
+                    help="MTTKRP kernel (default per workload: C5 plan, C1/C4 seg)")
+    ap.add_argument("--seed", type=int, default=20190210)
+    ap.add_argument("--scale", type=float, default=1.0, help="nnz scale (testing only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--prep-cpu", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--report", default=None,
+                    help="also write per-op rows in the reference's BenchReport schema "
+                         "(.json or .csv, P/include/spten/report.hpp)")
+    args = ap.parse_args()
+    if args.prep_cpu:
+        prep_cpu_inputs(args)
+        return
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        main_reference(args, world, rank)
+    else:
+        main_ours(args, world, rank, local)
 
 
 if __name__ == "__main__":
