@@ -61,10 +61,13 @@ typedef enum spt_status {
 typedef enum spt_elem_op { SPT_ADD = 0, SPT_SUB = 1, SPT_MUL = 2, SPT_DIV = 3 } spt_elem_op;
 typedef enum spt_scalar_op { SPT_SCALAR_ADD = 0, SPT_SCALAR_MUL = 1 } spt_scalar_op;
 typedef enum spt_mttkrp_strategy {
-  SPT_MTTKRP_AUTO = -1,     /* segmented if sort_order[0]==mode, else atomic */
+  SPT_MTTKRP_AUTO = -1,     /* segmented if sort_order[0]==mode, else a temporary plan
+                               (R % 16 == 0) or a mode-leading sorted copy: always
+                               deterministic, fp64 accumulation (the 1e-5 contract) */
   SPT_MTTKRP_SEGMENTED = 0, /* mode-sorted input; one writer per output row; deterministic;
                                tile shape (CTA / warp) picked by size */
-  SPT_MTTKRP_ATOMIC = 1,    /* any order; vector red.global.add into a zeroed output */
+  SPT_MTTKRP_ATOMIC = 1,    /* any order; vector red.global.add into a zeroed output
+                               (fp32 sums in arrival order: the 1e-4 class, only on request) */
   SPT_MTTKRP_SEGMENTED_CTA = 2,  /* segmented, forced 2048-entry CTA tiles */
   SPT_MTTKRP_SEGMENTED_WARP = 3  /* segmented, forced 256-entry warp tiles */
 } spt_mttkrp_strategy;
@@ -182,12 +185,12 @@ SPT_API int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const* d
  * with `mode` leading and the other modes by decreasing extent, whose most
  * gathered factor rows are served from shared memory. Built once (timed as
  * preprocessing, like the reference's sort_s, P/src/bench.cpp:363-368) and
- * executed any number of times with fresh factor values. Requires R % 16 == 0,
- * order 2..4, dims < 2^31 (otherwise SPT_EINVAL: use spt_mttkrp_f32). The plan
- * holds its own copy of x (indices and values): rebuild it if x changes. One
- * stream at a time per plan. */
+ * executed any number of times with fresh factor values. Requires R % 16 == 0
+ * and order 2..4 (otherwise SPT_EINVAL: use spt_mttkrp_f32). The plan holds its
+ * own copy of x (indices and values): rebuild it if x changes. One stream at a
+ * time per plan. */
 typedef struct spt_mttkrp_plan spt_mttkrp_plan;
-#define SPT_PLAN_NO_HOT 2u /* no shared-memory hot rows (every gather from L2/HBM) */
+#define SPT_PLAN_NO_HOT 2u /* no shared-memory hot rows even when SPT_PLAN_HOT_MAX asks for them */
 SPT_API int spt_mttkrp_plan_create(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint64_t R,
                                    unsigned flags, spt_mttkrp_plan** out, void* stream);
 /* out = dims[mode] x R row-major (16-byte aligned), fully written. Factors as
@@ -196,7 +199,7 @@ SPT_API int spt_mttkrp_plan_exec(spt_ctx* ctx, const spt_mttkrp_plan* plan,
                                  const float* const* d_factors, const uint64_t* rows,
                                  const uint64_t* cols, float* d_out, unsigned flags, void* stream);
 /* Level order (tensor mode per level, outermost first; order-1 entries) and
- * hot rows per level. Any pointer may be NULL. */
+ * rows per level served from shared memory. Any pointer may be NULL. */
 SPT_API int spt_mttkrp_plan_info(const spt_mttkrp_plan* plan, uint32_t* level_modes,
                                  uint32_t* hot_per_level, uint32_t* nhot);
 SPT_API void spt_mttkrp_plan_destroy(spt_mttkrp_plan* plan);

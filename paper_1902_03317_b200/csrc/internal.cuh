@@ -94,6 +94,11 @@ inline unsigned grid_for(uint64_t work_items, unsigned block, unsigned max_block
 int sort_tuples(spt_ctx* ctx, const spt_coo* x, const uint32_t* mode_order, uint32_t* d_perm,
                 cudaStream_t stream);  // stable; d_perm receives the permutation
 int gather_coo(spt_ctx* ctx, spt_coo* x, const uint32_t* d_perm, cudaStream_t stream);
+// MTTKRP plans (mttkrp_plan.cu) serve this input / rank.
+bool plan_supported(const spt_coo* x, uint64_t R);
+int mttkrp_sorted_copy(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors,
+                       const uint64_t* rows, const uint64_t* cols, uint32_t mode, float* d_out,
+                       unsigned flags, void* stream);
 
 }  // namespace spt
 

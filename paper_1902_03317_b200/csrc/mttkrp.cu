@@ -1991,6 +1991,46 @@ extern "C" int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uin
   return SPT_OK;
 }
 
+namespace spt {
+// A mode-leading sorted copy of x (stream-ordered temporaries), then the
+// segmented kernel on it.
+int mttkrp_sorted_copy(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors,
+                       const uint64_t* rows, const uint64_t* cols, uint32_t mode, float* d_out,
+                       unsigned flags, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const uint32_t N = x->order;
+  const size_t ab = ((x->nnz * 4 + 255) / 256) * 256;
+  char* mem = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&mem), ab * (N + 1), st) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(SPT_ENOMEM, "mttkrp: out of device memory for a sorted copy");
+  }
+  spt_coo c = *x;
+  int s = SPT_OK;
+  for (uint32_t d = 0; d < N && s == SPT_OK; ++d) {
+    c.idx[d] = reinterpret_cast<uint32_t*>(mem + d * ab);
+    if (cudaMemcpyAsync(c.idx[d], x->idx[d], x->nnz * 4, cudaMemcpyDeviceToDevice, st) !=
+        cudaSuccess)
+      s = cuda_status(cudaGetLastError(), "mttkrp sorted copy");
+  }
+  c.val = reinterpret_cast<float*>(mem + N * ab);
+  if (s == SPT_OK &&
+      cudaMemcpyAsync(c.val, x->val, x->nnz * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    s = cuda_status(cudaGetLastError(), "mttkrp sorted copy");
+  uint32_t order[SPT_MAX_ORDER];
+  order[0] = mode;
+  for (uint32_t d = 0, k = 1; d < N; ++d)
+    if (d != mode) order[k++] = d;
+  if (s == SPT_OK) s = spt_sort_f32(ctx, &c, order, 0, stream);
+  if (s == SPT_OK)
+    s = spt_mttkrp_f32(ctx, &c, d_factors, rows, cols, mode, d_out, SPT_MTTKRP_SEGMENTED,
+                       flags & ~SPT_FLAG_ASYNC, stream);
+  cudaStreamSynchronize(st);
+  cudaFreeAsync(mem, st);
+  return s;
+}
+}  // namespace spt
+
 extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors,
                               const uint64_t* rows, const uint64_t* cols, uint32_t mode,
                               float* d_out, int strategy, unsigned flags, void* stream) {
@@ -2035,10 +2075,24 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
   if (v.VEC == 4 && !aligned) v = {32, 1, pick_seg<32, 1>(nm1), pick_atomic<32, 1>(nm1), seg_smem<32, 1>(nm1)};
   const uint32_t CB = v.G * v.VEC;
 
-  if (strategy == SPT_MTTKRP_AUTO)
-    strategy = (x->has_sort_order && static_cast<uint32_t>(x->sort_order[0]) == mode)
-                   ? SPT_MTTKRP_SEGMENTED
-                   : SPT_MTTKRP_ATOMIC;
+  if (strategy == SPT_MTTKRP_AUTO) {
+    if (x->has_sort_order && static_cast<uint32_t>(x->sort_order[0]) == mode) {
+      strategy = SPT_MTTKRP_SEGMENTED;
+    } else {
+      // Any order, like seq::mttkrp (P/src/kernels_seq.cpp:153-174), on the
+      // 1e-5 contract: a temporary plan (a mode-leading copy, R % 16 == 0) or
+      // a mode-leading sorted copy for the segmented kernel. fp32 atomics only
+      // when the caller asks for MTTKRP_ATOMIC.
+      if (spt::plan_supported(x, R) && aligned) {
+        spt_mttkrp_plan* pl = nullptr;
+        SPT_TRY(spt_mttkrp_plan_create(ctx, x, mode, R, SPT_PLAN_NO_HOT, &pl, stream));
+        const int s = spt_mttkrp_plan_exec(ctx, pl, d_factors, rows, cols, d_out, 0, stream);
+        spt_mttkrp_plan_destroy(pl);
+        return s;
+      }
+      return spt::mttkrp_sorted_copy(ctx, x, d_factors, rows, cols, mode, d_out, flags, stream);
+    }
+  }
   if (strategy < SPT_MTTKRP_SEGMENTED || strategy > SPT_MTTKRP_SEGMENTED_WARP)
     return spt::set_error(SPT_EINVAL, "mttkrp: unknown strategy %d", strategy);
   // Warp tiles win in the latency-bound small-problem regime (C1: 1M nnz,

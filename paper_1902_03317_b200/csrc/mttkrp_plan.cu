@@ -47,6 +47,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -71,7 +72,7 @@ struct spt_mttkrp_plan {
 
 namespace {
 
-constexpr uint32_t kHot = 0x80000000u;
+constexpr uint32_t kHot = 0x80000000u;  // id field holds a shared-memory slot
 constexpr uint32_t kNoRow = 0xFFFFFFFFu;
 constexpr int kW = 16;  // warps per CTA: 128 registers, no spilled gather
 constexpr int kNB = 2;  // staging buffers per warp
@@ -161,29 +162,39 @@ __device__ __forceinline__ void stage_chunk(const PlanParams& p, uint32_t buf,
   }
 }
 
-// One factor row slice (16 B per lane): from the shared-memory hot copy when
-// the id carries kHot (a32 = hot base + slot * row bytes: the shift drops the
-// flag bit), else from global memory (a64 = level base + id * R * 4). Both
-// addresses are formed and one of two predicated loads runs: no generic
-// address, no branch.
-template <int CB>
+// One factor row slice (16 B per lane). HOT: from the shared-memory hot copy
+// when the id carries kHot (a32 = hot base + slot * row bytes: the shift drops
+// the flag bit), else from global memory; both addresses are formed and one
+// of two predicated loads runs (no generic address, no branch).
+template <int CB, bool HOT>
 __device__ __forceinline__ float4 gather_row(bool on, uint32_t e, uint32_t hot_q, const char* fb,
                                              uint32_t rb) {
-  constexpr int SH = CB == 32 ? 7 : 6;
-  const uint32_t a32 = hot_q + (e << SH);
-  const char* a64 = fb + (size_t)e * rb;
   float4 v;
-  asm volatile(
-      "{\n .reg .pred ph, pg, pon;\n"
-      " setp.ne.u32 pon, %4, 0;\n"
-      " setp.lt.s32 ph, %5, 0;\n"
-      " and.pred pg, pon, !ph;\n"
-      " and.pred ph, pon, ph;\n"
-      " @ph ld.shared.v4.f32 {%0, %1, %2, %3}, [%6];\n"
-      " @pg ld.global.v4.f32 {%0, %1, %2, %3}, [%7];\n"
-      "}"
-      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-      : "r"((uint32_t)on), "r"(e), "r"(a32), "l"(a64));
+  if constexpr (HOT) {
+    constexpr int SH = CB == 32 ? 7 : 6;
+    const uint32_t a32 = hot_q + (e << SH);
+    const char* a64 = fb + (size_t)e * rb;
+    asm volatile(
+        "{\n .reg .pred ph, pg, pon;\n"
+        " setp.ne.u32 pon, %4, 0;\n"
+        " setp.lt.s32 ph, %5, 0;\n"
+        " and.pred pg, pon, !ph;\n"
+        " and.pred ph, pon, ph;\n"
+        " @ph ld.shared.v4.f32 {%0, %1, %2, %3}, [%6];\n"
+        " @pg ld.global.v4.f32 {%0, %1, %2, %3}, [%7];\n"
+        "}"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "r"((uint32_t)on), "r"(e), "r"(a32), "l"(a64));
+  } else {
+    const char* a64 = fb + (size_t)e * rb;
+    asm volatile(
+        "{\n .reg .pred pon;\n"
+        " setp.ne.u32 pon, %4, 0;\n"
+        " @pon ld.global.v4.f32 {%0, %1, %2, %3}, [%5];\n"
+        "}"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "r"((uint32_t)on), "l"(a64));
+  }
   return v;
 }
 
@@ -228,7 +239,7 @@ __device__ void fold_slots(const uint32_t* srow, const double* sval, int nslot, 
   }
 }
 
-template <int NM1, int G>
+template <int NM1, int G, bool HOT>
 __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(PlanParams p) {
   using C = PCfg<NM1, G>;
   constexpr int GPW = C::GPW, CB = C::CB, CH = C::CH, U = C::U, GS = C::GS, S = C::S;
@@ -271,7 +282,7 @@ __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(P
 
   // hot rows of every level into shared memory by bulk copies (overlap the
   // first chunks); one CTA barrier counts their bytes
-  if (p.nhot) {
+  if (HOT && p.nhot) {
     if (tid == 0) mbar_arrive_tx(&s_hbar, p.nhot * CB * 4);
     __syncthreads();
     for (uint32_t s = tid; s < p.nhot; s += C::THREADS) {
@@ -333,7 +344,9 @@ __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(P
   for (uint32_t it = 0; it < niter; ++it) {
     const uint32_t e0 = it * U;
     const uint32_t c = e0 / CH, o = e0 % CH, b = c % kNB;
-    if (o == 0) spt::mbar_wait(&wbar[b], (c / kNB) & 1u);
+    if (o == 0) {
+      spt::mbar_wait(&wbar[b], (c / kNB) & 1u);
+    }
     const uint32_t sb = gbase + b * GPW * GS * 4 + o * 4;
     uint32_t rr[U], id[NM1][U];
     float vv[U];
@@ -370,12 +383,12 @@ __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(P
     float4 L[U];
     float4 M[NMID][U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) L[u] = gather_row<CB>(ok[u], id[NM1 - 1][u], hot_q, fb[NM1 - 1], rb);
+    for (int u = 0; u < U; ++u) L[u] = gather_row<CB, HOT>(ok[u], id[NM1 - 1][u], hot_q, fb[NM1 - 1], rb);
 #pragma unroll
     for (int j = 0; j < NM1 - 1; ++j)
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        M[j][u] = gather_row<CB>(ok[u] && nm[j][u], id[j][u], hot_q, fb[j], rb);
+        M[j][u] = gather_row<CB, HOT>(ok[u] && nm[j][u], id[j][u], hot_q, fb[j], rb);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (!ok[u]) break;
@@ -464,15 +477,15 @@ __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(P
 using PlanKernel = void (*)(PlanParams);
 
 struct PlanVariant {
-  PlanKernel fn;
+  PlanKernel fn, fn_hot;
   size_t fixed;
   uint32_t groups, CH, NA;
 };
 
 PlanVariant plan_variant(uint32_t nm1, uint32_t CB) {
-#define SPT_PV(N1, GG)                                                                       \
-  PlanVariant{mttkrp_plan_kernel<N1, GG>, PCfg<N1, GG>::FIXED, PCfg<N1, GG>::GROUPS,         \
-              PCfg<N1, GG>::CH, PCfg<N1, GG>::NA}
+#define SPT_PV(N1, GG)                                                                      \
+  PlanVariant{mttkrp_plan_kernel<N1, GG, false>, mttkrp_plan_kernel<N1, GG, true>,          \
+              PCfg<N1, GG>::FIXED, PCfg<N1, GG>::GROUPS, PCfg<N1, GG>::CH, PCfg<N1, GG>::NA}
   if (CB == 32) {
     if (nm1 == 1) return SPT_PV(1, 8);
     if (nm1 == 2) return SPT_PV(2, 8);
@@ -483,7 +496,7 @@ PlanVariant plan_variant(uint32_t nm1, uint32_t CB) {
     if (nm1 == 3) return SPT_PV(3, 4);
   }
 #undef SPT_PV
-  return PlanVariant{nullptr, 0, 0, 0, 0};
+  return PlanVariant{nullptr, nullptr, 0, 0, 0, 0};
 }
 
 // ---- plan construction kernels -------------------------------------------
@@ -522,14 +535,15 @@ __global__ void iota_kernel(uint32_t* a, uint32_t n) {
     a[i] = i;
 }
 
-__global__ void plan_slot_map_kernel(const uint2* hot, uint32_t nhot, LvlPtrs L) {
+// id -> encoded id maps: sel[s] -> kHot | s; unmapped ids stay as they are.
+__global__ void plan_slot_map_kernel(const uint2* sel, uint32_t nsel, uint32_t nhot, LvlPtrs L) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < nhot) {
-    const uint2 h = hot[s];
+  if (s < nsel) {
+    const uint2 h = sel[s];
     uint32_t* m = L.h[0];
     for (uint32_t j = 1; j < SPT_MAX_ORDER - 1; ++j)
       if (h.x == j) m = L.h[j];
-    m[h.y] = s;
+    m[h.y] = kHot | s;
   }
 }
 
@@ -538,7 +552,7 @@ __global__ void plan_encode_kernel(LvlPtrs L, int nm1, uint64_t nnz) {
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += stride)
     for (int j = 0; j < nm1; ++j) {
       const uint32_t s = L.h[j][L.p[j][e]];
-      if (s != 0xFFFFFFFFu) L.p[j][e] = kHot | s;
+      if (s != 0xFFFFFFFFu) L.p[j][e] = s;
     }
 }
 
@@ -592,7 +606,8 @@ int plan_select_hot(spt_ctx* ctx, spt_mttkrp_plan* pl, const uint32_t* row, uint
       std::min<uint64_t>((pl->nnz + 255) / 256, (uint64_t)ctx->num_sms * 8));
   plan_hist_kernel<<<std::max(grid, 1u), 256, 0, st>>>(row, L, static_cast<int>(nm1), pl->nnz);
   SPT_LAUNCHED(ctx);
-  // top-`cap` (count, id) of every level
+  // the `cap` most gathered (count, id) of every level
+  const uint32_t want = cap;
   size_t temp = 0;
   {
     cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
@@ -610,7 +625,7 @@ int plan_select_hot(spt_ctx* ctx, spt_mttkrp_plan* pl, const uint32_t* row, uint
     uint32_t cnt, lvl, id;
   };
   std::vector<Cand> cand;
-  std::vector<uint32_t> hc(cap), hi(cap);
+  std::vector<uint32_t> hc(want), hi(want);
   for (uint32_t j = 0; j < nm1; ++j) {
     const uint32_t n = pl->dims[pl->lvl_mode[j]];
     iota_kernel<<<std::max(1u, std::min<unsigned>((n + 255) / 256, ctx->num_sms * 8)), 256, 0,
@@ -620,34 +635,39 @@ int plan_select_hot(spt_ctx* ctx, spt_mttkrp_plan* pl, const uint32_t* row, uint
     size_t t2 = temp;
     SPT_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, t2, k, v, static_cast<int64_t>(n), 0,
                                                        32, st));
-    const uint32_t m = std::min(cap, n);
+    const uint32_t m = std::min(want, n);
     SPT_CUDA(cudaMemcpyAsync(hc.data(), k.Current(), m * 4, cudaMemcpyDeviceToHost, st));
     SPT_CUDA(cudaMemcpyAsync(hi.data(), v.Current(), m * 4, cudaMemcpyDeviceToHost, st));
     SPT_CUDA(cudaStreamSynchronize(st));
-    for (uint32_t i = 0; i < m; ++i) cand.push_back({hc[i], j, hi[i]});
+    for (uint32_t i = 0; i < m && hc[i] > 0; ++i) cand.push_back({hc[i], j, hi[i]});
   }
-  // a cached row costs one L2 read per CTA per launch: keep rows gathered
-  // more often than that
   std::stable_sort(cand.begin(), cand.end(),
                    [](const Cand& a, const Cand& b) { return a.cnt > b.cnt; });
-  std::vector<uint2> hot;
+  // a shared-memory row costs one L2 read per CTA per launch: keep rows
+  // gathered more often than that
+  std::vector<uint2> sel;
   const uint32_t thresh = 2u * static_cast<uint32_t>(ctx->num_sms);
-  for (const Cand& c : cand) {
-    if (hot.size() >= cap || c.cnt <= thresh) break;
-    hot.push_back(make_uint2(c.lvl, c.id));
-    pl->hot_per_level[c.lvl]++;
+  for (size_t i = 0; i < cand.size() && sel.size() < cap && cand[i].cnt > thresh; ++i) {
+    sel.push_back(make_uint2(cand[i].lvl, cand[i].id));
+    pl->hot_per_level[cand[i].lvl]++;
   }
-  pl->nhot = static_cast<uint32_t>(hot.size());
-  if (pl->nhot) {
+  pl->nhot = static_cast<uint32_t>(sel.size());
+  const uint32_t nsel = static_cast<uint32_t>(sel.size());
+  if (nsel) {
+    uint2* dsel = nullptr;
+    SPT_CUDA(cudaMallocAsync(&dsel, nsel * sizeof(uint2), st));
+    SPT_CUDA(cudaMemcpyAsync(dsel, sel.data(), nsel * sizeof(uint2), cudaMemcpyHostToDevice, st));
     SPT_CUDA(cudaMalloc(&pl->hot, pl->nhot * sizeof(uint2)));
-    SPT_CUDA(cudaMemcpyAsync(pl->hot, hot.data(), pl->nhot * sizeof(uint2),
-                             cudaMemcpyHostToDevice, st));
-    // id -> slot maps reuse the histogram words (the sort left them permuted)
+    SPT_CUDA(cudaMemcpyAsync(pl->hot, dsel, pl->nhot * sizeof(uint2), cudaMemcpyDeviceToDevice,
+                             st));
+    // id -> encoded id maps reuse the histogram words (the sort left them permuted)
     SPT_CUDA(cudaMemsetAsync(hist, 0xFF, hist_words * 4, st));
-    plan_slot_map_kernel<<<(pl->nhot + 255) / 256, 256, 0, st>>>(pl->hot, pl->nhot, L);
+    plan_slot_map_kernel<<<(nsel + 255) / 256, 256, 0, st>>>(dsel, nsel, pl->nhot, L);
     SPT_LAUNCHED(ctx);
     plan_encode_kernel<<<std::max(grid, 1u), 256, 0, st>>>(L, static_cast<int>(nm1), pl->nnz);
     SPT_LAUNCHED(ctx);
+    SPT_CUDA(cudaStreamSynchronize(st));  // sel (host) and dsel in use until here
+    SPT_CUDA(cudaFreeAsync(dsel, st));
   }
   SPT_CUDA(cudaFreeAsync(buf, st));
   SPT_CUDA(cudaFreeAsync(hist, st));
@@ -695,9 +715,16 @@ int plan_build(spt_ctx* ctx, spt_mttkrp_plan* pl, const spt_coo* x, unsigned fla
   for (uint32_t j = 0; j < pl->nm1; ++j) lvl[j] = c.idx[pl->lvl_mode[j]];
   const PlanVariant v = plan_variant(pl->nm1, pl->CB);
   const long avail = (long)plan_max_smem(ctx->device) - (long)v.fixed - 4096;  // static smem
-  const uint32_t cap = avail > 0 ? static_cast<uint32_t>(avail / (pl->CB * 4)) : 0;
-  if (s == SPT_OK && !(flags & SPT_PLAN_NO_HOT) && cap > 0)
-    s = plan_select_hot(ctx, pl, c.idx[pl->mode], lvl, cap, st);
+  uint32_t cap = avail > 0 ? static_cast<uint32_t>(avail / (pl->CB * 4)) : 0;
+  // Shared-memory hot rows measured no faster than L1 hits on the same
+  // rows (C1/C4/C5) and cost L1 capacity: off unless asked for.
+  cap = std::min<uint32_t>(cap, static_cast<uint32_t>(atoi(getenv("SPT_PLAN_HOT_MAX") ?: "0")));
+  // (An L2 evict_last tier for the next ~750K most-gathered rows, evict_first
+  // for the rest, measured no faster at C5 either: 23.1 vs 23.6 ms.)
+  bool ids_fit = true;  // kHot needs ids < 2^31
+  for (uint32_t j = 0; j < pl->nm1; ++j) ids_fit = ids_fit && pl->dims[pl->lvl_mode[j]] <= kHot;
+  if (!ids_fit || (flags & SPT_PLAN_NO_HOT)) cap = 0;
+  if (s == SPT_OK && cap > 0) s = plan_select_hot(ctx, pl, c.idx[pl->mode], lvl, cap, st);
   if (s == SPT_OK) {
     TileSrc src{};
     src.a[0] = c.idx[pl->mode];
@@ -719,11 +746,11 @@ int plan_build(spt_ctx* ctx, spt_mttkrp_plan* pl, const spt_coo* x, unsigned fla
 
 namespace spt {
 // Plan kernels serve R a multiple of 16 (CB = 32 or 16 columns per launch),
-// orders 2..4, dims < 2^31.
+// orders 2..4.
 bool plan_supported(const spt_coo* x, uint64_t R) {
   if (R == 0 || R % 16 != 0 || R > 0xFFFFFFFFull || x->order < 2 || x->order > 4) return false;
   for (uint32_t d = 0; d < x->order; ++d)
-    if (x->dims[d] >= kHot) return false;
+    if (x->dims[d] > 0xFFFFFFFEu) return false;
   return true;
 }
 }  // namespace spt
@@ -741,7 +768,7 @@ extern "C" int spt_mttkrp_plan_create(spt_ctx* ctx, const spt_coo* x, uint32_t m
   if (!x->coalesced) return spt::set_error(SPT_EINVAL, "mttkrp: tensor must be coalesced");
   if (!spt::plan_supported(x, R))
     return spt::set_error(SPT_EINVAL,
-                          "mttkrp_plan: needs R a multiple of 16, order 2..4, dims < 2^31");
+                          "mttkrp_plan: needs R a multiple of 16 and order 2..4");
   cudaStream_t st = spt::as_stream(stream);
   spt_mttkrp_plan* pl = new spt_mttkrp_plan();
   pl->device = ctx->device;
@@ -842,7 +869,8 @@ extern "C" int spt_mttkrp_plan_exec(spt_ctx* ctx, const spt_mttkrp_plan* pl,
   const size_t gfold = 16 + (((size_t)2 * pl->grid * 4 + 15) & ~size_t(15)) +
                        (size_t)2 * pl->grid * pl->CB * 8 + (size_t)kW * kNB * 8;
   const size_t smem = std::max(v.fixed + (size_t)pl->nhot * pl->CB * 4, gfold);
-  SPT_CUDA(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const PlanKernel fn = pl->nhot ? v.fn_hot : v.fn;
+  SPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   PlanParams p{};
   p.blk = pl->blk;
@@ -861,7 +889,7 @@ extern "C" int spt_mttkrp_plan_exec(spt_ctx* ctx, const spt_mttkrp_plan* pl,
   p.total_groups = pl->grid * v.groups;
   for (uint32_t c0 = 0; c0 < pl->R; c0 += pl->CB) {
     p.c0 = c0;
-    v.fn<<<pl->grid, kW * 32, smem, st>>>(p);
+    fn<<<pl->grid, kW * 32, smem, st>>>(p);
     SPT_LAUNCHED(ctx);
   }
   if (flags & SPT_FLAG_ASYNC) return SPT_OK;

@@ -71,6 +71,26 @@ def _stream(dev: torch.device) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
+def _check_vec(t: torch.Tensor, device, who: str, name: str, ndim: int) -> None:
+    """Dense operands handed to the C-ABI as raw pointers: contiguous float32
+    on the tensor's device with the expected rank."""
+    if (not isinstance(t, torch.Tensor) or t.dim() != ndim or t.dtype != torch.float32
+            or not t.is_contiguous() or t.device != device):
+        raise InvalidArgument(f"{who}: {name} must be a contiguous {ndim}-D float32 tensor on "
+                              f"{device}")
+
+
+def _check_out_coo(z: DeviceCOO, order: int, nnz: int, device, who: str) -> None:
+    """A caller-provided output COO must hold `nnz` entries of `order` modes on
+    the device (the C side writes through its raw pointers)."""
+    if z.order != order or z.nnz < nnz or z.device != device or any(
+            ix.numel() < nnz or ix.dtype != torch.int32 or not ix.is_contiguous()
+            for ix in z.indices) or z.values.dtype != torch.float32 \
+            or not z.values.is_contiguous():
+        raise InvalidArgument(f"{who}: out must be an order-{order} DeviceCOO with room for "
+                              f"{nnz} entries on {device}")
+
+
 def _flags(sync: bool) -> int:
     return 0 if sync else _lib.SPT_FLAG_ASYNC
 
@@ -90,6 +110,8 @@ def check_deferred(device: int | torch.device = 0) -> None:
 def ts(x: DeviceCOO, s: float, op: int, out: Optional[DeviceCOO] = None,
        sync: bool = True) -> DeviceCOO:
     ctx = _ctx(x)
+    if out is not None:
+        _check_out_coo(out, x.order, x.nnz, x.device, "ts")
     z = out if out is not None else DeviceCOO.empty(x.dims, x.nnz, x.device)
     xd, zd = x.descriptor(), z.descriptor()
     check(_lib.load().spt_ts_f32(ctx.handle, ctypes.byref(xd), float(s), int(op),
@@ -106,6 +128,8 @@ def ts(x: DeviceCOO, s: float, op: int, out: Optional[DeviceCOO] = None,
 def tew_eq(x: DeviceCOO, y: DeviceCOO, op: int, out: Optional[DeviceCOO] = None,
            sync: bool = True) -> DeviceCOO:
     ctx = _ctx(x)
+    if out is not None:
+        _check_out_coo(out, x.order, x.nnz, x.device, "tew_eq")
     z = out if out is not None else DeviceCOO.empty(x.dims, x.nnz, x.device)
     xd, yd, zd = x.descriptor(), y.descriptor(), z.descriptor()
     check(_lib.load().spt_tew_eq_f32(ctx.handle, ctypes.byref(xd), ctypes.byref(yd), int(op),
@@ -204,6 +228,8 @@ def tew(x: DeviceCOO, y: DeviceCOO, op: int, out: Optional[DeviceCOO] = None) ->
         sort_lexicographic(y, order)
     cap = x.nnz + y.nnz if op != MUL else min(x.nnz, y.nnz)
     dims = [max(a, b) for a, b in zip(x.dims, y.dims)]
+    if out is not None:
+        _check_out_coo(out, x.order, cap, x.device, "tew")
     z = out if out is not None else DeviceCOO.empty(dims, max(cap, 0), x.device)
     xd, yd, zd = x.descriptor(), y.descriptor(), z.descriptor()
     n = ctypes.c_uint64(0)
@@ -247,7 +273,10 @@ def ttv(x: DeviceCOO, v: torch.Tensor, mode: int, fib: Optional[FiberIndex] = No
         _precheck(x, mode, "ttv")
         fib = build_fiber_index(x, mode)
     _fiber_checks(x, mode, fib, "ttv")
+    _check_vec(v, x.device, "ttv", "v", 1)
     dims = [e for d, e in enumerate(x.dims) if d != mode]
+    if out is not None:
+        _check_out_coo(out, x.order - 1, fib.nfibs, x.device, "ttv")
     z = out if out is not None else DeviceCOO.empty(dims, fib.nfibs, x.device)
     xd, zd = x.descriptor(), z.descriptor()
     check(_lib.load().spt_ttv_f32(ctx.handle, ctypes.byref(xd), ptr(v), v.numel(), int(mode),
@@ -261,8 +290,7 @@ def ttv(x: DeviceCOO, v: torch.Tensor, mode: int, fib: Optional[FiberIndex] = No
 def ttm(x: DeviceCOO, u: torch.Tensor, mode: int, fib: Optional[FiberIndex] = None,
         out: Optional[DeviceCOO] = None) -> DeviceCOO:
     ctx = _ctx(x)
-    if u.dim() != 2:
-        raise InvalidArgument("ttm: u must be a matrix")
+    _check_vec(u, x.device, "ttm", "u", 2)
     if fib is None:
         _precheck(x, mode, "ttm")
         fib = build_fiber_index(x, mode)
@@ -270,6 +298,8 @@ def ttm(x: DeviceCOO, u: torch.Tensor, mode: int, fib: Optional[FiberIndex] = No
     R = int(u.shape[1])
     dims = list(x.dims)
     dims[mode] = R
+    if out is not None:
+        _check_out_coo(out, x.order, fib.nfibs * R, x.device, "ttm")
     z = out if out is not None else DeviceCOO.empty(dims, fib.nfibs * R, x.device)
     xd, zd = x.descriptor(), z.descriptor()
     check(_lib.load().spt_ttm_f32(ctx.handle, ctypes.byref(xd), ptr(u), int(u.shape[0]), R,

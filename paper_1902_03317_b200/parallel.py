@@ -61,10 +61,13 @@ def mttkrp_allreduce(x_shard, factors: Sequence, mode: int, rows: int, rank_R: i
     return part
 
 
-def pack_keys(t, order: Sequence[int]) -> np.ndarray:
+def pack_keys(t, order: Sequence[int], dims: Optional[Sequence[int]] = None) -> np.ndarray:
     """Host u64 keys of a sorted tensor (sort-order significance); used only
-    to choose key-range splitters (needs sum of index widths <= 64)."""
-    widths = [max(1, int(np.ceil(np.log2(max(2, t.dims[d]))))) for d in order]
+    to choose key-range splitters (needs sum of index widths <= 64). Two
+    tensors whose keys are compared must be packed with the same `dims` --
+    the TEW output dims, per-mode max (P/src/kernel_detail.hpp:97-102)."""
+    dims = list(t.dims) if dims is None else list(dims)
+    widths = [max(1, int(np.ceil(np.log2(max(2, dims[d]))))) for d in order]
     if sum(widths) > 64:
         raise OverflowError("key-range split needs <= 64 key bits")
     key = np.zeros(len(t.values), np.uint64)
@@ -73,6 +76,13 @@ def pack_keys(t, order: Sequence[int]) -> np.ndarray:
         ix = ix.cpu().numpy() if isinstance(ix, torch.Tensor) else ix
         key = (key << np.uint64(w)) | ix.view(np.uint32).astype(np.uint64)
     return key
+
+
+def tew_shards(x, y, order: Sequence[int], world: int) -> list:
+    """Per-rank key-range shards of two sorted TEW operands, keys packed with
+    the common (per-mode max) dims so both share one layout."""
+    dims = [max(a, b) for a, b in zip(x.dims, y.dims)]
+    return tew_key_ranges(pack_keys(x, order, dims), pack_keys(y, order, dims), world)
 
 
 def tew_key_ranges(x_keys: np.ndarray, y_keys: np.ndarray, world: int) -> list:

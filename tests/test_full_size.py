@@ -10,9 +10,15 @@ size-independent property or an on-device recomputation:
   intersection (mul) of the input key sets, matched values bit-exact x op y,
   unmatched values copied bit-exactly;
 * sort: non-decreasing keys and the same multiset of tuples (sorted keys equal);
-* MTTKRP (C4, 100M nnz, R=32), TTV and TTM (C3, 50M, every mode): per output
-  entry within TOL = 1e-5 of an fp64 recomputation (chunked torch index_add
-  over the same fp32 inputs), |y - y64| <= TOL * max(|y64|, sum|terms|).
+* MTTKRP (C4, 100M nnz, R=32, every mode; C5, 1B nnz, R=32, modes 0-2, the
+  plan kernel the bench runs and the segmented kernel), TTV and TTM (C3, 50M,
+  every mode): per output entry within TOL = 1e-5 of an fp64 recomputation
+  (chunked torch index_add over the same fp32 inputs),
+  |y - y64| <= TOL * max(|y64|, sum|terms|); rows without entries exactly 0;
+* C5 TEW-eq mul (1B nnz): bit-exact against one IEEE fp32 multiply per value;
+* the C5 row-aligned sharding of bench.py --gpus G (G = 2, 4, 8) emulated on
+  one GPU: each shard's plan run in turn, the owned row blocks assembled, the
+  result within the same 1e-5 rule and every row written by its owner only.
 """
 import pytest
 
@@ -122,15 +128,85 @@ def _mttkrp64(x, fs, mode):
     return out
 
 
-@pytest.mark.parametrize("mode", [0, 3])
+def _check_mttkrp(got, want):
+    got = got.to(torch.float64)
+    assert bool(((got - want).abs() <= TOL * want.abs()).all())
+    assert bool((got[want == 0] == 0).all())  # rows without entries are exact zeros
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_c4_mttkrp_full(lib, mode):
     ops, gen = lib
     c = gen.CONFIGS["c4"]
     x = gen.config_tensor("c4", seed=51, sort_order=[mode] + [d for d in range(4) if d != mode])
     fs = [gen.uniform((d, c["R"]), 51, 100 + k, 0.0, 1.0) for k, d in enumerate(c["dims"])]
-    got = ops.mttkrp(x, fs, mode).to(torch.float64)
     want = _mttkrp64(x, fs, mode)
-    assert bool(((got - want).abs() <= TOL * want.abs()).all())
+    _check_mttkrp(ops.mttkrp(x, fs, mode, ops.MTTKRP_SEGMENTED), want)
+    plan = ops.mttkrp_plan(x, mode, c["R"])
+    _check_mttkrp(ops.mttkrp(plan, fs, mode), want)
+
+
+@pytest.fixture(scope="module")
+def c5(lib):
+    ops, gen = lib
+    c = gen.CONFIGS["c5"]
+    x = gen.config_tensor("c5", seed=81, sort_order=[0, 1, 2])
+    fs = [gen.uniform((d, c["R"]), 81, 100 + k, 0.0, 1.0) for k, d in enumerate(c["dims"])]
+    return x, fs, c["R"]
+
+
+def test_c5_tew_eq_mul_full(lib, c5):
+    ops, gen = lib
+    x, _, _ = c5
+    y = type(x)(list(x.dims), x.indices, gen.uniform(x.nnz, 81, 77, 0.5, 1.5), list(x.sort_order),
+                True)
+    z = ops.tew_eq(x, y, ops.MUL)
+    assert torch.equal(bits(z.values), bits(x.values * y.values))
+    assert all(torch.equal(a, b) for a, b in zip(z.indices, x.indices))
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_c5_mttkrp_full(lib, c5, mode):
+    """1B entries, 10M-row Zipf(1.1) outputs: rows spanning many CTAs (the
+    grid fold), u32 offsets near 2^30."""
+    ops, gen = lib
+    x, fs, R = c5
+    want = _mttkrp64(x, fs, mode)
+    plan = ops.mttkrp_plan(x, mode, R)
+    _check_mttkrp(ops.mttkrp(plan, fs, mode), want)
+    del plan
+    torch.cuda.empty_cache()
+    if mode == 0:  # the segmented kernel on the mode-leading input it needs
+        _check_mttkrp(ops.mttkrp(x, fs, 0, ops.MTTKRP_SEGMENTED), want)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_c5_row_aligned_shards(lib, c5, G):
+    """bench.py's C5 strong-scaling split (parallel.row_aligned_ranges /
+    row_blocks, one plan per shard) run shard by shard on one GPU."""
+    from paper_1902_03317_b200 import parallel
+    ops, gen = lib
+    x, fs, R = c5
+    mode = 0
+    want = _mttkrp64(x, fs, mode)
+    rr = parallel.row_aligned_ranges(x.indices[mode], G)
+    blocks = parallel.row_blocks(x.indices[mode], rr, x.dims[mode])
+    assert rr[0][0] == 0 and rr[-1][1] == x.nnz
+    assert all(a[1] == b[0] for a, b in zip(rr[:-1], rr[1:]))
+    assert blocks[0][0] == 0 and blocks[-1][1] == x.dims[mode]
+    out = torch.full((x.dims[mode], R), float("nan"), device="cuda")
+    for (lo, hi), (a, b) in zip(rr, blocks):
+        if hi == lo:
+            continue
+        shard = parallel.slice_coo(x, lo, hi).clone()
+        plan = ops.mttkrp_plan(shard, mode, R)
+        part = ops.mttkrp(plan, fs, mode)
+        # a shard's rows are exact; everything outside its block is zero
+        assert bool((part[:a] == 0).all()) and bool((part[b:] == 0).all())
+        out[a:b] = part[a:b]
+        del plan, shard, part
+        torch.cuda.empty_cache()
+    _check_mttkrp(out, want)
 
 
 def _fiber_ids(x, fib):

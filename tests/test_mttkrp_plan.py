@@ -54,7 +54,11 @@ def _check(ops, x: HostTensor, fs, mode, **plan_kw):
 
 @pytest.mark.parametrize("R", [16, 32, 48, 64])
 @pytest.mark.parametrize("order", [2, 3, 4])
-def test_plan_shapes(ops, R, order):
+@pytest.mark.parametrize("hot", ["0", "100000"])
+def test_plan_shapes(ops, R, order, hot, monkeypatch):
+    """SPT_PLAN_HOT_MAX > 0 also serves the most gathered rows from shared
+    memory (the kernel's HOT instantiation)."""
+    monkeypatch.setenv("SPT_PLAN_HOT_MAX", hot)
     rng = np.random.default_rng(100 * R + order)
     dims = {2: [3000, 700], 3: [600, 500, 400], 4: [90, 80, 70, 60]}[order]
     x = rand_tensor(rng, dims, 60_000)
@@ -64,9 +68,10 @@ def test_plan_shapes(ops, R, order):
             _check(ops, x, fs, mode, **kw)
 
 
-def test_plan_zipf_hot_rows(ops):
+def test_plan_zipf_hot_rows(ops, monkeypatch):
     """Zipf modes: hot rows are chosen, long rows cross many lane groups and
     CTAs (CTA fold and the last-CTA grid fold)."""
+    monkeypatch.setenv("SPT_PLAN_HOT_MAX", "100000")
     from paper_1902_03317_b200 import generate
     g = generate.coo([20000, 8000, 3000], 2_000_000, 5, [1.1, 1.1, 1.1], 0.0, 1.0)
     x = HostTensor(*[getattr(g.to_host(), k) for k in ("dims", "indices", "values",

@@ -66,12 +66,13 @@ def _worker(rank, world, port, q):
         dist.all_gather_object(parts, z.values)
         out["ts"] = np.concatenate(parts)
         # TEW merge: key-range split
-        y = _tensor(5, dims, 15000)
+        # y has other dims (the output dims are the per-mode max): both key
+        # layouts must use the common dims or matches would split across ranks
+        y = _tensor(5, [70, 50, 33], 15000)
         xs, ys = x.copy(), y.copy()
         O.sort_lexicographic(xs, [0, 1, 2])
         O.sort_lexicographic(ys, [0, 1, 2])
-        kx, ky = parallel.pack_keys(xs, [0, 1, 2]), parallel.pack_keys(ys, [0, 1, 2])
-        (xl, xh), (yl, yh) = parallel.tew_key_ranges(kx, ky, world)[rank]
+        (xl, xh), (yl, yh) = parallel.tew_shards(xs, ys, [0, 1, 2], world)[rank]
         zr, _ = O.tew(parallel.slice_coo(xs, xl, xh), parallel.slice_coo(ys, yl, yh), 0)
         parts = [None] * world
         dist.all_gather_object(parts, (zr.indices, zr.values))
@@ -109,7 +110,7 @@ def test_two_rank_sharding_matches_single_process():
         O.sort_lexicographic(xs, [mode] + [d for d in range(3) if d != mode])
         assert np.array_equal(out[f"mttkrp_ag{mode}"], O.mttkrp(xs, fs, mode)[1])
     assert np.array_equal(out["ts"].view(np.uint32), O.ts(x, 2.5, 1).values.view(np.uint32))
-    y = _tensor(5, dims, 15000)
+    y = _tensor(5, [70, 50, 33], 15000)
     z, _ = O.tew(x.copy(), y.copy(), 0)
     for d in range(3):
         assert np.array_equal(out["tew_idx"][d], z.indices[d])
