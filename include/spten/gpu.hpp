@@ -27,35 +27,35 @@
 
 namespace spten::gpu {
 
-// P/include/spten/kernels_seq.hpp:25-30 (tew_eq): bit-identical to seq::tew_eq.
+// P/include/spten/kernels_seq.hpp:18-20 (tew_eq): bit-identical to seq::tew_eq.
 SparseTensorCOO<float> tew_eq(const SparseTensorCOO<float>& x, const SparseTensorCOO<float>& y,
                               ElemOp op);
 
-// P/include/spten/kernels_seq.hpp:32-40 (tew): bit-identical to seq::tew,
+// P/include/spten/kernels_seq.hpp:29-30 (tew): bit-identical to seq::tew,
 // including the ascending in-place sort of both operands when their sort
 // orders differ (P/src/kernel_detail.hpp:88-95).
 SparseTensorCOO<float> tew(SparseTensorCOO<float>& x, SparseTensorCOO<float>& y, ElemOp op);
 
-// P/include/spten/kernels_seq.hpp:42-44 (ts): bit-identical to seq::ts.
+// P/include/spten/kernels_seq.hpp:33-34 (ts): bit-identical to seq::ts.
 SparseTensorCOO<float> ts(const SparseTensorCOO<float>& x, float s, ScalarOp op);
 
-// P/include/spten/kernels_seq.hpp:46-53 (ttv): indices bit-identical; values
+// P/include/spten/kernels_seq.hpp:39-43 (ttv): indices bit-identical; values
 // within 1e-5 of an fp64 recomputation (fp64 fiber accumulation).
 SparseTensorCOO<float> ttv(const SparseTensorCOO<float>& x, const DenseVector<float>& v,
                            unsigned mode, const FiberIndex& fib);
 SparseTensorCOO<float> ttv(const SparseTensorCOO<float>& x, const DenseVector<float>& v,
                            unsigned mode);
 
-// P/include/spten/kernels_seq.hpp:55-61 (ttm).
+// P/include/spten/kernels_seq.hpp:47-51 (ttm).
 SparseTensorCOO<float> ttm(const SparseTensorCOO<float>& x, const DenseMatrix<float>& u,
                            unsigned mode, const FiberIndex& fib);
 SparseTensorCOO<float> ttm(const SparseTensorCOO<float>& x, const DenseMatrix<float>& u,
                            unsigned mode);
 
-// P/include/spten/kernels_seq.hpp:63-71 (mttkrp): any storage order; an input
+// P/include/spten/kernels_seq.hpp:59-61 (mttkrp): any storage order; an input
 // not sorted with `mode` leading is sorted on the device (a copy) and then
 // reduced by the deterministic segmented kernel. `strategy` mirrors
-// par::mttkrp (P/include/spten/kernels_par.hpp:341-346): privatize -> the
+// par::mttkrp (P/include/spten/kernels_par.hpp:70-72): privatize -> the
 // segmented (one writer per row) kernel, atomic -> vector red.global.add.
 DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
                           const std::vector<DenseMatrix<float>>& factors, unsigned mode);

@@ -106,16 +106,16 @@ SPT_API int spt_ctx_check(spt_ctx* ctx, void* stream);
 #define SPT_FLAG_ASYNC 1u /* do not synchronise; data-dependent errors deferred to spt_ctx_check */
 
 /* ---- TS: tensor-scalar ---------------------------------------------------
- * Replaces seq::ts / par::ts (P/include/spten/kernels_seq.hpp:42-44,
- * P/include/spten/kernels_par.hpp:324-325; body P/src/kernels_seq.cpp:55-67,
+ * Replaces seq::ts / par::ts (P/include/spten/kernels_seq.hpp:33-34,
+ * P/include/spten/kernels_par.hpp:50-51; body P/src/kernels_seq.cpp:55-67,
  * P/src/kernels_par.cpp:69-91). z gets x's indices (copied), values x+s or
  * x*s, x's dims/sort_order/coalesced. z->idx/z->val must hold x->nnz. */
 SPT_API int spt_ts_f32(spt_ctx* ctx, const spt_coo* x, float s, int op, spt_coo* z, unsigned flags,
                void* stream);
 
 /* ---- TEW-eq: elementwise op on identical patterns -------------------------
- * Replaces seq::tew_eq / par::tew_eq (P/include/spten/kernels_seq.hpp:25-30,
- * kernels_par.hpp:309-311; P/src/kernels_seq.cpp:11-39). Error precedence as
+ * Replaces seq::tew_eq / par::tew_eq (P/include/spten/kernels_seq.hpp:18-20,
+ * kernels_par.hpp:35-37; P/src/kernels_seq.cpp:11-39). Error precedence as
  * seq: the first failing entry decides; a pattern mismatch at entry m is
  * SPT_EINVAL, a stored zero divisor at entry m (pattern equal) SPT_EDOMAIN. */
 SPT_API int spt_tew_eq_f32(spt_ctx* ctx, const spt_coo* x, const spt_coo* y, int op, spt_coo* z,
@@ -150,7 +150,8 @@ SPT_API int spt_fiber_index(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint3
                     uint64_t* h_nfibs, uint64_t* d_nfibs, unsigned flags, void* stream);
 
 /* ---- TTV ------------------------------------------------------------------
- * Replaces seq::ttv / par::ttv with a FiberIndex (P/include/spten/kernels_seq.hpp:49-51,
+ * Replaces seq::ttv / par::ttv with a FiberIndex (P/include/spten/kernels_seq.hpp:39-41,
+ * kernels_par.hpp:53-55;
  * P/src/kernels_seq.cpp:69-101, P/src/kernel_detail.hpp:106-128). z is order N-1
  * with nfibs entries (buffers sized by the caller); values are fp32 fiber sums
  * (tolerance class), indices bit-exact. */
@@ -159,7 +160,8 @@ SPT_API int spt_ttv_f32(spt_ctx* ctx, const spt_coo* x, const float* d_v, uint64
                 void* stream);
 
 /* ---- TTM ------------------------------------------------------------------
- * Replaces seq::ttm / par::ttm (P/include/spten/kernels_seq.hpp:55-61,
+ * Replaces seq::ttm / par::ttm (P/include/spten/kernels_seq.hpp:47-49,
+ * kernels_par.hpp:60-62;
  * P/src/kernels_seq.cpp:108-151, P/src/kernel_detail.hpp:132-140). u is
  * u_rows x R row-major (device); z has nfibs*R entries laid out f*R+r. */
 SPT_API int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uint64_t u_rows,
@@ -167,8 +169,8 @@ SPT_API int spt_ttm_f32(spt_ctx* ctx, const spt_coo* x, const float* d_u, uint64
                 spt_coo* z, unsigned flags, void* stream);
 
 /* ---- MTTKRP ---------------------------------------------------------------
- * Replaces seq::mttkrp / par::mttkrp (P/include/spten/kernels_seq.hpp:63-71,
- * kernels_par.hpp:341-346; P/src/kernels_seq.cpp:153-174,
+ * Replaces seq::mttkrp / par::mttkrp (P/include/spten/kernels_seq.hpp:59-61,
+ * kernels_par.hpp:70-72; P/src/kernels_seq.cpp:153-174,
  * P/src/kernels_par.cpp:275-337, P/src/kernel_detail.hpp:153-188).
  * d_factors[d] (device, row-major rows[d] x cols[d]) for every mode d; entry
  * `mode` is ignored (may be NULL). d_out is dims[mode] x R row-major, fully

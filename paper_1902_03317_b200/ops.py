@@ -1,7 +1,7 @@
 """Host-side mirror of the reference's kernel entry points, on device tensors.
 
 Same names, argument meaning and error behaviour as `spten::seq` / `spten::par`
-(P/include/spten/kernels_seq.hpp:18-71, P/include/spten/kernels_par.hpp:305-346)
+(P/include/spten/kernels_seq.hpp:18-61, P/include/spten/kernels_par.hpp:35-72)
 and the tensor helpers (P/include/spten/tensor.hpp:147-165); every call goes
 through the C-ABI (include/spten_b200.h) to the sm_100a kernels. There is no
 CPU path: without the built extension these functions raise.
