@@ -572,6 +572,9 @@ class C2(Workload):
                         "sample": f"full C2 workload (4 x tew_eq on {self.nnz} nnz + tew "
                                   f"add/mul on {self.nnz} + {self.nnz} nnz)"}
 
+    def host_inputs(self):
+        return [self.x.to_host(), self.y.to_host(), self.y2.to_host()]
+
     E2E_CHUNKS = 8
     E2E_PATH = ("ops.* -> C-ABI; pinned host buffers; H2D / kernels / D2H overlapped on three "
                 "streams (staging.Pipeline), x/y uploaded in 8 chunks")
@@ -583,8 +586,7 @@ class C2(Workload):
         dev = torch.device("cuda", device)
         n = self.nnz
         return {"pipe": Pipeline(dev),
-                "pinned": [PinnedCOO.from_host(h) for h in (self.x.to_host(), self.y.to_host(),
-                                                            self.y2.to_host())],
+                "pinned": [PinnedCOO.from_host(h) for h in self.host_inputs()],
                 "dev": [DeviceCOO(list(self.dims), [torch.empty(n, dtype=torch.int32, device=dev)
                                                     for _ in self.dims],
                                   torch.empty(n, dtype=torch.float32, device=dev), [0, 1, 2],

@@ -30,7 +30,7 @@ def test_c2_pipelined_e2e_matches_oracle(scale):
         for o in host["out_eq"] + host["out_tew"]:
             o.val.fill_(np.nan)
             o.nnz = 0
-        h2d, d2h = wl.e2e_step(host, "cuda:0")
+        h2d, d2h = wl.e2e_step(host)
         torch.cuda.synchronize()
     hx, hy, hy2 = (_ht(h) for h in wl.host_inputs())
     assert h2d == 3 * wl.nnz * 16
@@ -59,7 +59,7 @@ def test_c1_pipelined_e2e_matches_oracle(scale):
             o.val.fill_(np.nan)
             o.nnz = 0
         host["out_m"].fill_(np.nan)
-        h2d, d2h = wl.e2e_step(host, "cuda:0")
+        h2d, d2h = wl.e2e_step(host)
         torch.cuda.synchronize()
     n = wl.nnz
     assert h2d == n * 16 + sum(f.numel() * 4 for f in wl.f)
@@ -71,3 +71,33 @@ def test_c1_pipelined_e2e_matches_oracle(scale):
     _, y64, yab = O.mttkrp(hx, [f.cpu().numpy() for f in wl.f], 0)
     got = host["out_m"].numpy()
     assert np.all(np.abs(got - y64) <= 1e-5 * np.maximum(np.abs(y64), yab))
+
+
+def test_c5_e2e_small_matches_fp64():
+    """C5's host-buffer path (uploads, one plan per mode built and run, the
+    I x R results and the TEW-eq output downloaded) at 1/1000 of the nnz."""
+    import bench
+    wl = bench.C5(20190210, 0, 0.001)
+    hx = wl.x.to_host()
+    hyv = wl.y.values.cpu().numpy()
+    fs = [f.clone() for f in wl.f]
+    host = wl.e2e_host(0)
+    h2d, d2h = wl.e2e_step(host)
+    torch.cuda.synchronize()
+    n = wl.nnz
+    assert h2d == 2 * n * 16 + sum(f.numel() * 4 for f in fs)
+    assert d2h == sum(o.numel() * 4 for o in host["out_m"]) + n * 16
+    idx = [torch.from_numpy(a.astype(np.int64)).cuda() for a in hx.indices]
+    val = torch.from_numpy(hx.values).cuda().to(torch.float64)
+    for m in range(3):
+        t = val[:, None].expand(-1, wl.R).clone()
+        for d in range(3):
+            if d != m:
+                t *= fs[d][idx[d]].to(torch.float64)
+        want = torch.zeros((wl.dims[m], wl.R), dtype=torch.float64, device="cuda")
+        want.index_add_(0, idx[m], t)
+        got = host["out_m"][m].cuda().to(torch.float64)
+        assert bool(((got - want).abs() <= 1e-5 * want.abs()).all()), m
+    z = host["out_eq"].to_host()
+    assert np.array_equal(z.values.view(np.uint32), (hx.values * hyv).view(np.uint32))
+    assert all(np.array_equal(a, b) for a, b in zip(z.indices, hx.indices))
