@@ -704,7 +704,7 @@ class C4(Workload):
     """configs[3]: MTTKRP every mode, R=32, 4th order, 100M nnz, Zipf(1.2) modes."""
 
     name = "c4-mttkrp"
-    MTTKRP = "seg"
+    MTTKRP = "plan"
     CPU_SAMPLE = 4_000_000
 
     def __init__(self, seed, device, scale=1.0, mttkrp=None):
@@ -1320,7 +1320,7 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mttkrp", default=None, choices=["plan", "seg"],
-                    help="MTTKRP kernel (default per workload: C5 plan, C1/C4 seg)")
+                    help="MTTKRP kernel (default per workload: C4/C5 plan, C1 seg)")
     ap.add_argument("--seed", type=int, default=20190210)
     ap.add_argument("--scale", type=float, default=1.0, help="nnz scale (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
