@@ -5,7 +5,7 @@ import json, sys, os
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from parse_launches import load
 
-def main(w, rnd="r01"):
+def main(w, rnd=os.environ.get("SPT_ROUND", "r02")):
     L = load(f"gpurun_out/launches_{w}.csv")
     plain = json.loads(open(f"gpurun_out/plain_{w}.json").read().strip().splitlines()[-1])
     names = list(plain["ops"].keys())
@@ -26,6 +26,8 @@ def main(w, rnd="r01"):
                    "kernels, mean over the bench's warmup+timed calls) from "
                    f"profiles/{rnd}_launches_{w}.csv (ncu --metrics ... --clock-control none, "
                    "cold L2: the bench flushes before every op)"}
+    out["mttkrp_impl"] = plain.get("config", {}).get("mttkrp", "seg")
+    out["source"] = f"profiles/{rnd}_launches_{w}.csv"
     for n, v in per.items():
         if v:
             out[n] = int(sum(b for _, b, _ in v) / len(v))
