@@ -13,6 +13,12 @@ SURVEY.md section 8(e):
     per rank instead of the all-reduce's 2(G-1)/G.
   * TEW-eq and TS shard with no communication (contiguous nnz ranges; the
     output stays sharded, rank order = global order).
+  * TTV / TTM shard by fibers (fiber_aligned_ranges): a tensor sorted with
+    the mode last is cut at the fiber start nearest below each equal-nnz
+    point, every rank computes the output entries of its own fibers, and the
+    outputs concatenate in rank order -- the single-process output, entry for
+    entry (the fiber loops of par::ttv / par::ttm, P/src/kernels_par.cpp:
+    199-212, :244-263, over rank-sized fiber ranges). No communication.
   * TEW (merge) shards by key range, the distributed form of
     par::partition_for_tew (P/src/kernels_par.cpp:93-142): splitter keys taken
     from x at equal-nnz positions, y cut at the same keys, each rank merges its
@@ -155,6 +161,32 @@ def row_blocks(rows, ranges: Sequence, n_rows: int) -> list:
     if first is not None:
         blocks[first] = (0, blocks[first][1])
     return blocks
+
+
+def fiber_aligned_ranges(fptr, world: int) -> list:
+    """Per-rank [lo, hi) entry ranges of a tensor sorted with `mode` last,
+    cut at fiber starts (fptr = build_fiber_index's nfibs+1 offsets): the
+    first fiber start at or after each equal-nnz point, so no fiber is
+    split. Returns [(lo, hi, f_lo, f_hi)]: entry range and fiber range."""
+    f = fptr.cpu().numpy() if isinstance(fptr, torch.Tensor) else np.asarray(fptr)
+    f = (f.view(np.uint32) if f.dtype == np.int32 else f).astype(np.int64)
+    n, nf = int(f[-1]), len(f) - 1
+    cuts = [0]
+    for r in range(1, world):
+        t = shard_range(n, world, r)[0]
+        k = int(np.searchsorted(f, t, side="left"))  # first fiber starting at or after t
+        cuts.append(max(min(k, nf), cuts[-1]))
+    cuts.append(nf)
+    return [(int(f[cuts[r]]), int(f[cuts[r + 1]]), cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def fiber_shard_index(fptr, f_lo: int, f_hi: int):
+    """The shard's own fiber index: fptr[f_lo..f_hi] rebased to 0."""
+    if isinstance(fptr, torch.Tensor):
+        f = fptr[f_lo:f_hi + 1].to(torch.int64) & 0xFFFFFFFF
+        return (f - f[0]).to(fptr.dtype)
+    f = np.asarray(fptr)[f_lo:f_hi + 1].astype(np.int64)
+    return f - f[0]
 
 
 def mttkrp_row_allgather(x_shard, factors: Sequence, mode: int, rows: int, rank_R: int,

@@ -78,6 +78,24 @@ def _worker(rank, world, port, q):
         dist.all_gather_object(parts, (zr.indices, zr.values))
         out["tew_idx"] = [np.concatenate([p[0][d] for p in parts]) for d in range(3)]
         out["tew_val"] = np.concatenate([p[1] for p in parts])
+        # TTV / TTM: fiber-aligned shards, outputs concatenated in rank order
+        for mode in range(3):
+            xs = x.copy()
+            O.sort_lexicographic(xs, [d for d in range(3) if d != mode] + [mode])
+            fptr = O.build_fiber_index(xs, mode)
+            lo, hi, f_lo, f_hi = parallel.fiber_aligned_ranges(fptr, world)[rank]
+            shard = parallel.slice_coo(xs, lo, hi)
+            sf = parallel.fiber_shard_index(fptr, f_lo, f_hi)
+            v = np.linspace(-1, 1, dims[mode]).astype(np.float32)
+            u = np.linspace(-1, 1, dims[mode] * 3).astype(np.float32).reshape(dims[mode], 3)
+            zv, _, _ = O.ttv(shard, v, mode, sf)
+            zm, _, _ = O.ttm(shard, u, mode, sf)
+            parts = [None] * world
+            dist.all_gather_object(parts, (zv.indices, zv.values, zm.indices, zm.values))
+            out[f"ttv{mode}"] = ([np.concatenate([p[0][d] for p in parts]) for d in range(2)],
+                                 np.concatenate([p[1] for p in parts]))
+            out[f"ttm{mode}"] = ([np.concatenate([p[2][d] for p in parts]) for d in range(3)],
+                                 np.concatenate([p[3] for p in parts]))
         if rank == 0:
             q.put(out)
     finally:
@@ -110,6 +128,19 @@ def test_two_rank_sharding_matches_single_process():
         O.sort_lexicographic(xs, [mode] + [d for d in range(3) if d != mode])
         assert np.array_equal(out[f"mttkrp_ag{mode}"], O.mttkrp(xs, fs, mode)[1])
     assert np.array_equal(out["ts"].view(np.uint32), O.ts(x, 2.5, 1).values.view(np.uint32))
+    for mode in range(3):  # fiber shards concatenate to the single-process output
+        xs = x.copy()
+        O.sort_lexicographic(xs, [d for d in range(3) if d != mode] + [mode])
+        v = np.linspace(-1, 1, dims[mode]).astype(np.float32)
+        u = np.linspace(-1, 1, dims[mode] * 3).astype(np.float32).reshape(dims[mode], 3)
+        zv, _, _ = O.ttv(xs, v, mode)
+        zm, _, _ = O.ttm(xs, u, mode)
+        gi, gv = out[f"ttv{mode}"]
+        assert all(np.array_equal(a, b) for a, b in zip(gi, zv.indices))
+        assert np.array_equal(gv.view(np.uint32), zv.values.view(np.uint32))
+        gi, gv = out[f"ttm{mode}"]
+        assert all(np.array_equal(a, b) for a, b in zip(gi, zm.indices))
+        assert np.array_equal(gv.view(np.uint32), zm.values.view(np.uint32))
     y = _tensor(5, [70, 50, 33], 15000)
     z, _ = O.tew(x.copy(), y.copy(), 0)
     for d in range(3):
@@ -125,6 +156,22 @@ def test_shard_range_partitions():
             assert r[0][0] == 0 and r[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
             assert max(h - l for l, h in r) - min(h - l for l, h in r) <= 1
+
+
+def test_fiber_aligned_ranges():
+    from paper_1902_03317_b200.parallel import fiber_aligned_ranges, fiber_shard_index
+    rng = np.random.default_rng(3)
+    for nf, world in ((100, 2), (100, 8), (3, 8), (1, 4)):
+        lens = rng.integers(1, 50, nf)
+        fptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+        rr = fiber_aligned_ranges(fptr, world)
+        assert rr[0][0] == 0 and rr[-1][1] == fptr[-1] and rr[-1][3] == nf
+        for (lo, hi, a, b), (lo2, _, a2, _) in zip(rr, rr[1:]):
+            assert hi == lo2 and b == a2
+        for lo, hi, a, b in rr:
+            assert fptr[a] == lo and fptr[b] == hi  # cuts on fiber starts
+            sf = fiber_shard_index(fptr, a, b)
+            assert sf[0] == 0 and sf[-1] == hi - lo and len(sf) == b - a + 1
 
 
 def test_row_aligned_ranges_and_blocks():
