@@ -458,6 +458,10 @@ class C1(Workload):
                         "sample": f"full C1 workload: mttkrp mode 0 (R={self.R}, faster "
                                   f"strategy) + ts add/mul on {self.nnz} nnz"}
 
+    def e2e_arrays(self):
+        """The full workload as host arrays for the C++ drop-in leg."""
+        return self.cpu_arrays()
+
     # e2e through the C-ABI with host buffers
     E2E_CHUNKS = 4
     E2E_PATH = ("ops.* -> C-ABI; pinned host buffers; x uploaded in 4 chunks (TS of each chunk "
@@ -574,6 +578,10 @@ class C2(Workload):
 
     def host_inputs(self):
         return [self.x.to_host(), self.y.to_host(), self.y2.to_host()]
+
+    def e2e_arrays(self):
+        """The full workload as host arrays for the C++ drop-in leg."""
+        return self.cpu_arrays()
 
     E2E_CHUNKS = 8
     E2E_PATH = ("ops.* -> C-ABI; pinned host buffers; H2D / kernels / D2H overlapped on three "
@@ -920,6 +928,16 @@ class C5(Workload):
                 "downloaded while the next plan builds; TEW-eq mul and its full output "
                 "(indices + values) downloaded")
 
+    def e2e_arrays(self):
+        """The full workload as host arrays for the C++ drop-in leg (x in its
+        mode-0 order, y's values, the factors); releases the device state."""
+        arrays = {f"x_i{d}": _idx_np(self.x.indices[d]) for d in range(3)}
+        arrays["x_val"] = _np(self.x.values)
+        arrays["yval"] = _np(self.y.values)
+        arrays.update({f"f{d}": _np(f) for d, f in enumerate(self.f)})
+        self.e2e_release()
+        return arrays, {"dims": self.dims}
+
     def e2e_release(self):
         """Free the device-timed state (e2e needs the memory)."""
         import torch
@@ -1249,7 +1267,32 @@ def main_ours(args, world, rank, local):
         cpu_in = wl.cpu_arrays()
 
     e2e = None
-    if not args.no_e2e and hasattr(wl, "e2e_step"):
+    dropin = os.path.join(ROOT, "paper_1902_03317_b200", "host", "dropin_bench")
+    use_dropin = (not args.no_e2e and args.e2e_via == "dropin" and world == 1
+                  and hasattr(wl, "e2e_arrays") and os.path.exists(dropin))
+    if use_dropin:
+        # the C++ drop-in (spten::gpu::*) on host SparseTensorCOO data: every
+        # call uploads its operands, computes and returns its result by value
+        arrays, meta = wl.e2e_arrays()
+        base = "/dev/shm" if os.path.isdir("/dev/shm") else None
+        dd = tempfile.mkdtemp(prefix="spt_e2e_", dir=base)
+        try:
+            save_arrays(dd, arrays, meta)
+            del arrays
+            torch.cuda.empty_cache()
+            key = {"c1-mttkrp-ts": "c1", "c2-tew_eq-tew": "c2", "c5-mttkrp-tew_eq": "c5"}[wl.name]
+            out = subprocess.run([dropin, dd, key, str(max(2, min(args.steps, 3))), "1"],
+                                 capture_output=True, text=True, check=True).stdout
+        finally:
+            shutil.rmtree(dd, ignore_errors=True)
+        r = json.loads(out.strip().splitlines()[-1])
+        e2e = {"value": r["units_per_step"] / (r["ms_per_step"] / 1e3), "unit": "nnz/s",
+               "h2d_bytes_per_step": int(r["h2d_bytes_per_step"]),
+               "d2h_bytes_per_step": int(r["d2h_bytes_per_step"]),
+               "ms_per_step": r["ms_per_step"], "ms_median": r["ms_median"],
+               "path": r["path"] + " (paper_1902_03317_b200/host/dropin_bench)",
+               "timing": "host wall clock per step, one call per op, each returning by value"}
+    elif not args.no_e2e and hasattr(wl, "e2e_step"):
         # every rank runs its own host-buffer pipeline (its own PCIe link);
         # whole-job throughput over the slowest rank, like `value`
         host = wl.e2e_host(local)
@@ -1324,6 +1367,9 @@ def main():
     ap.add_argument("--seed", type=int, default=20190210)
     ap.add_argument("--scale", type=float, default=1.0, help="nnz scale (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-via", default="dropin", choices=["dropin", "python"],
+                    help="e2e through the C++ drop-in (spten::gpu::*, host SparseTensorCOO "
+                         "data) or the Python ops.* pipeline with pinned buffers")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--prep-cpu", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--report", default=None,

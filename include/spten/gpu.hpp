@@ -5,8 +5,9 @@
 // SparseTensorCOO<float> / DenseVector<float> / DenseMatrix<float> /
 // FiberIndex values: this header includes the reference's own type headers
 // (P/include/spten/tensor.hpp, ops.hpp), it does not redeclare them.
-// Every function forwards to the C-ABI in include/spten_b200.h (H2D, one
-// sm_100a kernel chain on a per-thread stream, D2H) and
+// Every function forwards to the C-ABI in include/spten_b200.h (H2D through
+// pinned bounce buffers into device buffers kept per thread across calls,
+// the sm_100a kernel chain on a per-thread stream, D2H likewise) and
 //   * throws the reference's exception types: std::invalid_argument,
 //     std::domain_error, std::overflow_error, std::bad_alloc,
 //     std::runtime_error (CUDA failures);
@@ -53,10 +54,11 @@ SparseTensorCOO<float> ttm(const SparseTensorCOO<float>& x, const DenseMatrix<fl
                            unsigned mode);
 
 // P/include/spten/kernels_seq.hpp:59-61 (mttkrp): any storage order; an input
-// not sorted with `mode` leading is sorted on the device (a copy) and then
-// reduced by the deterministic segmented kernel. `strategy` mirrors
-// par::mttkrp (P/include/spten/kernels_par.hpp:70-72): privatize -> the
-// segmented (one writer per row) kernel, atomic -> vector red.global.add.
+// sorted with `mode` leading goes to the deterministic segmented kernel,
+// any other to a device-side plan (a mode-leading copy, R % 16 == 0) or sorted
+// copy: fp64 accumulation, within 1e-5 of fp64 per entry. `strategy` mirrors
+// par::mttkrp (P/include/spten/kernels_par.hpp:70-72): privatize -> those
+// deterministic paths, atomic -> vector red.global.add (fp32, 1e-4 class).
 DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
                           const std::vector<DenseMatrix<float>>& factors, unsigned mode);
 DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
@@ -67,5 +69,28 @@ DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
 void sort_lexicographic(SparseTensorCOO<float>& t, std::span<const unsigned> mode_order);
 SparseTensorCOO<float> coalesce(const SparseTensorCOO<float>& t);
 FiberIndex build_fiber_index(const SparseTensorCOO<float>& t, unsigned mode);
+
+// The par:: twins (P/include/spten/kernels_par.hpp:35-72), so a caller of
+// spten::par:: only swaps the namespace. The device is the parallelism:
+// nthreads is accepted with any value (as par::resolve_threads accepts any,
+// P/src/kernels_par.cpp:15-17) and has no effect.
+namespace par {
+SparseTensorCOO<float> tew_eq(const SparseTensorCOO<float>& x, const SparseTensorCOO<float>& y,
+                              ElemOp op, int nthreads);
+SparseTensorCOO<float> tew(SparseTensorCOO<float>& x, SparseTensorCOO<float>& y, ElemOp op,
+                           int nthreads);
+SparseTensorCOO<float> ts(const SparseTensorCOO<float>& x, float s, ScalarOp op, int nthreads);
+SparseTensorCOO<float> ttv(const SparseTensorCOO<float>& x, const DenseVector<float>& v,
+                           unsigned mode, const FiberIndex& fib, int nthreads);
+SparseTensorCOO<float> ttv(const SparseTensorCOO<float>& x, const DenseVector<float>& v,
+                           unsigned mode, int nthreads);
+SparseTensorCOO<float> ttm(const SparseTensorCOO<float>& x, const DenseMatrix<float>& u,
+                           unsigned mode, const FiberIndex& fib, int nthreads);
+SparseTensorCOO<float> ttm(const SparseTensorCOO<float>& x, const DenseMatrix<float>& u,
+                           unsigned mode, int nthreads);
+DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
+                          const std::vector<DenseMatrix<float>>& factors, unsigned mode,
+                          int nthreads, MttkrpStrategy strategy);
+}  // namespace par
 
 }  // namespace spten::gpu

@@ -41,15 +41,108 @@ inline void cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// One context + stream per host thread and device (contexts are not
-// thread-safe; streams keep concurrent callers independent).
+// Per host thread and device: a context, a compute stream and two copy
+// streams, grow-only device buffers reused across calls (no allocation in the
+// steady state) and pinned bounce buffers, so host <-> device traffic from the
+// caller's pageable std::vectors runs at PCIe speed: the host copies chunk k
+// into a pinned buffer (several threads) while the DMA engine moves chunk k-1.
+constexpr size_t kChunk = size_t(32) << 20;  // bytes per pinned bounce buffer
+
+void par_memcpy(void* dst, const void* src, size_t n) {
+  constexpr size_t kPiece = size_t(1) << 20;
+  const long pieces = static_cast<long>((n + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static) num_threads(8) if (pieces > 1)
+  for (long i = 0; i < pieces; ++i) {
+    const size_t o = static_cast<size_t>(i) * kPiece;
+    std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                std::min(kPiece, n - o));
+  }
+}
+
 struct Session {
   int device = -1;
   spt_ctx* ctx = nullptr;
-  cudaStream_t stream = nullptr;
-  ~Session() {
+  cudaStream_t stream = nullptr, h2d = nullptr, d2h = nullptr;
+  void* pin[4] = {};  // [0,1] upload, [2,3] download
+  cudaEvent_t ev[4] = {}, done_h2d = nullptr, done_cmp = nullptr;
+  std::vector<std::pair<void*, size_t>> slots;  // grow-only device buffers
+  int next = 0;  // round robin over the two upload buffers
+  ~Session() { release(); }
+  void release() {
+    if (device < 0) return;
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();
     if (ctx) spt_ctx_destroy(ctx);
-    if (stream) cudaStreamDestroy(stream);
+    for (auto& s : slots) cudaFree(s.first);
+    for (int i = 0; i < 4; ++i) {
+      if (pin[i]) cudaFreeHost(pin[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+    for (cudaStream_t s : {stream, h2d, d2h})
+      if (s) cudaStreamDestroy(s);
+    if (done_h2d) cudaEventDestroy(done_h2d);
+    if (done_cmp) cudaEventDestroy(done_cmp);
+    *this = Session();
+    device = -1;
+  }
+  Session& operator=(const Session&) = default;
+
+  // Device buffer `slot`, at least `bytes`, kept across calls.
+  void* buf(size_t slot, size_t bytes) {
+    if (slots.size() <= slot) slots.resize(slot + 1, {nullptr, 0});
+    auto& s = slots[slot];
+    if (s.second < bytes || !s.first) {
+      cuda(cudaStreamSynchronize(stream), "sync");
+      if (s.first) cudaFree(s.first);
+      s = {nullptr, 0};
+      const size_t want = std::max<size_t>(bytes + bytes / 8, 256);
+      cuda(cudaMalloc(&s.first, want), "cudaMalloc");
+      s.second = want;
+    }
+    return s.first;
+  }
+
+  // Pageable host -> device through the pinned ring (stream h2d).
+  void upload(void* dst, const void* src, size_t n) {
+    if (!n) return;
+    for (size_t o = 0; o < n; o += kChunk) {
+      const size_t c = std::min(kChunk, n - o);
+      const int k = next;
+      next ^= 1;
+      cuda(cudaEventSynchronize(ev[k]), "sync");  // the DMA out of this buffer is done
+      par_memcpy(pin[k], static_cast<const char*>(src) + o, c);
+      cuda(cudaMemcpyAsync(static_cast<char*>(dst) + o, pin[k], c, cudaMemcpyHostToDevice, h2d),
+           "H2D");
+      cuda(cudaEventRecord(ev[k], h2d), "event");
+    }
+  }
+  // Compute stream waits for every upload issued so far.
+  void uploads_done() {
+    cuda(cudaEventRecord(done_h2d, h2d), "event");
+    cuda(cudaStreamWaitEvent(stream, done_h2d, 0), "wait");
+  }
+  // Device -> pageable host after the compute stream's work so far: DMA of
+  // chunk k overlaps the host copy of chunk k-1.
+  void download(void* dst, const void* src, size_t n) {
+    if (!n) return;
+    cuda(cudaEventRecord(done_cmp, stream), "event");
+    cuda(cudaStreamWaitEvent(d2h, done_cmp, 0), "wait");
+    size_t prev_o = 0, prev_c = 0;
+    int prev_k = -1, k = 2;
+    for (size_t o = 0; o < n; o += kChunk) {
+      const size_t c = std::min(kChunk, n - o);
+      cuda(cudaMemcpyAsync(pin[k], static_cast<const char*>(src) + o, c, cudaMemcpyDeviceToHost,
+                           d2h), "D2H");
+      cuda(cudaEventRecord(ev[k], d2h), "event");
+      if (prev_k >= 0) {
+        cuda(cudaEventSynchronize(ev[prev_k]), "sync");
+        par_memcpy(static_cast<char*>(dst) + prev_o, pin[prev_k], prev_c);
+      }
+      prev_k = k, prev_o = o, prev_c = c;
+      k = k == 2 ? 3 : 2;
+    }
+    cuda(cudaEventSynchronize(ev[prev_k]), "sync");
+    par_memcpy(static_cast<char*>(dst) + prev_o, pin[prev_k], prev_c);
   }
 };
 
@@ -58,68 +151,55 @@ Session& session() {
   int dev = 0;
   cuda(cudaGetDevice(&dev), "cudaGetDevice");
   if (s.device != dev) {
-    if (s.ctx) spt_ctx_destroy(s.ctx);
-    if (s.stream) cudaStreamDestroy(s.stream);
-    s.ctx = nullptr;
-    s.stream = nullptr;
+    s.release();
     check(spt_ctx_create(dev, &s.ctx));
-    cuda(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (cudaStream_t* p : {&s.stream, &s.h2d, &s.d2h})
+      cuda(cudaStreamCreateWithFlags(p, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < 4; ++i) {
+      cuda(cudaMallocHost(&s.pin[i], kChunk), "cudaMallocHost");
+      cuda(cudaEventCreateWithFlags(&s.ev[i], cudaEventDisableTiming), "event");
+    }
+    cuda(cudaEventCreateWithFlags(&s.done_h2d, cudaEventDisableTiming), "event");
+    cuda(cudaEventCreateWithFlags(&s.done_cmp, cudaEventDisableTiming), "event");
     s.device = dev;
   }
   return s;
 }
 
-// Stream-ordered device buffer.
-struct DBuf {
-  void* p = nullptr;
-  cudaStream_t st;
-  DBuf(size_t bytes, cudaStream_t s) : st(s) {
-    cuda(cudaMallocAsync(&p, bytes ? bytes : 16, st), "cudaMallocAsync");
-  }
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() { cudaFreeAsync(p, st); }
-  template <typename T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
+// Device buffer slots of one call: tensors take 9 slots each (N <= 8 index
+// arrays + values).
+enum Slot : size_t { kX = 0, kY = 9, kZ = 18, kF = 27, kOut = 36, kAux = 37, kAux2 = 38 };
 
-// Device copy of a SparseTensorCOO<float> plus its C-ABI descriptor.
+// A SparseTensorCOO<float> in session slots, with its C-ABI descriptor.
 struct DevCoo {
   spt_coo d{};
-  std::vector<DBuf*> bufs;
-  cudaStream_t st;
-  DevCoo(unsigned order, const std::vector<Index>& dims, size_t nnz, cudaStream_t s) : st(s) {
+  Session* S;
+  DevCoo(Session& s, size_t base, unsigned order, const std::vector<Index>& dims, size_t nnz)
+      : S(&s) {
     if (order > SPT_MAX_ORDER)
       throw std::invalid_argument("spten::gpu: order exceeds " + std::to_string(SPT_MAX_ORDER));
     d.order = order;
     d.nnz = nnz;
     for (unsigned m = 0; m < order; ++m) {
       d.dims[m] = m < dims.size() ? dims[m] : 0;
-      bufs.push_back(new DBuf(nnz * sizeof(Index), st));
-      d.idx[m] = bufs.back()->as<uint32_t>();
+      d.idx[m] = static_cast<uint32_t*>(s.buf(base + m, nnz * sizeof(Index)));
     }
-    bufs.push_back(new DBuf(nnz * sizeof(float), st));
-    d.val = bufs.back()->as<float>();
+    d.val = static_cast<float*>(s.buf(base + 8, nnz * sizeof(float)));
   }
-  ~DevCoo() {
-    for (auto* b : bufs) delete b;
-  }
-  static DevCoo* upload(const SparseTensorCOO<float>& t, cudaStream_t s) {
+  static DevCoo upload(Session& s, size_t base, const SparseTensorCOO<float>& t) {
     for (unsigned m = 0; m < t.order(); ++m)
       if (t.indices[m].size() != t.nnz())
         throw std::invalid_argument("spten::gpu: index array length != nnz");
-    auto* dc = new DevCoo(t.order(), t.dims, t.nnz(), s);
+    DevCoo dc(s, base, t.order(), t.dims, t.nnz());
     const size_t n = t.nnz();
-    for (unsigned m = 0; m < t.order(); ++m)
-      if (n) cuda(cudaMemcpyAsync(dc->d.idx[m], t.indices[m].data(), n * 4, cudaMemcpyHostToDevice, s), "H2D");
-    if (n) cuda(cudaMemcpyAsync(dc->d.val, t.values.data(), n * 4, cudaMemcpyHostToDevice, s), "H2D");
+    for (unsigned m = 0; m < t.order(); ++m) s.upload(dc.d.idx[m], t.indices[m].data(), n * 4);
+    s.upload(dc.d.val, t.values.data(), n * 4);
     if (t.sort_order) {
-      dc->d.has_sort_order = 1;
-      for (unsigned m = 0; m < t.order(); ++m) dc->d.sort_order[m] = static_cast<int32_t>((*t.sort_order)[m]);
+      dc.d.has_sort_order = 1;
+      for (unsigned m = 0; m < t.order(); ++m)
+        dc.d.sort_order[m] = static_cast<int32_t>((*t.sort_order)[m]);
     }
-    dc->d.coalesced = t.coalesced ? 1 : 0;
+    dc.d.coalesced = t.coalesced ? 1 : 0;
     return dc;
   }
   // Copy the first n entries and the metadata of descriptor `meta` back.
@@ -127,21 +207,14 @@ struct DevCoo {
     t.dims.assign(meta.dims, meta.dims + meta.order);
     t.indices.assign(meta.order, std::vector<Index>(n));
     t.values.resize(n);
-    for (unsigned m = 0; m < meta.order; ++m)
-      if (n) cuda(cudaMemcpyAsync(t.indices[m].data(), meta.idx[m], n * 4, cudaMemcpyDeviceToHost, st), "D2H");
-    if (n) cuda(cudaMemcpyAsync(t.values.data(), meta.val, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
-    cuda(cudaStreamSynchronize(st), "sync");
-    if (meta.has_sort_order) t.sort_order = std::vector<unsigned>(meta.sort_order, meta.sort_order + meta.order);
-    else t.sort_order.reset();
+    for (unsigned m = 0; m < meta.order; ++m) S->download(t.indices[m].data(), meta.idx[m], n * 4);
+    S->download(t.values.data(), meta.val, n * 4);
+    if (meta.has_sort_order)
+      t.sort_order = std::vector<unsigned>(meta.sort_order, meta.sort_order + meta.order);
+    else
+      t.sort_order.reset();
     t.coalesced = meta.coalesced != 0;
   }
-};
-
-struct Owned {
-  DevCoo* p;
-  explicit Owned(DevCoo* q) : p(q) {}
-  ~Owned() { delete p; }
-  DevCoo* operator->() const { return p; }
 };
 
 // check_fiber_kernel_inputs, P/src/kernel_detail.hpp:106-119 (host-side part)
@@ -158,28 +231,30 @@ void check_fiber(const SparseTensorCOO<float>& x, unsigned mode, const FiberInde
     throw std::invalid_argument(k + ": fiber index does not match the tensor");
 }
 
-DBuf* upload_fptr(const FiberIndex& fib, cudaStream_t st) {
+uint32_t* upload_fptr(Session& S, const FiberIndex& fib) {
   std::vector<uint32_t> f(fib.fptr.size());
   for (size_t i = 0; i < f.size(); ++i) {
     if (fib.fptr[i] >= (size_t{1} << 32))
       throw std::overflow_error("spten::gpu: fiber offsets exceed the u32 device range");
     f[i] = static_cast<uint32_t>(fib.fptr[i]);
   }
-  auto* b = new DBuf(f.size() * 4, st);
-  cuda(cudaMemcpyAsync(b->p, f.data(), f.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
-  cuda(cudaStreamSynchronize(st), "sync");  // f is a temporary
-  return b;
+  auto* d = static_cast<uint32_t*>(S.buf(kAux, f.size() * 4));
+  S.upload(d, f.data(), f.size() * 4);
+  cuda(cudaStreamSynchronize(S.h2d), "sync");  // f is a temporary
+  return d;
 }
 
 }  // namespace
 
 SparseTensorCOO<float> ts(const SparseTensorCOO<float>& x, float s, ScalarOp op) {
   Session& S = session();
-  Owned dx(DevCoo::upload(x, S.stream));
-  DevCoo dz(x.order(), x.dims, x.nnz(), S.stream);
-  check(spt_ts_f32(S.ctx, &dx->d, s, static_cast<int>(op), &dz.d, 0, S.stream));
+  DevCoo dx = DevCoo::upload(S, kX, x);
+  S.uploads_done();
+  DevCoo dz(S, kZ, x.order(), x.dims, x.nnz());
+  check(spt_ts_f32(S.ctx, &dx.d, s, static_cast<int>(op), &dz.d, SPT_FLAG_ASYNC, S.stream));
   SparseTensorCOO<float> z;
   dz.download(z, dz.d, x.nnz());
+  check(spt_ctx_check(S.ctx, S.stream));
   flops::record(x.nnz());
   return z;
 }
@@ -192,12 +267,17 @@ SparseTensorCOO<float> tew_eq(const SparseTensorCOO<float>& x, const SparseTenso
   if (x.nnz() != y.nnz())
     throw std::invalid_argument("tew_eq: tensors must have identical nonzero counts");
   Session& S = session();
-  Owned dx(DevCoo::upload(x, S.stream));
-  Owned dy(DevCoo::upload(y, S.stream));
-  DevCoo dz(x.order(), x.dims, x.nnz(), S.stream);
-  check(spt_tew_eq_f32(S.ctx, &dx->d, &dy->d, static_cast<int>(op), &dz.d, 0, S.stream));
+  DevCoo dx = DevCoo::upload(S, kX, x);
+  DevCoo dy = DevCoo::upload(S, kY, y);
+  S.uploads_done();
+  DevCoo dz(S, kZ, x.order(), x.dims, x.nnz());
+  // data-dependent errors (pattern mismatch, stored-zero divisor) are raised
+  // by spt_ctx_check before the result is handed out
+  check(spt_tew_eq_f32(S.ctx, &dx.d, &dy.d, static_cast<int>(op), &dz.d, SPT_FLAG_ASYNC,
+                       S.stream));
   SparseTensorCOO<float> z;
   dz.download(z, dz.d, x.nnz());
+  check(spt_ctx_check(S.ctx, S.stream));
   flops::record(x.nnz());
   return z;
 }
@@ -211,25 +291,26 @@ SparseTensorCOO<float> tew(SparseTensorCOO<float>& x, SparseTensorCOO<float>& y,
   if (!x.coalesced || !y.coalesced)
     throw std::invalid_argument("tew: both inputs must be coalesced");
   Session& S = session();
-  Owned dx(DevCoo::upload(x, S.stream));
-  Owned dy(DevCoo::upload(y, S.stream));
+  DevCoo dx = DevCoo::upload(S, kX, x);
+  DevCoo dy = DevCoo::upload(S, kY, y);
+  S.uploads_done();
   // unify_tew_sort, P/src/kernel_detail.hpp:88-95: sort both ascending in
   // place unless they already share an order (and hand the sorted operands
   // back, as the reference's non-const references do).
   if (!(x.sort_order && y.sort_order && *x.sort_order == *y.sort_order)) {
     std::vector<uint32_t> asc(x.order());
     for (unsigned m = 0; m < x.order(); ++m) asc[m] = m;
-    check(spt_sort_f32(S.ctx, &dx->d, asc.data(), 0, S.stream));
-    check(spt_sort_f32(S.ctx, &dy->d, asc.data(), 0, S.stream));
-    dx->download(x, dx->d, x.nnz());
-    dy->download(y, dy->d, y.nnz());
+    check(spt_sort_f32(S.ctx, &dx.d, asc.data(), 0, S.stream));
+    check(spt_sort_f32(S.ctx, &dy.d, asc.data(), 0, S.stream));
+    dx.download(x, dx.d, x.nnz());
+    dy.download(y, dy.d, y.nnz());
   }
   const size_t cap = op == ElemOp::mul ? std::min(x.nnz(), y.nnz()) : x.nnz() + y.nnz();
   std::vector<Index> dims(x.order());
   for (unsigned m = 0; m < x.order(); ++m) dims[m] = std::max(x.dims[m], y.dims[m]);
-  DevCoo dz(x.order(), dims, cap, S.stream);
+  DevCoo dz(S, kZ, x.order(), dims, cap);
   uint64_t nz = 0;
-  check(spt_tew_f32(S.ctx, &dx->d, &dy->d, static_cast<int>(op), &dz.d, cap, &nz, nullptr, 0,
+  check(spt_tew_f32(S.ctx, &dx.d, &dy.d, static_cast<int>(op), &dz.d, cap, &nz, nullptr, 0,
                     S.stream));
   SparseTensorCOO<float> z;
   dz.download(z, dz.d, nz);
@@ -244,16 +325,16 @@ SparseTensorCOO<float> ttv(const SparseTensorCOO<float>& x, const DenseVector<fl
   if (v.len() != x.dims[mode])
     throw std::invalid_argument("ttv: vector length must match the mode dimension");
   Session& S = session();
-  Owned dx(DevCoo::upload(x, S.stream));
-  std::unique_ptr<DBuf> df(upload_fptr(fib, S.stream));
-  DBuf dv(v.len() * 4, S.stream);
-  if (v.len()) cuda(cudaMemcpyAsync(dv.p, v.data.data(), v.len() * 4, cudaMemcpyHostToDevice, S.stream), "H2D");
+  DevCoo dx = DevCoo::upload(S, kX, x);
+  uint32_t* df = upload_fptr(S, fib);
+  auto* dv = static_cast<float*>(S.buf(kAux2, v.len() * 4));
+  S.upload(dv, v.data.data(), v.len() * 4);
+  S.uploads_done();
   std::vector<Index> od;
   for (unsigned d = 0; d < x.order(); ++d)
     if (d != mode) od.push_back(x.dims[d]);
-  DevCoo dz(x.order() - 1, od, fib.nfibs, S.stream);
-  check(spt_ttv_f32(S.ctx, &dx->d, dv.as<float>(), v.len(), mode, df->as<uint32_t>(), fib.nfibs,
-                    &dz.d, 0, S.stream));
+  DevCoo dz(S, kZ, x.order() - 1, od, fib.nfibs);
+  check(spt_ttv_f32(S.ctx, &dx.d, dv, v.len(), mode, df, fib.nfibs, &dz.d, 0, S.stream));
   SparseTensorCOO<float> z;
   dz.download(z, dz.d, fib.nfibs);
   flops::record(2 * x.nnz());
@@ -273,16 +354,15 @@ SparseTensorCOO<float> ttm(const SparseTensorCOO<float>& x, const DenseMatrix<fl
   const size_t R = u.cols;
   if (R == 0) throw std::invalid_argument("ttm: matrix must have at least one column");
   Session& S = session();
-  Owned dx(DevCoo::upload(x, S.stream));
-  std::unique_ptr<DBuf> df(upload_fptr(fib, S.stream));
-  DBuf du(u.data.size() * 4, S.stream);
-  if (!u.data.empty())
-    cuda(cudaMemcpyAsync(du.p, u.data.data(), u.data.size() * 4, cudaMemcpyHostToDevice, S.stream), "H2D");
+  DevCoo dx = DevCoo::upload(S, kX, x);
+  uint32_t* df = upload_fptr(S, fib);
+  auto* du = static_cast<float*>(S.buf(kAux2, u.data.size() * 4));
+  S.upload(du, u.data.data(), u.data.size() * 4);
+  S.uploads_done();
   std::vector<Index> od = x.dims;
   od[mode] = static_cast<Index>(R);
-  DevCoo dz(x.order(), od, fib.nfibs * R, S.stream);
-  check(spt_ttm_f32(S.ctx, &dx->d, du.as<float>(), u.rows, R, mode, df->as<uint32_t>(),
-                    fib.nfibs, &dz.d, 0, S.stream));
+  DevCoo dz(S, kZ, x.order(), od, fib.nfibs * R);
+  check(spt_ttm_f32(S.ctx, &dx.d, du, u.rows, R, mode, df, fib.nfibs, &dz.d, 0, S.stream));
   SparseTensorCOO<float> z;
   dz.download(z, dz.d, fib.nfibs * R);
   flops::record(2 * R * x.nnz());
@@ -294,10 +374,10 @@ SparseTensorCOO<float> ttm(const SparseTensorCOO<float>& x, const DenseMatrix<fl
   return ttm(x, u, mode, build_fiber_index(x, mode));
 }
 
-DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
-                          const std::vector<DenseMatrix<float>>& factors, unsigned mode,
-                          MttkrpStrategy strategy) {
-  // check_mttkrp_inputs, P/src/kernel_detail.hpp:153-174
+namespace {
+// check_mttkrp_inputs, P/src/kernel_detail.hpp:153-174; returns R
+size_t check_mttkrp(const SparseTensorCOO<float>& x,
+                    const std::vector<DenseMatrix<float>>& factors, unsigned mode) {
   const unsigned N = x.order();
   if (N < 2) throw std::invalid_argument("mttkrp: input must have order >= 2");
   if (mode >= N) throw std::invalid_argument("mttkrp: mode out of range");
@@ -313,42 +393,37 @@ DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
       throw std::invalid_argument("mttkrp: factor rows must match the mode dimension");
   }
   if (R == 0) throw std::invalid_argument("mttkrp: factor rank must be >= 1");
+  return R;
+}
+}  // namespace
+
+DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
+                          const std::vector<DenseMatrix<float>>& factors, unsigned mode,
+                          MttkrpStrategy strategy) {
+  const unsigned N = x.order();
+  const size_t R = check_mttkrp(x, factors, mode);
   Session& S = session();
-  Owned dx(DevCoo::upload(x, S.stream));
-  int strat = SPT_MTTKRP_ATOMIC;
-  if (strategy == MttkrpStrategy::privatize) {
-    strat = SPT_MTTKRP_SEGMENTED;
-    const bool leading = x.sort_order && (*x.sort_order)[0] == mode;
-    if (!leading) {  // mode-leading copy (device sort, bit-exact permutation)
-      std::vector<uint32_t> mo{mode};
-      for (unsigned d = 0; d < N; ++d)
-        if (d != mode) mo.push_back(d);
-      check(spt_sort_f32(S.ctx, &dx->d, mo.data(), 0, S.stream));
-    }
-  }
-  std::vector<DBuf*> fb;
+  DevCoo dx = DevCoo::upload(S, kX, x);
   std::vector<const float*> fp(N, nullptr);
   std::vector<uint64_t> rows(N, 0), cols(N, 0);
   for (unsigned d = 0; d < N; ++d) {
     if (d == mode) continue;
-    fb.push_back(new DBuf(factors[d].data.size() * 4, S.stream));
-    if (!factors[d].data.empty())
-      cuda(cudaMemcpyAsync(fb.back()->p, factors[d].data.data(), factors[d].data.size() * 4,
-                           cudaMemcpyHostToDevice, S.stream), "H2D");
-    fp[d] = fb.back()->as<float>();
+    auto* f = static_cast<float*>(S.buf(kF + d, factors[d].data.size() * 4));
+    S.upload(f, factors[d].data.data(), factors[d].data.size() * 4);
+    fp[d] = f;
     rows[d] = factors[d].rows;
     cols[d] = factors[d].cols;
   }
+  S.uploads_done();
   DenseMatrix<float> out(x.dims[mode], R);
-  DBuf dout(out.data.size() * 4, S.stream);
-  int st = spt_mttkrp_f32(S.ctx, &dx->d, fp.data(), rows.data(), cols.data(), mode,
-                          dout.as<float>(), strat, 0, S.stream);
-  if (st == SPT_OK && !out.data.empty())
-    cuda(cudaMemcpyAsync(out.data.data(), dout.p, out.data.size() * 4, cudaMemcpyDeviceToHost,
-                         S.stream), "D2H");
-  if (st == SPT_OK) cuda(cudaStreamSynchronize(S.stream), "sync");
-  for (auto* b : fb) delete b;
-  check(st);
+  auto* dout = static_cast<float*>(S.buf(kOut, out.data.size() * 4));
+  // privatize (the reference's deterministic strategy) -> AUTO: the segmented
+  // kernel on a mode-leading input, else a device-side plan / sorted copy;
+  // atomic -> vector red.global.add
+  const int strat = strategy == MttkrpStrategy::atomic ? SPT_MTTKRP_ATOMIC : SPT_MTTKRP_AUTO;
+  check(spt_mttkrp_f32(S.ctx, &dx.d, fp.data(), rows.data(), cols.data(), mode, dout, strat, 0,
+                       S.stream));
+  S.download(out.data.data(), dout, out.data.size() * 4);
   flops::record(static_cast<std::uint64_t>(x.nnz()) * N * R);
   return out;
 }
@@ -369,23 +444,25 @@ void sort_lexicographic(SparseTensorCOO<float>& t, std::span<const unsigned> mod
     seen[d] = true;
   }
   Session& S = session();
-  Owned dt(DevCoo::upload(t, S.stream));
+  DevCoo dt = DevCoo::upload(S, kX, t);
+  S.uploads_done();
   std::vector<uint32_t> mo(mode_order.begin(), mode_order.end());
-  check(spt_sort_f32(S.ctx, &dt->d, mo.data(), 0, S.stream));
-  dt->download(t, dt->d, t.nnz());
+  check(spt_sort_f32(S.ctx, &dt.d, mo.data(), 0, S.stream));
+  dt.download(t, dt.d, t.nnz());
 }
 
 SparseTensorCOO<float> coalesce(const SparseTensorCOO<float>& t) {
   Session& S = session();
-  Owned dt(DevCoo::upload(t, S.stream));
+  DevCoo dt = DevCoo::upload(S, kX, t);
+  S.uploads_done();
   if (!t.sort_order) {
     std::vector<uint32_t> asc(t.order());
     for (unsigned m = 0; m < t.order(); ++m) asc[m] = m;
-    check(spt_sort_f32(S.ctx, &dt->d, asc.data(), 0, S.stream));
+    check(spt_sort_f32(S.ctx, &dt.d, asc.data(), 0, S.stream));
   }
-  DevCoo dz(t.order(), t.dims, t.nnz(), S.stream);
+  DevCoo dz(S, kZ, t.order(), t.dims, t.nnz());
   uint64_t n = 0;
-  check(spt_coalesce_f32(S.ctx, &dt->d, &dz.d, &n, nullptr, 0, S.stream));
+  check(spt_coalesce_f32(S.ctx, &dt.d, &dz.d, &n, nullptr, 0, S.stream));
   SparseTensorCOO<float> z;
   dz.download(z, dz.d, n);
   return z;
@@ -398,18 +475,53 @@ FiberIndex build_fiber_index(const SparseTensorCOO<float>& t, unsigned mode) {
     throw std::invalid_argument(
         "build_fiber_index: tensor must be sorted with the target mode as the last key");
   Session& S = session();
-  Owned dt(DevCoo::upload(t, S.stream));
-  DBuf fptr((t.nnz() + 1) * 4, S.stream);
+  DevCoo dt = DevCoo::upload(S, kX, t);
+  S.uploads_done();
+  auto* fptr = static_cast<uint32_t*>(S.buf(kAux, (t.nnz() + 1) * 4));
   uint64_t nf = 0;
-  check(spt_fiber_index(S.ctx, &dt->d, mode, fptr.as<uint32_t>(), &nf, nullptr, 0, S.stream));
+  check(spt_fiber_index(S.ctx, &dt.d, mode, fptr, &nf, nullptr, 0, S.stream));
   std::vector<uint32_t> f(nf + 1);
-  cuda(cudaMemcpyAsync(f.data(), fptr.p, (nf + 1) * 4, cudaMemcpyDeviceToHost, S.stream), "D2H");
-  cuda(cudaStreamSynchronize(S.stream), "sync");
+  S.download(f.data(), fptr, (nf + 1) * 4);
   FiberIndex fib;
   fib.mode = mode;
   fib.nfibs = nf;
   fib.fptr.assign(f.begin(), f.end());
   return fib;
 }
+
+// ---- par:: twins (P/include/spten/kernels_par.hpp:35-72) --------------------
+namespace par {
+SparseTensorCOO<float> tew_eq(const SparseTensorCOO<float>& x, const SparseTensorCOO<float>& y,
+                              ElemOp op, int) {
+  return gpu::tew_eq(x, y, op);
+}
+SparseTensorCOO<float> tew(SparseTensorCOO<float>& x, SparseTensorCOO<float>& y, ElemOp op, int) {
+  return gpu::tew(x, y, op);
+}
+SparseTensorCOO<float> ts(const SparseTensorCOO<float>& x, float s, ScalarOp op, int) {
+  return gpu::ts(x, s, op);
+}
+SparseTensorCOO<float> ttv(const SparseTensorCOO<float>& x, const DenseVector<float>& v,
+                           unsigned mode, const FiberIndex& fib, int) {
+  return gpu::ttv(x, v, mode, fib);
+}
+SparseTensorCOO<float> ttv(const SparseTensorCOO<float>& x, const DenseVector<float>& v,
+                           unsigned mode, int) {
+  return gpu::ttv(x, v, mode);
+}
+SparseTensorCOO<float> ttm(const SparseTensorCOO<float>& x, const DenseMatrix<float>& u,
+                           unsigned mode, const FiberIndex& fib, int) {
+  return gpu::ttm(x, u, mode, fib);
+}
+SparseTensorCOO<float> ttm(const SparseTensorCOO<float>& x, const DenseMatrix<float>& u,
+                           unsigned mode, int) {
+  return gpu::ttm(x, u, mode);
+}
+DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
+                          const std::vector<DenseMatrix<float>>& factors, unsigned mode, int,
+                          MttkrpStrategy strategy) {
+  return gpu::mttkrp(x, factors, mode, strategy);
+}
+}  // namespace par
 
 }  // namespace spten::gpu

@@ -16,6 +16,7 @@
 #include "spten/flop_counter.hpp"
 #include "spten/gpu.hpp"
 #include "spten/io.hpp"
+#include "spten/kernels_par.hpp"
 #include "spten/kernels_seq.hpp"
 #include "spten/tensor.hpp"
 
@@ -186,8 +187,12 @@ void random_parity() {
     for (int op = 0; op < 4; ++op)
       CHECK(bit_identical(gpu::tew_eq(x, y, static_cast<ElemOp>(op)),
                           seq::tew_eq(x, y, static_cast<ElemOp>(op))));
-    for (auto sop : {ScalarOp::add, ScalarOp::mul})
+    for (auto sop : {ScalarOp::add, ScalarOp::mul}) {
       CHECK(bit_identical(gpu::ts(x, 2.5f, sop), seq::ts(x, 2.5f, sop)));
+      // the par:: twins (P/include/spten/kernels_par.hpp:35-72): same results
+      CHECK(bit_identical(gpu::par::ts(x, 2.5f, sop, 4), spten::par::ts(x, 2.5f, sop, 4)));
+    }
+    CHECK(bit_identical(gpu::par::tew_eq(x, y, ElemOp::mul, 0), spten::par::tew_eq(x, y, ElemOp::mul, 0)));
     auto y2 = gen_synthetic<float>(x.dims, x.nnz(), rng());
     for (int op = 0; op < 3; ++op) {
       auto xa = x, ya = y2, xb = x, yb = y2;
@@ -232,6 +237,9 @@ void random_parity() {
     worst_mt = std::max(worst_mt, max_rel_diff(kr, kg));
     auto ka = gpu::mttkrp(x, fs, mode, MttkrpStrategy::atomic);
     worst_mt = std::max(worst_mt, max_rel_diff(kr, ka));
+    auto kp = gpu::par::mttkrp(x, fs, mode, 8, MttkrpStrategy::privatize);
+    worst_mt = std::max(worst_mt, max_rel_diff(kr, kp));
+    CHECK(same_structure(gpu::par::ttv(xs, v, mode, fg, 2), tr));
   }
   CHECK(worst_ttv <= 1e-5);
   CHECK(worst_ttm <= 1e-4);
