@@ -930,12 +930,11 @@ class C5(Workload):
 
     def e2e_arrays(self):
         """The full workload as host arrays for the C++ drop-in leg (x in its
-        mode-0 order, y's values, the factors); releases the device state."""
+        mode-0 order, y's values, the factors)."""
         arrays = {f"x_i{d}": _idx_np(self.x.indices[d]) for d in range(3)}
         arrays["x_val"] = _np(self.x.values)
         arrays["yval"] = _np(self.y.values)
         arrays.update({f"f{d}": _np(f) for d, f in enumerate(self.f)})
-        self.e2e_release()
         return arrays, {"dims": self.dims}
 
     def e2e_release(self):
@@ -1266,33 +1265,18 @@ def main_ours(args, world, rank, local):
     if not args.no_cpu and rank == 0 and world == 1 and hasattr(wl, "cpu_arrays"):
         cpu_in = wl.cpu_arrays()
 
-    e2e = None
+    e2e = e2e_dropin = None
     dropin = os.path.join(ROOT, "paper_1902_03317_b200", "host", "dropin_bench")
-    use_dropin = (not args.no_e2e and args.e2e_via == "dropin" and world == 1
-                  and hasattr(wl, "e2e_arrays") and os.path.exists(dropin))
-    if use_dropin:
-        # the C++ drop-in (spten::gpu::*) on host SparseTensorCOO data: every
-        # call uploads its operands, computes and returns its result by value
+    dropin_dir = None
+    if (not args.no_e2e and world == 1 and hasattr(wl, "e2e_arrays")
+            and os.path.exists(dropin)):
+        # inputs of the C++ drop-in leg (run after the pipeline, in its own process)
         arrays, meta = wl.e2e_arrays()
         base = "/dev/shm" if os.path.isdir("/dev/shm") else None
-        dd = tempfile.mkdtemp(prefix="spt_e2e_", dir=base)
-        try:
-            save_arrays(dd, arrays, meta)
-            del arrays
-            torch.cuda.empty_cache()
-            key = {"c1-mttkrp-ts": "c1", "c2-tew_eq-tew": "c2", "c5-mttkrp-tew_eq": "c5"}[wl.name]
-            out = subprocess.run([dropin, dd, key, str(max(2, min(args.steps, 3))), "1"],
-                                 capture_output=True, text=True, check=True).stdout
-        finally:
-            shutil.rmtree(dd, ignore_errors=True)
-        r = json.loads(out.strip().splitlines()[-1])
-        e2e = {"value": r["units_per_step"] / (r["ms_per_step"] / 1e3), "unit": "nnz/s",
-               "h2d_bytes_per_step": int(r["h2d_bytes_per_step"]),
-               "d2h_bytes_per_step": int(r["d2h_bytes_per_step"]),
-               "ms_per_step": r["ms_per_step"], "ms_median": r["ms_median"],
-               "path": r["path"] + " (paper_1902_03317_b200/host/dropin_bench)",
-               "timing": "host wall clock per step, one call per op, each returning by value"}
-    elif not args.no_e2e and hasattr(wl, "e2e_step"):
+        dropin_dir = tempfile.mkdtemp(prefix="spt_e2e_", dir=base)
+        save_arrays(dropin_dir, arrays, meta)
+        del arrays
+    if not args.no_e2e and hasattr(wl, "e2e_step"):
         # every rank runs its own host-buffer pipeline (its own PCIe link);
         # whole-job throughput over the slowest rank, like `value`
         host = wl.e2e_host(local)
@@ -1319,6 +1303,36 @@ def main_ours(args, world, rank, local):
                "h2d_bytes_per_step": world * h2d, "d2h_bytes_per_step": world * d2h,
                "ms_per_step": ms, "path": getattr(wl, "E2E_PATH", "ops.* -> C-ABI")}
         del host
+    if dropin_dir is not None:
+        # the C++ drop-in (spten::gpu::*) on host SparseTensorCOO data in its own
+        # process: every call uploads its operands from pageable std::vectors,
+        # computes and returns its result by value (the reference API's contract)
+        if hasattr(wl, "e2e_release"):
+            wl.e2e_release()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        ctx.trim()
+        try:
+            key = {"c1-mttkrp-ts": "c1", "c2-tew_eq-tew": "c2", "c5-mttkrp-tew_eq": "c5"}[wl.name]
+            env = {k: v for k, v in os.environ.items() if k not in ("OMP_PROC_BIND", "OMP_PLACES")}
+            r = subprocess.run([dropin, dropin_dir, key, str(max(2, min(args.steps, 3))), "1"],
+                               capture_output=True, text=True, env=env)
+            res = json.loads(r.stdout.strip().splitlines()[-1])
+            if "error" in res:
+                e2e_dropin = {"value": None, "error": res["error"]}
+            else:
+                e2e_dropin = {"value": res["units_per_step"] / (res["ms_per_step"] / 1e3),
+                              "unit": "nnz/s",
+                              "h2d_bytes_per_step": int(res["h2d_bytes_per_step"]),
+                              "d2h_bytes_per_step": int(res["d2h_bytes_per_step"]),
+                              "ms_per_step": res["ms_per_step"], "ms_median": res["ms_median"],
+                              "path": res["path"] + " (paper_1902_03317_b200/host/dropin_bench)",
+                              "timing": "host wall clock per step; one call per op, operands "
+                                        "uploaded from pageable vectors, results by value"}
+        except (OSError, ValueError, IndexError, KeyError) as err:
+            e2e_dropin = {"value": None, "error": str(err)}
+        finally:
+            shutil.rmtree(dropin_dir, ignore_errors=True)
 
     cpu = None
     if cpu_in is not None:
@@ -1341,7 +1355,7 @@ def main_ours(args, world, rank, local):
                 "config": wl.config(),
                 "timing": {"l2": "inputs > L2 and L2 flushed before every op",
                            "clock": "CUDA events per op on the launch stream, max over ranks"},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
                 "gpu_launches": gpu_launches,
                 "clocks": clk, "ops": ops_out,
                 "preprocess_s": getattr(wl, "preprocess", {})}
@@ -1367,9 +1381,6 @@ def main():
     ap.add_argument("--seed", type=int, default=20190210)
     ap.add_argument("--scale", type=float, default=1.0, help="nnz scale (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-via", default="dropin", choices=["dropin", "python"],
-                    help="e2e through the C++ drop-in (spten::gpu::*, host SparseTensorCOO "
-                         "data) or the Python ops.* pipeline with pinned buffers")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--prep-cpu", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--report", default=None,

@@ -96,6 +96,10 @@ SPT_API const char* spt_last_error(void);
 /* Create a context on `device` (cudaSetDevice is called). */
 SPT_API int spt_ctx_create(int device, spt_ctx** out);
 SPT_API void spt_ctx_destroy(spt_ctx* ctx);
+/* Hand back the context's cached device memory (sort scratch, look-back
+ * state, the L2 flush buffer, its private pool of temporaries); they grow
+ * again on demand. Synchronises the device. */
+SPT_API int spt_ctx_trim(spt_ctx* ctx);
 /* Number of kernels this context launched so far (evidence counter). */
 SPT_API uint64_t spt_ctx_launches(const spt_ctx* ctx);
 /* Deferred error check for calls made with SPT_FLAG_ASYNC: synchronises the

@@ -88,6 +88,7 @@ _SIGNATURES = {
     "spt_last_error": ([], ctypes.c_char_p),
     "spt_ctx_create": ([_I, ctypes.POINTER(_P)], _I),
     "spt_ctx_destroy": ([_P], None),
+    "spt_ctx_trim": ([_P], _I),
     "spt_ctx_launches": ([_P], _U64),
     "spt_ctx_check": ([_P, _P], _I),
     "spt_ts_f32": ([_P, _PCOO, ctypes.c_float, _I, _PCOO, ctypes.c_uint, _P], _I),
@@ -175,3 +176,7 @@ class Context:
 
     def launches(self) -> int:
         return int(load().spt_ctx_launches(self.handle))
+
+    def trim(self) -> None:
+        """Release the context's cached device memory (spt_ctx_trim)."""
+        check(load().spt_ctx_trim(self.handle))

@@ -203,14 +203,17 @@ int spt_ctx_create(int device, spt_ctx** out) {
   SPT_CUDA(cudaMalloc(&c->d_tile_ctr, 4 * sizeof(unsigned long long)));
   SPT_CUDA(cudaMemset(c->d_tile_ctr, 0, 4 * sizeof(unsigned long long)));
   SPT_CUDA(cudaMallocHost(&c->h_pinned, 8 * sizeof(unsigned long long)));
-  // Stream-ordered temporaries (sort permutations) come from the device's
-  // default pool; keep its freed memory mapped instead of trimming it at every
-  // synchronisation (an unmap/remap of tens of MB per call otherwise).
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t keep = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
+  // Stream-ordered temporaries (sort permutations, plan copies) come from a
+  // private pool that keeps its freed memory mapped (no unmap/remap of tens
+  // of MB per call); spt_ctx_trim hands it back. The device's default pool
+  // -- the caller's -- is left alone.
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  SPT_CUDA(cudaMemPoolCreate(&c->pool, &props));
+  uint64_t keep = ~0ull;
+  SPT_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
   *out = c;
   return SPT_OK;
 }
@@ -227,7 +230,31 @@ void spt_ctx_destroy(spt_ctx* c) {
   cudaFree(c->d_status64);
   cudaFree(c->l2buf);
   cudaFreeHost(c->h_pinned);
+  if (c->pool) cudaMemPoolDestroy(c->pool);
   delete c;
+}
+
+int spt_ctx_trim(spt_ctx* c) {
+  if (!c) return spt::set_error(SPT_EINVAL, "spt_ctx_trim: null context");
+  SPT_CUDA(cudaSetDevice(c->device));
+  SPT_CUDA(cudaDeviceSynchronize());
+  cudaFree(c->scratch);
+  c->scratch = nullptr;
+  c->scratch_bytes = 0;
+  cudaFree(c->d_status);
+  c->d_status = nullptr;
+  c->status_cap = 0;
+  cudaFree(c->d_payload);
+  c->d_payload = nullptr;
+  c->payload_cap = 0;
+  cudaFree(c->d_status64);
+  c->d_status64 = nullptr;
+  c->status64_cap = 0;
+  cudaFree(c->l2buf);
+  c->l2buf = nullptr;
+  c->l2buf_bytes = 0;
+  SPT_CUDA(cudaMemPoolTrimTo(c->pool, 0));
+  return SPT_OK;
 }
 
 uint64_t spt_ctx_launches(const spt_ctx* c) { return c ? c->launches : 0; }

@@ -219,16 +219,16 @@ extern "C" int spt_gen_coo_f32(spt_ctx* ctx, spt_coo* x, uint64_t seed, const do
     if (!md.zipf) continue;
     double* cdf;
     uint32_t* guide;
-    SPT_CUDA(cudaMallocAsync(&cdf, (size_t)md.dim * sizeof(double), st));
+    SPT_CUDA(spt::tmp_alloc(ctx, &cdf, (size_t)md.dim * sizeof(double), st));
     allocs.push_back(cdf);
-    SPT_CUDA(cudaMallocAsync(&guide, ((1u << kGuideBits) + 1) * sizeof(uint32_t), st));
+    SPT_CUDA(spt::tmp_alloc(ctx, &guide, ((1u << kGuideBits) + 1) * sizeof(uint32_t), st));
     allocs.push_back(guide);
     zipf_weights_kernel<<<spt::grid_for(md.dim, 256, 4096), 256, 0, st>>>(cdf, md.dim, s);
     SPT_LAUNCHED(ctx);
     size_t tb = 0;
     SPT_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, cdf, cdf, (int64_t)md.dim, st));
     void* tmp;
-    SPT_CUDA(cudaMallocAsync(&tmp, tb, st));
+    SPT_CUDA(spt::tmp_alloc(ctx, &tmp, tb, st));
     SPT_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, cdf, cdf, (int64_t)md.dim, st));
     cudaFreeAsync(tmp, st);
     normalize_kernel<<<spt::grid_for(md.dim, 256, 4096), 256, 0, st>>>(cdf, md.dim);
@@ -264,10 +264,10 @@ extern "C" int spt_gen_coo_f32(spt_ctx* ctx, spt_coo* x, uint64_t seed, const do
       return spt::cuda_status(_e, #call);             \
     }                                                 \
   } while (0)
-    for (int d = 0; d < N; ++d) GEN_CUDA(cudaMallocAsync(&cand[d], M * 4, st));
-    GEN_CUDA(cudaMallocAsync(&perm, M * 4, st));
-    GEN_CUDA(cudaMallocAsync(&keep, M * 4, st));
-    GEN_CUDA(cudaMallocAsync(&pos, M * 4, st));
+    for (int d = 0; d < N; ++d) GEN_CUDA(spt::tmp_alloc(ctx, &cand[d], M * 4, st));
+    GEN_CUDA(spt::tmp_alloc(ctx, &perm, M * 4, st));
+    GEN_CUDA(spt::tmp_alloc(ctx, &keep, M * 4, st));
+    GEN_CUDA(spt::tmp_alloc(ctx, &pos, M * 4, st));
     for (int d = 0; d < N; ++d) dp.out[d] = cand[d];
     dp.M = M;
     draw_kernel<<<spt::grid_for(M, 256, ctx->num_sms * 16), 256, 0, st>>>(dp);
@@ -297,7 +297,7 @@ extern "C" int spt_gen_coo_f32(spt_ctx* ctx, spt_coo* x, uint64_t seed, const do
     ctx->launches++;
     size_t tb = 0;
     GEN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, keep, pos, (int64_t)M, st));
-    GEN_CUDA(cudaMallocAsync(&tmp, tb, st));
+    GEN_CUDA(spt::tmp_alloc(ctx, &tmp, tb, st));
     GEN_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, keep, pos, (int64_t)M, st));
     uint32_t last[2];
     GEN_CUDA(cudaMemcpyAsync(&last[0], pos + M - 1, 4, cudaMemcpyDeviceToHost, st));

@@ -37,6 +37,9 @@ struct spt_ctx {
   size_t status64_cap = 0;
   // Pinned host words for count read-back.
   unsigned long long* h_pinned = nullptr;
+  // Private stream-ordered pool for the library's temporaries (its release
+  // threshold is raised here only, never the device's default pool's).
+  cudaMemPool_t pool = nullptr;
   // L2 flush buffer.
   void* l2buf = nullptr;
   size_t l2buf_bytes = 0;
@@ -61,6 +64,12 @@ int check_coo(const spt_coo* t, const char* who, bool need_values = true);
 int sync_and_check(spt_ctx* ctx, cudaStream_t stream);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Stream-ordered temporaries from the context's private pool.
+template <typename T>
+inline cudaError_t tmp_alloc(spt_ctx* ctx, T** p, size_t bytes, cudaStream_t st) {
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, ctx->pool, st);
+}
 
 __host__ __device__ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

@@ -2001,7 +2001,7 @@ int mttkrp_sorted_copy(spt_ctx* ctx, const spt_coo* x, const float* const* d_fac
   const uint32_t N = x->order;
   const size_t ab = ((x->nnz * 4 + 255) / 256) * 256;
   char* mem = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&mem), ab * (N + 1), st) != cudaSuccess) {
+  if (spt::tmp_alloc(ctx, reinterpret_cast<void**>(&mem), ab * (N + 1), st) != cudaSuccess) {
     cudaGetLastError();
     return set_error(SPT_ENOMEM, "mttkrp: out of device memory for a sorted copy");
   }

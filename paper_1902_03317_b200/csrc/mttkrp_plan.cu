@@ -600,7 +600,7 @@ int plan_select_hot(spt_ctx* ctx, spt_mttkrp_plan* pl, const uint32_t* row, uint
     maxd = std::max(maxd, pl->dims[pl->lvl_mode[j]]);
   }
   uint32_t* hist = nullptr;
-  SPT_CUDA(cudaMallocAsync(&hist, hist_words * 4, st));
+  SPT_CUDA(spt::tmp_alloc(ctx, &hist, hist_words * 4, st));
   SPT_CUDA(cudaMemsetAsync(hist, 0, hist_words * 4, st));
   for (uint32_t j = 0; j < nm1; ++j) {
     L.p[j] = lvl[j];
@@ -620,7 +620,7 @@ int plan_select_hot(spt_ctx* ctx, spt_mttkrp_plan* pl, const uint32_t* row, uint
   }
   char* buf = nullptr;
   const size_t wb = align256((size_t)maxd * 4);
-  SPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), 3 * wb + align256(temp), st));
+  SPT_CUDA(spt::tmp_alloc(ctx, reinterpret_cast<void**>(&buf), 3 * wb + align256(temp), st));
   uint32_t* kalt = reinterpret_cast<uint32_t*>(buf);
   uint32_t* vcur = reinterpret_cast<uint32_t*>(buf + wb);
   uint32_t* valt = reinterpret_cast<uint32_t*>(buf + 2 * wb);
@@ -659,7 +659,7 @@ int plan_select_hot(spt_ctx* ctx, spt_mttkrp_plan* pl, const uint32_t* row, uint
   const uint32_t nsel = static_cast<uint32_t>(sel.size());
   if (nsel) {
     uint2* dsel = nullptr;
-    SPT_CUDA(cudaMallocAsync(&dsel, nsel * sizeof(uint2), st));
+    SPT_CUDA(spt::tmp_alloc(ctx, &dsel, nsel * sizeof(uint2), st));
     SPT_CUDA(cudaMemcpyAsync(dsel, sel.data(), nsel * sizeof(uint2), cudaMemcpyHostToDevice, st));
     SPT_CUDA(cudaMalloc(&pl->hot, pl->nhot * sizeof(uint2)));
     SPT_CUDA(cudaMemcpyAsync(pl->hot, dsel, pl->nhot * sizeof(uint2), cudaMemcpyDeviceToDevice,
@@ -696,7 +696,7 @@ int plan_build(spt_ctx* ctx, spt_mttkrp_plan* pl, const spt_coo* x, unsigned fla
   const uint32_t N = pl->N;
   const size_t ab = align256((x->nnz + 4) * 4);
   char* soa = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&soa), ab * (N + 1), st) != cudaSuccess) {
+  if (spt::tmp_alloc(ctx, reinterpret_cast<void**>(&soa), ab * (N + 1), st) != cudaSuccess) {
     cudaGetLastError();
     return spt::set_error(SPT_ENOMEM, "mttkrp_plan: out of device memory (%zu bytes)",
                           ab * (N + 1));

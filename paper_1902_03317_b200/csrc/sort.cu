@@ -324,10 +324,10 @@ int spt_sort_f32(spt_ctx* ctx, spt_coo* x, const uint32_t* mode_order, unsigned 
     // perm lives in its own allocation (sort_tuples uses the ctx scratch).
     uint32_t* perm = nullptr;
     uint32_t* tmp = nullptr;
-    SPT_CUDA(cudaMallocAsync(&perm, n * sizeof(uint32_t), st));
+    SPT_CUDA(spt::tmp_alloc(ctx, &perm, n * sizeof(uint32_t), st));
     int s = spt::sort_tuples(ctx, x, mode_order, perm, st);
     if (s == SPT_OK) {
-      cudaError_t e = cudaMallocAsync(&tmp, n * sizeof(uint32_t), st);
+      cudaError_t e = spt::tmp_alloc(ctx, &tmp, n * sizeof(uint32_t), st);
       if (e != cudaSuccess) s = spt::cuda_status(e, "sort gather buffer");
     }
     if (s == SPT_OK) {

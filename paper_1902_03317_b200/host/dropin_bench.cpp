@@ -15,6 +15,7 @@
 #include <cstring>
 #include <fstream>
 #include <functional>
+#include <malloc.h>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -22,6 +23,7 @@
 #include "spten/gpu.hpp"
 
 using namespace spten;
+extern "C" double spten_gpu_copy_probe(const void* src, size_t n);
 
 namespace {
 
@@ -107,11 +109,28 @@ double now_ms() {
 
 }  // namespace
 
+int run(int argc, char** argv);
+
 int main(int argc, char** argv) {
+  try {
+    return run(argc, argv);
+  } catch (const std::exception& e) {
+    std::printf("{\"error\": \"%s\"}\n", e.what());
+    return 1;
+  }
+}
+
+int run(int argc, char** argv) {
   if (argc < 5) {
     std::fprintf(stderr, "usage: %s <dir> <c1|c2|c5> <steps> <warmup>\n", argv[0]);
     return 2;
   }
+  // The app's allocator policy (not the library's): the by-value outputs of
+  // the reference API are hundreds of MB; glibc would mmap each one afresh and
+  // fault every page in on its single-threaded zero-fill (~2.7 GB/s on the
+  // box). From the heap, with trimming off, freed outputs are reused.
+  mallopt(M_MMAP_MAX, 0);
+  mallopt(M_TRIM_THRESHOLD, -1);
   const std::string dir = argv[1], wl = argv[2];
   const int steps = std::atoi(argv[3]), warmup = std::atoi(argv[4]);
   const std::vector<Index> dims = read_dims(dir);
@@ -185,6 +204,13 @@ int main(int argc, char** argv) {
   } else {
     std::fprintf(stderr, "unknown workload %s\n", wl.c_str());
     return 2;
+  }
+  if (std::getenv("SPT_COPY_PROBE")) {
+    std::vector<char> fresh(size_t(256) << 20, 1);
+    std::fprintf(stderr, "copy probe: fresh %.1f GB/s, x.indices[0] %.1f GB/s, again %.1f GB/s\n",
+                 spten_gpu_copy_probe(fresh.data(), fresh.size()),
+                 spten_gpu_copy_probe(x.indices[0].data(), x.indices[0].size() * 4),
+                 spten_gpu_copy_probe(x.indices[0].data(), x.indices[0].size() * 4));
   }
   double up = 0, down = 0, chk = 0;
   for (int i = 0; i < warmup; ++i) step(up, down, chk);

@@ -8,7 +8,17 @@
 
 #include <cuda_runtime.h>
 
+#include <pthread.h>
+#include <sched.h>
+
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -48,16 +58,102 @@ inline void cuda(cudaError_t e, const char* what) {
 // into a pinned buffer (several threads) while the DMA engine moves chunk k-1.
 constexpr size_t kChunk = size_t(32) << 20;  // bytes per pinned bounce buffer
 
-void par_memcpy(void* dst, const void* src, size_t n) {
-  constexpr size_t kPiece = size_t(1) << 20;
-  const long pieces = static_cast<long>((n + kPiece - 1) / kPiece);
-#pragma omp parallel for schedule(static) num_threads(8) if (pieces > 1)
-  for (long i = 0; i < pieces; ++i) {
-    const size_t o = static_cast<size_t>(i) * kPiece;
-    std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
-                std::min(kPiece, n - o));
+// SPT_DROPIN_TRACE=1: per-phase host times of every call on stderr (tuning).
+struct Trace {
+  const bool on = std::getenv("SPT_DROPIN_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dropin] %-12s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
   }
-}
+};
+
+// Host copies between the caller's pageable vectors and the pinned buffers,
+// split over a small persistent thread pool (std::thread: independent of the
+// caller's OpenMP settings -- OMP_PROC_BIND=close, set for the reference's
+// kernels, packed OpenMP copies onto a few cores at ~8 GB/s).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool p;
+    return p;
+  }
+  void memcpy(void* dst, const void* src, size_t n) {
+    constexpr size_t kPiece = size_t(1) << 20;
+    if (n <= 2 * kPiece || workers_.empty()) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(m_);
+    dst_ = static_cast<char*>(dst);
+    src_ = static_cast<const char*>(src);
+    n_ = n;
+    next_.store(0);
+    busy_ = static_cast<int>(workers_.size());
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    work();
+    lk.lock();
+    done_.wait(lk, [&] { return busy_ == 0; });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    for (unsigned i = 0; i < std::min(hw, 8u) - 1; ++i)
+      workers_.emplace_back([this, hw] {
+        // a thread inherits its creator's CPU mask: a caller whose OpenMP
+        // runtime pinned the main thread (OMP_PROC_BIND) would put every
+        // copy worker on that one core
+        cpu_set_t all;
+        CPU_ZERO(&all);
+        for (unsigned c = 0; c < hw && c < CPU_SETSIZE; ++c) CPU_SET(c, &all);
+        pthread_setaffinity_np(pthread_self(), sizeof all, &all);
+        uint64_t seen = 0;
+        while (true) {
+          {
+            std::unique_lock<std::mutex> lk(m_);
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+            if (stop_) return;
+          }
+          work();
+          std::lock_guard<std::mutex> lk(m_);
+          if (--busy_ == 0) done_.notify_one();
+        }
+      });
+  }
+  void work() {
+    constexpr size_t kPiece = size_t(1) << 20;
+    for (size_t o; (o = next_.fetch_add(kPiece)) < n_;)
+      std::memcpy(dst_ + o, src_ + o, std::min(kPiece, n_ - o));
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  uint64_t gen_ = 0;
+  int busy_ = 0;
+  bool stop_ = false;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t n_ = 0;
+  std::atomic<size_t> next_{0};
+};
+
+void par_memcpy(void* dst, const void* src, size_t n) { CopyPool::get().memcpy(dst, src, n); }
 
 struct Session {
   int device = -1;
@@ -103,14 +199,19 @@ struct Session {
   }
 
   // Pageable host -> device through the pinned ring (stream h2d).
+  double t_wait = 0, t_copy = 0;  // SPT_DROPIN_TRACE accounting
   void upload(void* dst, const void* src, size_t n) {
     if (!n) return;
     for (size_t o = 0; o < n; o += kChunk) {
       const size_t c = std::min(kChunk, n - o);
       const int k = next;
       next ^= 1;
+      const auto t0 = std::chrono::steady_clock::now();
       cuda(cudaEventSynchronize(ev[k]), "sync");  // the DMA out of this buffer is done
+      const auto t1 = std::chrono::steady_clock::now();
       par_memcpy(pin[k], static_cast<const char*>(src) + o, c);
+      t_wait += std::chrono::duration<double, std::milli>(t1 - t0).count();
+      t_copy += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
       cuda(cudaMemcpyAsync(static_cast<char*>(dst) + o, pin[k], c, cudaMemcpyHostToDevice, h2d),
            "H2D");
       cuda(cudaEventRecord(ev[k], h2d), "event");
@@ -204,9 +305,12 @@ struct DevCoo {
   }
   // Copy the first n entries and the metadata of descriptor `meta` back.
   void download(SparseTensorCOO<float>& t, const spt_coo& meta, size_t n) const {
+    Trace tr;
     t.dims.assign(meta.dims, meta.dims + meta.order);
-    t.indices.assign(meta.order, std::vector<Index>(n));
+    t.indices.resize(meta.order);  // by-value outputs (the reference API): one
+    for (auto& ix : t.indices) ix.resize(n);  // value-init pass each, no copies
     t.values.resize(n);
+    tr.mark("  alloc");
     for (unsigned m = 0; m < meta.order; ++m) S->download(t.indices[m].data(), meta.idx[m], n * 4);
     S->download(t.values.data(), meta.val, n * 4);
     if (meta.has_sort_order)
@@ -266,18 +370,26 @@ SparseTensorCOO<float> tew_eq(const SparseTensorCOO<float>& x, const SparseTenso
     throw std::invalid_argument("tew_eq: tensors must have identical dimensions");
   if (x.nnz() != y.nnz())
     throw std::invalid_argument("tew_eq: tensors must have identical nonzero counts");
+  Trace tr;
   Session& S = session();
+  tr.mark("session");
+  S.t_wait = S.t_copy = 0;
   DevCoo dx = DevCoo::upload(S, kX, x);
   DevCoo dy = DevCoo::upload(S, kY, y);
   S.uploads_done();
+  tr.mark("upload");
+  if (tr.on) std::fprintf(stderr, "[dropin]   wait %.3f copy %.3f ms\n", S.t_wait, S.t_copy);
   DevCoo dz(S, kZ, x.order(), x.dims, x.nnz());
   // data-dependent errors (pattern mismatch, stored-zero divisor) are raised
   // by spt_ctx_check before the result is handed out
   check(spt_tew_eq_f32(S.ctx, &dx.d, &dy.d, static_cast<int>(op), &dz.d, SPT_FLAG_ASYNC,
                        S.stream));
+  tr.mark("launch");
   SparseTensorCOO<float> z;
   dz.download(z, dz.d, x.nnz());
+  tr.mark("download");
   check(spt_ctx_check(S.ctx, S.stream));
+  tr.mark("check");
   flops::record(x.nnz());
   return z;
 }
@@ -525,3 +637,14 @@ DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
 }  // namespace par
 
 }  // namespace spten::gpu
+
+// Tuning hook (tune/ only): GB/s of the drop-in's host copy from `src` into
+// its pinned upload buffer.
+extern "C" double spten_gpu_copy_probe(const void* src, size_t n) {
+  using namespace spten::gpu;
+  Session& S = session();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (size_t o = 0; o < n; o += kChunk)
+    par_memcpy(S.pin[0], static_cast<const char*>(src) + o, std::min(kChunk, n - o));
+  return n / std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / 1e9;
+}
