@@ -210,6 +210,26 @@ SPT_API int spt_mttkrp_plan_info(const spt_mttkrp_plan* plan, uint32_t* level_mo
                                  uint32_t* hot_per_level, uint32_t* nhot);
 SPT_API void spt_mttkrp_plan_destroy(spt_mttkrp_plan* plan);
 
+/* ---- multi-GPU MTTKRP (one process, one context per device) ---------------
+ * SURVEY.md 8(e); the reference's analogue is the private-buffer reduction of
+ * par::mttkrp (P/src/kernels_par.cpp:290-319). spt_row_aligned_cuts splits x
+ * (sorted with `mode` leading) into `parts` entry ranges cut at row starts
+ * (entry_cuts, parts+1 host u64) and the output row block each owns (row_lo,
+ * parts+1 host u32: [row_lo[k], row_lo[k+1]), covering [0, dims[mode])). */
+SPT_API int spt_row_aligned_cuts(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint32_t parts,
+                                 uint64_t* entry_cuts, uint32_t* row_lo, void* stream);
+/* Device k (ctxs[k], one per distinct device) holds shards[k] -- entries
+ * [entry_cuts[k], entry_cuts[k+1]) of that sorted x -- and its factors
+ * d_factors[k*order + d]; it computes its rows exactly into its own full
+ * dims[mode] x R buffer d_out[k], then one NCCL group of in-place broadcasts
+ * (root k: rows [row_lo[k], row_lo[k+1])) leaves the whole result in every
+ * d_out[k]: (G-1)/G of the output per device, no cross-device sums. NCCL is
+ * loaded on first use; ndev == 1 needs none. Synchronises every stream. */
+SPT_API int spt_mttkrp_f32_multi(int ndev, spt_ctx* const* ctxs, const spt_coo* shards,
+                                 const uint32_t* row_lo, const float* const* d_factors,
+                                 const uint64_t* rows, const uint64_t* cols, uint32_t mode,
+                                 float* const* d_out, void* const* streams);
+
 /* ---- seeded synthetic generator (bench / test input, not a reference path) --
  * Draws `nnz` distinct tuples: per-mode index distribution `dist[d]`
  * (0 = uniform, s>0 = Zipf(s) over a seeded permutation of ids), duplicates

@@ -215,3 +215,47 @@ def mttkrp_row_allgather(x_shard, factors: Sequence, mode: int, rows: int, rank_
     for r, (a, b) in enumerate(blocks):
         out[a:b] = recv[r * B: r * B + (b - a)]
     return out
+
+
+def mttkrp_multi(x_sorted, factors_per_dev: Sequence[Sequence[torch.Tensor]], mode: int,
+                 R: int) -> list:
+    """Single-process multi-GPU MTTKRP through the C-ABI (spt_row_aligned_cuts
+    + spt_mttkrp_f32_multi): x_sorted (mode leading) lives on device 0, its
+    row-aligned shards are copied to the devices of `factors_per_dev`, every
+    device gets the whole dims[mode] x R result. Returns the per-device outputs."""
+    import ctypes
+    from . import _lib
+    from .coo import DeviceCOO
+    lib = _lib.load()
+    G = len(factors_per_dev)
+    N = x_sorted.order
+    ctx0 = _lib.Context.get(x_sorted.device.index or 0)
+    cuts = (ctypes.c_uint64 * (G + 1))()
+    rlo = (ctypes.c_uint32 * (G + 1))()
+    d = x_sorted.descriptor()
+    _lib.check(lib.spt_row_aligned_cuts(ctx0.handle, ctypes.byref(d), mode, G, cuts, rlo,
+                                        torch.cuda.current_stream(x_sorted.device).cuda_stream))
+    ctxs = (ctypes.c_void_p * G)()
+    shards = (_lib.SptCoo * G)()
+    fps = (ctypes.c_void_p * (G * N))()
+    outs, streams, keep = [], (ctypes.c_void_p * G)(), []
+    rows = (ctypes.c_uint64 * N)(*[x_sorted.dims[k] for k in range(N)])
+    cols = (ctypes.c_uint64 * N)(*[R] * N)
+    outp = (ctypes.c_void_p * G)()
+    for k, fs in enumerate(factors_per_dev):
+        dev = fs[0].device if fs[0] is not None else fs[1].device
+        sh = slice_coo(x_sorted, int(cuts[k]), int(cuts[k + 1]))
+        sh = DeviceCOO(list(sh.dims), [i.to(dev) for i in sh.indices], sh.values.to(dev),
+                       list(sh.sort_order), True)
+        keep.append(sh)
+        ctxs[k] = _lib.Context.get(dev.index or 0).handle
+        shards[k] = sh.descriptor()
+        for j in range(N):
+            fps[k * N + j] = fs[j].data_ptr() if (j != mode and fs[j] is not None) else None
+        o = torch.empty((x_sorted.dims[mode], R), dtype=torch.float32, device=dev)
+        outs.append(o)
+        outp[k] = o.data_ptr()
+        streams[k] = torch.cuda.current_stream(dev).cuda_stream
+    _lib.check(lib.spt_mttkrp_f32_multi(G, ctxs, shards, rlo, fps, rows, cols, mode, outp,
+                                        streams))
+    return outs
