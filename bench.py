@@ -347,6 +347,70 @@ def run_cpu_leg(name, arrays, meta, steps, warmup, seq=True) -> dict:
     return res
 
 
+def crosscheck(name, arrays, meta, k=200_000) -> dict:
+    """The reference bench's crosscheck (P/src/bench.cpp:226-229, :346-443)
+    for the GPU rows: each op of the workload on the first k entries of the
+    CPU sample, GPU (this library) against the reference's seq:: kernels,
+    with the reference's own rules -- bit-identical outputs, MTTKRP
+    max_rel_diff <= 1e-4 at f32 (P/src/bench.cpp:282). Returns op -> pass/fail."""
+    import torch
+    from oracle.oracle import HostTensor, Ref
+    from paper_1902_03317_b200 import ops
+    from paper_1902_03317_b200.coo import HostCOO
+    ref = Ref()
+    dims = meta["dims"]
+    N = len(dims)
+
+    def dev(t):
+        return HostCOO(t.dims, t.indices, t.values, t.sort_order, t.coalesced).to_device(0)
+
+    def same(g, r):
+        g = g.to_host()
+        return (list(g.dims) == list(r.dims) and
+                all(np.array_equal(a, b) for a, b in zip(g.indices, r.indices)) and
+                np.array_equal(g.values.view(np.uint32), r.values.view(np.uint32)))
+
+    def rel(a, b):
+        den = np.maximum(np.abs(a), np.abs(b))
+        return float(np.max(np.where(den > 0, np.abs(a - b) / np.where(den > 0, den, 1), 0)))
+
+    out = {}
+    if name in ("c1", "c2"):
+        x = _host_tensor(arrays, "x_", dims, meta["sort_order"], k)
+        dx = dev(x)
+        if name == "c1":
+            for op, nm in ((0, "ts_add"), (1, "ts_mul")):
+                out[nm] = "pass" if same(ops.ts(dx, 2.5, op), ref.ts(x, 2.5, op)) else "fail"
+            fs = [arrays[f"f{d}"] for d in range(N)]
+            g = ops.mttkrp(dx, [torch.from_numpy(f).cuda() for f in fs], 0).cpu().numpy()
+            out["mttkrp_m0"] = "pass" if rel(g, ref.mttkrp(x, fs, 0)) <= 1e-4 else "fail"
+        else:
+            y = HostTensor(x.dims, x.indices, np.ascontiguousarray(arrays["yval"][:k]),
+                           x.sort_order, True)
+            dy = dev(y)
+            for op, nm in ((0, "tew_eq_add"), (1, "tew_eq_sub"), (2, "tew_eq_mul"),
+                           (3, "tew_eq_div")):
+                out[nm] = "pass" if same(ops.tew_eq(dx, dy, op), ref.tew_eq(x, y, op)) else "fail"
+            y2 = _host_tensor(arrays, "y2_", dims, meta["sort_order"], k)
+            for op, nm in ((0, "tew_add"), (2, "tew_mul")):
+                z, _, _, _ = ref.tew(x.copy(), y2.copy(), op)
+                out[nm] = "pass" if same(ops.tew(dev(x), dev(y2), op), z) else "fail"
+    elif name in ("c4", "c5"):
+        fs = [arrays[f"f{d}"] for d in range(N)]
+        tf = [torch.from_numpy(f).cuda() for f in fs]
+        for m in range(N):
+            x = _host_tensor(arrays, f"m{m}_", dims, meta["sort_orders"][m], k)
+            g = ops.mttkrp(dev(x), tf, m).cpu().numpy()
+            out[f"mttkrp_m{m}"] = "pass" if rel(g, ref.mttkrp(x, fs, m)) <= 1e-4 else "fail"
+        if name == "c5":
+            x = _host_tensor(arrays, "eq_", dims, meta["eq_sort_order"], k)
+            y = HostTensor(x.dims, x.indices, np.ascontiguousarray(arrays["eq_yval"][:k]),
+                           x.sort_order, True)
+            out["tew_eq_mul"] = ("pass" if same(ops.tew_eq(dev(x), dev(y), 2),
+                                                ref.tew_eq(x, y, 2)) else "fail")
+    return out
+
+
 def save_arrays(d, arrays, meta):
     os.makedirs(d, exist_ok=True)
     for k, a in arrays.items():
@@ -363,6 +427,13 @@ def load_arrays(d):
 
 # ===========================================================================
 # GPU workloads (torch + the C-ABI library)
+
+
+class _OpRecord:
+    """An Op's name and timings without its closures (which hold device state)."""
+
+    def __init__(self, op):
+        self.name, self.times, self.units = op.name, list(op.times), op.units
 
 
 class Op:
@@ -1260,7 +1331,8 @@ def main_ours(args, world, rank, local):
 
     # everything that needs the device-timed state before e2e may release it
     gpu_launches = int(sum(op.launches for op in wl.ops))
-    rows = report_rows(wl, wl.ops) if (args.report and rank == 0) else None
+    ops_snapshot = [_OpRecord(op) for op in wl.ops]  # the ops' timings outlive the device state
+    rows = report_rows(wl, ops_snapshot) if (args.report and rank == 0) else None
     cpu_in = None
     if not args.no_cpu and rank == 0 and world == 1 and hasattr(wl, "cpu_arrays"):
         cpu_in = wl.cpu_arrays()
@@ -1334,6 +1406,13 @@ def main_ours(args, world, rank, local):
         finally:
             shutil.rmtree(dropin_dir, ignore_errors=True)
 
+    if cpu_in is not None:
+        try:
+            wl.crosscheck = crosscheck(args.workload, cpu_in[0], cpu_in[1])
+        except Exception as e:  # reported, never silently replaced
+            wl.crosscheck = {"error": str(e)}
+        if args.report and rank == 0:
+            rows = report_rows(wl, ops_snapshot)
     cpu = None
     if cpu_in is not None:
         try:
@@ -1358,6 +1437,7 @@ def main_ours(args, world, rank, local):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
                 "gpu_launches": gpu_launches,
                 "clocks": clk, "ops": ops_out,
+                "crosscheck": getattr(wl, "crosscheck", None),
                 "preprocess_s": getattr(wl, "preprocess", {})}
         print(json.dumps(line))
         if rows is not None:
