@@ -298,6 +298,13 @@ def _cpu_leg(name, ref, arrays, meta, nthreads):
                                     hxt.sort_order, True))
             leg.add("tew_eq_mul", meta["sample_nnz"],
                     lambda v, nt: leg._run(leg.lib.ref_tew_eq, hx, hy, 2, v, nt))
+    elif name == "tns":
+        base = "/dev/shm" if os.path.isdir("/dev/shm") else None
+        fd, path = tempfile.mkstemp(suffix=".tns", dir=base)
+        with os.fdopen(fd, "wb") as fh:
+            fh.write(arrays["text"].tobytes())
+        leg.keep.append(("file", path))
+        leg.add("read_tns", meta["sample_nnz"], lambda v, nt: leg.ref.read_tns(path))
     elif name == "pre":
         from oracle.oracle import HostTensor
         t = _host_tensor(arrays, "x_", dims, None)
@@ -329,13 +336,16 @@ def run_cpu_leg(name, arrays, meta, steps, warmup, seq=True) -> dict:
         leg.step()
         t.append(time.perf_counter() - t0)
     units = leg.units()
+    for item in leg.keep:
+        if isinstance(item, tuple) and item[0] == "file":
+            os.remove(item[1])
     res = {"value": units / statistics.mean(t), "unit": "nnz/s", "cores": nthreads,
            "kind": "reference", "sample": meta["sample"], "step_s_mean": statistics.mean(t),
            "step_s_median": statistics.median(t), "value_median": units / statistics.median(t),
            "protocol": f"{warmup} untimed warm-up + {steps} timed runs, mean (P/src/bench.cpp:"
                        f"199-209) and median; par:: with nthreads={nthreads}",
            "mttkrp_strategy": strategies, "host": host_record()}
-    if seq and name != "pre":
+    if seq and name not in ("pre", "tns"):
         # seq:: on one core over the same calls (one pass; long calls on a
         # prefix of the sample when the par:: step is heavy)
         t0 = time.perf_counter()
@@ -395,6 +405,17 @@ def crosscheck(name, arrays, meta, k=200_000) -> dict:
             for op, nm in ((0, "tew_add"), (2, "tew_mul")):
                 z, _, _, _ = ref.tew(x.copy(), y2.copy(), op)
                 out[nm] = "pass" if same(ops.tew(dev(x), dev(y2), op), z) else "fail"
+    elif name == "tns":
+        from paper_1902_03317_b200 import tns
+        base = "/dev/shm" if os.path.isdir("/dev/shm") else None
+        fd, path = tempfile.mkstemp(suffix=".tns", dir=base)
+        try:
+            with os.fdopen(fd, "wb") as fh:
+                fh.write(arrays["text"].tobytes())
+            g, r = tns.read_tns(path), ref.read_tns(path)
+            out["read_tns"] = "pass" if same(g, r) else "fail"
+        finally:
+            os.remove(path)
     elif name in ("c4", "c5"):
         fs = [arrays[f"f{d}"] for d in range(N)]
         tf = [torch.from_numpy(f).cuda() for f in fs]
@@ -1132,7 +1153,70 @@ class Pre(Workload):
                                   "(the reference's sort is serial)"}
 
 
-WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c5": C5, "pre": Pre}
+class Tns(Workload):
+    """.tns ingest (read_tns<float>, P/src/io.cpp:42-120)
+    on C2's 10M-entry tensor written as text (1-based indices, values with 6
+    decimals, one entry per line): the device parse of text already in HBM
+    (spt_tns_scan + spt_tns_parse); e2e = read_tns(path) from the page cache
+    (file -> pinned -> H2D -> parse)."""
+
+    name = "tns-read"
+    CPU_SAMPLE = 2_000_000
+
+    def __init__(self, seed, device, scale=1.0, mttkrp=None):
+        from paper_1902_03317_b200 import generate, tns
+        c = generate.CONFIGS["c2"]
+        self.dims = c["dims"]
+        self.nnz = int(c["nnz"] * scale)
+        x = generate.coo(self.dims, self.nnz, seed, c["zipf"], 0.5, 1.5, None, device)
+        self.text = generate.tns_text(x)
+        del x
+        self.bytes = int(self.text.numel())
+        n, N = self.nnz, 3
+        self.ops = [Op("read_tns", lambda: tns.read_tns_bytes(self.text, None, device), n,
+                       lambda: self.bytes + 4 * (N + 1) * n)]
+        self.device = device
+
+    def config(self):
+        return {"workload": self.name, "dims": self.dims, "nnz": self.nnz,
+                "text_bytes": self.bytes,
+                "text": "C2's tensor (draw order) as .tns: 1-based indices, values %.6f, "
+                        "single spaces, one entry per line",
+                "note": "value: text resident in HBM; e2e: read_tns(path) from the page cache"}
+
+    def cpu_arrays(self):
+        t = self.text[: min(self.bytes, 64 << 20)].cpu().numpy()
+        nl = np.flatnonzero(t == 10)
+        k = min(self.CPU_SAMPLE, len(nl))
+        t = np.ascontiguousarray(t[: nl[k - 1] + 1])
+        return {"text": t}, {"dims": self.dims, "sample_nnz": k,
+                             "sample": f"read_tns<float> of the first {k} lines "
+                                       f"({t.size} bytes) from the page cache "
+                                       "(the reference's reader is serial)"}
+
+    E2E_PATH = ("tns.read_tns(path): file (page cache) -> pinned host buffer -> H2D -> "
+                "device scan + parse; dims read back")
+
+    def e2e_host(self, device=0):
+        base = "/dev/shm" if os.path.isdir("/dev/shm") else None
+        d = tempfile.mkdtemp(prefix="spt_tns_", dir=base)
+        path = os.path.join(d, "x.tns")
+        self.text.cpu().numpy().tofile(path)
+        self._tmpdir = d
+        return {"path": path}
+
+    def e2e_step(self, host):
+        from paper_1902_03317_b200 import tns
+        z = tns.read_tns(host["path"], None, self.device)
+        return self.bytes, 4 * len(z.dims)
+
+    def e2e_done(self):
+        d = getattr(self, "_tmpdir", None)
+        if d:
+            shutil.rmtree(d, ignore_errors=True)
+
+
+WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c5": C5, "pre": Pre, "tns": Tns}
 
 
 def report_rows(wl, ops_list):
@@ -1373,8 +1457,11 @@ def main_ours(args, world, rank, local):
             ms = float(t.item())
         e2e = {"value": world * units_per_step / (ms / 1e3), "unit": "nnz/s",
                "h2d_bytes_per_step": world * h2d, "d2h_bytes_per_step": world * d2h,
-               "ms_per_step": ms, "path": getattr(wl, "E2E_PATH", "ops.* -> C-ABI")}
+               "ms_per_step": ms, "ms_each": [round(t, 3) for t in times],
+               "path": getattr(wl, "E2E_PATH", "ops.* -> C-ABI")}
         del host
+        if hasattr(wl, "e2e_done"):
+            wl.e2e_done()
     if dropin_dir is not None:
         # the C++ drop-in (spten::gpu::*) on host SparseTensorCOO data in its own
         # process: every call uploads its operands from pageable std::vectors,

@@ -20,7 +20,9 @@
 // stays with the reference implementation.
 #pragma once
 
+#include <optional>
 #include <span>
+#include <string>
 #include <vector>
 
 #include "spten/ops.hpp"
@@ -69,6 +71,14 @@ DenseMatrix<float> mttkrp(const SparseTensorCOO<float>& x,
 void sort_lexicographic(SparseTensorCOO<float>& t, std::span<const unsigned> mode_order);
 SparseTensorCOO<float> coalesce(const SparseTensorCOO<float>& t);
 FiberIndex build_fiber_index(const SparseTensorCOO<float>& t, unsigned mode);
+
+// P/include/spten/io.hpp:22-23 (read_tns<float>): the file is streamed through
+// pinned buffers to the device, split and parsed there (include/spten_b200.h
+// spt_tns_scan / spt_tns_parse); same entries (file order), dims, flags and
+// error messages ("path:line: msg", std::runtime_error) as the reference.
+// Orders above SPT_MAX_ORDER (8) throw std::overflow_error.
+SparseTensorCOO<float> read_tns(const std::string& path,
+                                std::optional<std::vector<Index>> dims = std::nullopt);
 
 // The par:: twins (P/include/spten/kernels_par.hpp:35-72), so a caller of
 // spten::par:: only swaps the namespace. The device is the parallelism:

@@ -230,6 +230,28 @@ SPT_API int spt_mttkrp_f32_multi(int ndev, spt_ctx* const* ctxs, const spt_coo* 
                                  const uint64_t* rows, const uint64_t* cols, uint32_t mode,
                                  float* const* d_out, void* const* streams);
 
+/* ---- .tns text ingest on the device ----------------------------------------
+ * Replaces spten::read_tns<float>(path, dims) (P/include/spten/io.hpp:22-23,
+ * P/src/io.cpp:42-120) for text already in device memory (the caller reads
+ * the file and copies its bytes up). spt_tns_scan splits lines, classifies
+ * them and ranks the entry lines: it returns the order (from the first entry
+ * line, or n_override when dims_override is given) and nnz so the caller can
+ * size the output; spt_tns_parse fills z->idx[0..order) and z->val (device,
+ * nnz each, in file order) and sets order, nnz, dims (per-mode max + 1, or the
+ * override), has_sort_order = coalesced = 0. d_text must stay valid until
+ * spt_tns_destroy. Parse errors return SPT_ERUNTIME with the reference's
+ * message and *err_line = the failing 1-based line (the reference's
+ * "path:line: msg"; prepend the path); an empty override is SPT_EINVAL.
+ * Orders above SPT_MAX_ORDER and files of 2^32 lines or more are
+ * SPT_EOVERFLOW. */
+typedef struct spt_tns spt_tns;
+SPT_API int spt_tns_scan(spt_ctx* ctx, const char* d_text, uint64_t bytes,
+                         const uint32_t* dims_override, uint32_t n_override, spt_tns** out,
+                         uint32_t* order, uint64_t* nnz, uint64_t* err_line, void* stream);
+SPT_API int spt_tns_parse(spt_ctx* ctx, const spt_tns* scan, spt_coo* z, uint64_t* err_line,
+                          void* stream);
+SPT_API void spt_tns_destroy(spt_tns* scan);
+
 /* ---- seeded synthetic generator (bench / test input, not a reference path) --
  * Draws `nnz` distinct tuples: per-mode index distribution `dist[d]`
  * (0 = uniform, s>0 = Zipf(s) over a seeded permutation of ids), duplicates

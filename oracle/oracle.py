@@ -315,14 +315,33 @@ class Ref:
         lib.ref_factors_free.argtypes = [_P]
         lib.ref_mttkrp_fv.argtypes = [_P, _P, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.POINTER(_P)]
+        lib.ref_read_tns.argtypes = [ctypes.c_char_p, _u32p, ctypes.c_uint32, ctypes.POINTER(_P)]
+        lib.ref_write_tns.argtypes = [_P, ctypes.c_char_p]
         self.lib = lib
+
+    def read_tns(self, path: str, dims=None) -> HostTensor:
+        """spten::read_tns<float> (P/src/io.cpp:42-120)."""
+        h = _P()
+        d = _u32(dims) if dims is not None else None
+        self._check(self.lib.ref_read_tns(path.encode(), d.ctypes.data_as(_u32p) if d is not None
+                                          else None, len(dims) if dims is not None else 0,
+                                          ctypes.byref(h)))
+        return self.read(h.value)
+
+    def write_tns(self, x: HostTensor, path: str) -> None:
+        """spten::write_tns<float> (P/src/io.cpp:122-)."""
+        h = self.coo(x)
+        try:
+            self._check(self.lib.ref_write_tns(h, path.encode()))
+        finally:
+            self.free(h)
 
     def max_threads(self) -> int:
         return int(self.lib.ref_max_threads())
 
     def _check(self, rc):
         if rc:
-            _raise(rc, self.lib.ref_last_error().decode())
+            _raise(rc, self.lib.ref_last_error().decode("latin-1"))
 
     # handles ------------------------------------------------------------------
     def coo(self, t: HostTensor) -> int:
@@ -354,7 +373,7 @@ class Ref:
         d = _u32(dims)
         h = self.lib.ref_gen_synthetic(len(dims), d.ctypes.data_as(_u32p), nnz, seed)
         if not h:
-            raise ValueError(self.lib.ref_last_error().decode())
+            raise ValueError(self.lib.ref_last_error().decode("latin-1"))
         return self.read(h)
 
     def ts(self, x: HostTensor, s: float, op: int, variant=0, nthreads=0) -> HostTensor:
@@ -427,7 +446,7 @@ class Ref:
         out = _P()
         try:
             if not hf:
-                _raise(1, self.lib.ref_last_error().decode())
+                _raise(1, self.lib.ref_last_error().decode("latin-1"))
             self._check(self.lib.ref_ttv_fib(hx, hv, mode, hf, variant, nthreads,
                                              ctypes.byref(out)))
         finally:
@@ -474,3 +493,126 @@ class Ref:
         self.lib.ref_matrix_read(out.value, res.ctypes.data_as(_f32p))
         self.lib.ref_matrix_free(out.value)
         return res
+
+
+# ---------------------------------------------------------------------------
+# .tns ingest: a pure-Python restatement of spten::read_tns<float>
+# (P/src/io.cpp:42-120; split_ws / fail_at at io.cpp:17-39), for small files.
+# Pinned against the live reference (Ref.read_tns) by tests/test_tns_oracle.py.
+
+import re  # noqa: E402
+from fractions import Fraction  # noqa: E402
+
+_TNS_NUM = re.compile(rb"-?(?:[0-9]+\.?[0-9]*|\.[0-9]+)(?:[eE][+-]?[0-9]+)?\Z")
+_TNS_WORD = re.compile(rb"-?(?:inf|infinity|nan(?:\([A-Za-z0-9_]*\))?)\Z", re.I)
+_FLT_MAX = float(np.finfo(np.float32).max)
+
+
+def _f32_bits_of(q: Fraction) -> Optional[int]:
+    """Correctly rounded (ties to even) float32 bits of q > 0; None when the
+    result is out of range (rounds to infinity, or a nonzero q rounds to 0),
+    std::from_chars' result_out_of_range."""
+    c = np.float32(min(float(q), _FLT_MAX)).view(np.uint32).item()
+    # the candidates around c: bits c-2 .. c+2 (bit 0x7F800000 stands for
+    # "rounds to infinity", 0 for "rounds to zero")
+    best, best_err = None, None
+    for b in range(max(0, c - 2), min(0x7F800000, c + 2) + 1):
+        v = Fraction(2 ** 128) if b == 0x7F800000 else Fraction(
+            float(np.uint32(b).view(np.float32)))
+        err = abs(q - v)
+        if best is None or err < best_err or (err == best_err and b % 2 == 0):
+            best, best_err = b, err
+    if best in (0, 0x7F800000):
+        return None
+    return best
+
+
+def _tns_value(tok: bytes) -> Optional[int]:
+    """std::from_chars(float) over the whole token -> float32 bits or None."""
+    if _TNS_WORD.match(tok):
+        neg = tok.startswith(b"-")
+        w = tok.lstrip(b"-").lower()
+        bits = 0x7F800000 if w.startswith(b"inf") else 0x7FC00000
+        return bits | (0x80000000 if neg else 0)
+    if not _TNS_NUM.match(tok):
+        return None
+    neg = tok.startswith(b"-")
+    body = tok.lstrip(b"-")
+    mant, _, exp = body.lower().partition(b"e")
+    ip, _, fp = mant.partition(b".")
+    digits = (ip + fp).lstrip(b"0")
+    if not digits:
+        return 0x80000000 if neg else 0
+    E = (int(exp) if exp else 0) - len(fp)
+    mag = len(digits) - 1 + E
+    if mag > 38 or mag < -46:
+        return None
+    q = Fraction(int(digits)) * (Fraction(10) ** E)
+    b = _f32_bits_of(q)
+    if b is None:
+        return None
+    return b | (0x80000000 if neg else 0)
+
+
+def read_tns_py(data: bytes, dims: Optional[Sequence[int]] = None, name: str = "<text>"):
+    """read_tns<float> over the bytes of a file: returns (dims, [idx u32 arrays],
+    values f32) or raises RuntimeError("name:line: msg") / ValueError like the
+    reference (P/src/io.cpp:42-120)."""
+    def fail(lineno, msg):
+        raise RuntimeError(f"{name}:{lineno}: {msg}")
+
+    N = 0
+    have_order = False
+    if dims is not None:
+        N = len(dims)
+        if N == 0:
+            raise ValueError("read_tns: dims override must not be empty")
+        have_order = True
+    idx: list = [[] for _ in range(N)]
+    vals: list = []
+    maxidx = [0] * N
+    lines = data.split(b"\n")
+    if lines and lines[-1] == b"":
+        lines.pop()  # std::getline: a final '\n' ends the last line
+    for lineno, line in enumerate(lines, 1):
+        if line.endswith(b"\r"):
+            line = line[:-1]
+        s = line.lstrip(b" \t")
+        if not s or s.startswith(b"#"):
+            continue
+        tok = [t for t in re.split(rb"[ \t]+", line) if t]
+        if not have_order:
+            if len(tok) < 2:
+                fail(lineno, "need at least one index and a value per entry")
+            N = len(tok) - 1
+            have_order = True
+            idx = [[] for _ in range(N)]
+            maxidx = [0] * N
+        elif len(tok) != N + 1:
+            fail(lineno, f"expected {N + 1} tokens, got {len(tok)}")
+        for d in range(N):
+            t = tok[d]
+            if not re.fullmatch(rb"[0-9]+", t) or int(t) >= 1 << 64:
+                fail(lineno, f"non-numeric index token '{t.decode('latin-1')}'")
+            raw = int(t)
+            if raw < 1:
+                fail(lineno, "indices are 1-based; got 0")
+            if raw > 0xFFFFFFFF:
+                fail(lineno, f"index {raw} out of range")
+            if dims is not None:
+                if raw - 1 >= dims[d]:
+                    fail(lineno, f"index {raw} exceeds declared dimension {dims[d]} of mode {d}")
+            else:
+                maxidx[d] = max(maxidx[d], raw - 1)
+            idx[d].append(raw - 1)
+        b = _tns_value(tok[N])
+        if b is None:
+            fail(lineno, f"unparsable value '{tok[N].decode('latin-1')}'")
+        vals.append(b)
+    if not have_order:
+        raise RuntimeError(f"read_tns: {name} has no entries and no dims override; "
+                           "order is unknown")
+    nnz = len(vals)
+    out_dims = list(dims) if dims is not None else [(m + 1) if nnz else 0 for m in maxidx]
+    return (out_dims, [np.array(i, np.uint32) for i in idx],
+            np.array(vals, np.uint32).view(np.float32))

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstring>
 #include <new>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -246,6 +247,20 @@ int ref_mttkrp_fv(void* x, void* fv, uint32_t mode, int variant, int nthreads, i
         variant ? par::mttkrp(a, f, mode, nthreads, static_cast<MttkrpStrategy>(strategy))
                 : seq::mttkrp(a, f, mode));
   });
+}
+
+// ---- io (P/src/io.cpp) --------------------------------------------------------
+// read_tns<float>(path, dims override when n_dims > 0) into a handle.
+int ref_read_tns(const char* path, const uint32_t* dims, uint32_t n_dims, void** out) {
+  return guard([&] {
+    std::optional<std::vector<Index>> ov;
+    if (dims) ov = std::vector<Index>(dims, dims + n_dims);
+    *out = new Coo(read_tns<float>(path, ov));
+  });
+}
+
+int ref_write_tns(void* x, const char* path) {
+  return guard([&] { write_tns(*static_cast<Coo*>(x), path); });
 }
 
 int ref_max_threads() { return par::resolve_threads(0); }

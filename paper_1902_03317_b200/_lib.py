@@ -112,6 +112,10 @@ _SIGNATURES = {
     "spt_mttkrp_f32_multi": ([_I, ctypes.POINTER(_P), _PCOO, ctypes.POINTER(_U32),
                               ctypes.POINTER(_P), _PU64, _PU64, _U32, ctypes.POINTER(_P),
                               ctypes.POINTER(_P)], _I),
+    "spt_tns_scan": ([_P, _P, _U64, ctypes.POINTER(_U32), _U32, ctypes.POINTER(_P),
+                      ctypes.POINTER(_U32), _PU64, _PU64, _P], _I),
+    "spt_tns_parse": ([_P, _P, _PCOO, _PU64, _P], _I),
+    "spt_tns_destroy": ([_P], None),
     "spt_gen_coo_f32": ([_P, _PCOO, _U64, ctypes.POINTER(ctypes.c_double), ctypes.c_float,
                          ctypes.c_float, ctypes.POINTER(_U32), _P], _I),
     "spt_gen_uniform_f32": ([_P, _P, _U64, _U64, _U64, ctypes.c_float, ctypes.c_float, _P], _I),

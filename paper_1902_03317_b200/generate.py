@@ -72,3 +72,51 @@ def config_tensor(name: str, seed: int = 1, sort_order=None, device: int = 0,
                   nnz: Optional[int] = None) -> DeviceCOO:
     c = CONFIGS[name]
     return coo(c["dims"], nnz or c["nnz"], seed, c["zipf"], c["lo"], c["hi"], sort_order, device)
+
+
+def tns_text(x: DeviceCOO, decimals: int = 6) -> torch.Tensor:
+    """The .tns text of x (P/include/spten/io.hpp:14-20: 1-based indices, then
+    the value, single spaces, '\\n' endings) as a uint8 tensor on x's device,
+    built with tensor ops: bench / test input for the ingest path, not a
+    product path. Values are written in fixed notation with `decimals`
+    fractional digits (so they parse to the nearest float of that decimal,
+    not necessarily to x's values)."""
+    dev = x.device
+    n = x.nnz
+    chars, masks = [], []
+
+    def digits(v: torch.Tensor, width: int, keep_one: bool = True):
+        p = torch.tensor([10 ** k for k in range(width - 1, -1, -1)], dtype=torch.int64,
+                         device=dev)
+        d = (v[:, None] // p[None, :]) % 10
+        nd = (v[:, None] >= p[None, :]).sum(1)
+        if keep_one:
+            nd = nd.clamp(min=1)
+        mask = torch.arange(width, device=dev)[None, :] >= (width - nd)[:, None]
+        return (d + 48).to(torch.uint8), mask
+
+    def const(c: str):
+        chars.append(torch.full((n, 1), ord(c), dtype=torch.uint8, device=dev))
+        masks.append(torch.ones((n, 1), dtype=torch.bool, device=dev))
+
+    for d in range(x.order):
+        v = (x.indices[d].to(torch.int64) & 0xFFFFFFFF) + 1
+        c, m = digits(v, len(str(int(x.dims[d]))))
+        chars.append(c)
+        masks.append(m)
+        const(" ")
+    val = x.values.to(torch.float64)
+    chars.append(torch.full((n, 1), ord("-"), dtype=torch.uint8, device=dev))
+    masks.append((val < 0)[:, None])
+    q = torch.round(val.abs() * 10 ** decimals).to(torch.int64)
+    ip, fp = q // 10 ** decimals, q % 10 ** decimals
+    c, m = digits(ip, max(1, len(str(int(ip.max().item()))) if n else 1))
+    chars.append(c)
+    masks.append(m)
+    if decimals:
+        const(".")
+        c, _ = digits(fp, decimals, keep_one=False)
+        chars.append(c)
+        masks.append(torch.ones_like(c, dtype=torch.bool))
+    const("\n")
+    return torch.cat(chars, 1)[torch.cat(masks, 1)]

@@ -8,7 +8,10 @@
 
 #include <cuda_runtime.h>
 
+#include <fcntl.h>
 #include <pthread.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <sched.h>
 
 #include <algorithm>
@@ -22,6 +25,7 @@
 #include <cstring>
 #include <memory>
 #include <new>
+#include <optional>
 #include <stdexcept>
 #include <string>
 
@@ -87,18 +91,14 @@ class CopyPool {
       std::memcpy(dst, src, n);
       return;
     }
-    std::unique_lock<std::mutex> lk(m_);
-    dst_ = static_cast<char*>(dst);
-    src_ = static_cast<const char*>(src);
-    n_ = n;
-    next_.store(0);
-    busy_ = static_cast<int>(workers_.size());
-    ++gen_;
-    cv_.notify_all();
-    lk.unlock();
-    work();
-    lk.lock();
-    done_.wait(lk, [&] { return busy_ == 0; });
+    run(static_cast<char*>(dst), static_cast<const char*>(src), -1, 0, n);
+  }
+  // n bytes of file fd from offset off into dst, in parallel pieces; false on
+  // a read error or a short file.
+  bool pread(void* dst, int fd, uint64_t off, size_t n) {
+    read_error_.store(false);
+    run(static_cast<char*>(dst), nullptr, fd, off, n);
+    return !read_error_.load();
   }
   ~CopyPool() {
     {
@@ -111,6 +111,22 @@ class CopyPool {
   }
 
  private:
+  void run(char* dst, const char* src, int fd, uint64_t off, size_t n) {
+    std::unique_lock<std::mutex> lk(m_);
+    dst_ = dst;
+    src_ = src;
+    fd_ = fd;
+    foff_ = off;
+    n_ = n;
+    next_.store(0);
+    busy_ = static_cast<int>(workers_.size());
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    work();
+    lk.lock();
+    done_.wait(lk, [&] { return busy_ == 0; });
+  }
   CopyPool() {
     const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
     for (unsigned i = 0; i < std::min(hw, 8u) - 1; ++i)
@@ -138,8 +154,21 @@ class CopyPool {
   }
   void work() {
     constexpr size_t kPiece = size_t(1) << 20;
-    for (size_t o; (o = next_.fetch_add(kPiece)) < n_;)
-      std::memcpy(dst_ + o, src_ + o, std::min(kPiece, n_ - o));
+    for (size_t o; (o = next_.fetch_add(kPiece)) < n_;) {
+      const size_t c = std::min(kPiece, n_ - o);
+      if (fd_ < 0) {
+        std::memcpy(dst_ + o, src_ + o, c);
+        continue;
+      }
+      for (size_t got = 0; got < c;) {
+        const ssize_t r = ::pread(fd_, dst_ + o + got, c - got, static_cast<off_t>(foff_ + o + got));
+        if (r <= 0) {
+          read_error_.store(true);
+          break;
+        }
+        got += static_cast<size_t>(r);
+      }
+    }
   }
   std::vector<std::thread> workers_;
   std::mutex m_;
@@ -151,6 +180,9 @@ class CopyPool {
   const char* src_ = nullptr;
   size_t n_ = 0;
   std::atomic<size_t> next_{0};
+  int fd_ = -1;
+  uint64_t foff_ = 0;
+  std::atomic<bool> read_error_{false};
 };
 
 void par_memcpy(void* dst, const void* src, size_t n) { CopyPool::get().memcpy(dst, src, n); }
@@ -349,6 +381,63 @@ uint32_t* upload_fptr(Session& S, const FiberIndex& fib) {
 }
 
 }  // namespace
+
+SparseTensorCOO<float> read_tns(const std::string& path, std::optional<std::vector<Index>> dims) {
+  struct Fd {
+    int fd;
+    ~Fd() {
+      if (fd >= 0) ::close(fd);
+    }
+  } f{::open(path.c_str(), O_RDONLY)};
+  if (f.fd < 0) throw std::runtime_error("read_tns: cannot open " + path);  // P/src/io.cpp:45
+  if (dims && dims->empty())  // P/src/io.cpp:52
+    throw std::invalid_argument("read_tns: dims override must not be empty");
+  if (dims && dims->size() > SPT_MAX_ORDER)
+    throw std::overflow_error("read_tns: order exceeds " + std::to_string(SPT_MAX_ORDER));
+  struct stat sb;
+  if (::fstat(f.fd, &sb) != 0) throw std::runtime_error("read_tns: I/O error reading " + path);
+  Session& S = session();
+  // the file's bytes straight into the pinned ring (parallel preads), DMA of
+  // chunk k under the read of chunk k+1
+  const size_t bytes = static_cast<size_t>(sb.st_size);
+  char* d_text = static_cast<char*>(S.buf(kAux2, bytes + 1));
+  for (size_t o = 0; o < bytes; o += kChunk) {
+    const size_t c = std::min(kChunk, bytes - o);
+    const int k = S.next;
+    S.next ^= 1;
+    cuda(cudaEventSynchronize(S.ev[k]), "sync");
+    if (!CopyPool::get().pread(S.pin[k], f.fd, o, c))
+      throw std::runtime_error("read_tns: I/O error reading " + path);
+    cuda(cudaMemcpyAsync(d_text + o, S.pin[k], c, cudaMemcpyHostToDevice, S.h2d), "H2D");
+    cuda(cudaEventRecord(S.ev[k], S.h2d), "event");
+  }
+  S.uploads_done();
+  // errors: the reference's "path:line: msg" (P/src/io.cpp:37-39)
+  uint64_t line = 0;
+  auto fail = [&](int status) {
+    const std::string msg = spt_last_error();
+    if (status == SPT_ERUNTIME && line)
+      throw std::runtime_error(path + ":" + std::to_string(line) + ": " + msg);
+    if (status == SPT_ERUNTIME && msg.find("order is unknown") != std::string::npos)
+      throw std::runtime_error("read_tns: " + path + " " + msg);  // P/src/io.cpp:112-114
+    raise(status);
+  };
+  std::vector<uint32_t> ov;
+  if (dims) ov.assign(dims->begin(), dims->end());
+  spt_tns* scan = nullptr;
+  uint32_t order = 0;
+  uint64_t nnz = 0;
+  int st = spt_tns_scan(S.ctx, d_text, bytes, dims ? ov.data() : nullptr,
+                        static_cast<uint32_t>(ov.size()), &scan, &order, &nnz, &line, S.stream);
+  if (st != SPT_OK) fail(st);
+  std::unique_ptr<spt_tns, void (*)(spt_tns*)> own(scan, spt_tns_destroy);
+  DevCoo dz(S, kZ, order, ov, nnz);
+  st = spt_tns_parse(S.ctx, scan, &dz.d, &line, S.stream);
+  if (st != SPT_OK) fail(st);
+  SparseTensorCOO<float> z;
+  dz.download(z, dz.d, nnz);
+  return z;
+}
 
 SparseTensorCOO<float> ts(const SparseTensorCOO<float>& x, float s, ScalarOp op) {
   Session& S = session();

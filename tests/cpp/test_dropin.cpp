@@ -5,6 +5,7 @@
 // spten::gpu::op compared against spten::seq::op of the real reference
 // library (linked from oracle/_ref) with the reference's own predicates
 // (bit_identical, max_rel_diff). Run by tests/test_dropin.py (-m gpu).
+#include <unistd.h>
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -266,10 +267,81 @@ void rank1_ttm_is_ttv() {
     CHECK(a.nnz() == b.nnz() && rel(a.values, b.values) <= 1e-6);
   }
 }
+// read_tns (P/src/io.cpp:42-120) against the reference on the files of its
+// own tests (P/tests/test_io.cpp:40-150, acceptance.cpp:440-510).
+std::string write_file(const std::string& name, const std::string& body) {
+  const std::string p = "/tmp/spten_dropin_" + std::to_string(::getpid()) + "_" + name;
+  std::FILE* f = std::fopen(p.c_str(), "wb");
+  std::fwrite(body.data(), 1, body.size(), f);
+  std::fclose(f);
+  return p;
+}
+
+void read_tns_parity() {
+  const std::string basic = write_file("basic.tns", "# a comment\n\n1 2 3 4.5\n2 1 1 -1.25\n");
+  auto t = gpu::read_tns(basic);
+  CHECK(bit_identical(t, read_tns<float>(basic)));
+  CHECK(t.dims == std::vector<Index>({2, 2, 3}) && !t.coalesced && !t.sort_order);
+  const std::string padded = write_file("padded.tns", "1 1 1 2.0\n2 2 2 3.0\n");
+  CHECK(gpu::read_tns(padded, std::vector<Index>{4, 4, 4}).dims == std::vector<Index>({4, 4, 4}));
+  const std::string outside = write_file("outside.tns", "1 1 1 2.0\n5 1 1 3.0\n");
+  try {
+    gpu::read_tns(outside, std::vector<Index>{4, 4, 4});
+    CHECK(false);
+  } catch (const std::runtime_error& e) {
+    CHECK(std::string(e.what()) == outside + ":2: index 5 exceeds declared dimension 4 of mode 0");
+  }
+  const std::string comments = write_file("comments.tns", "# nothing\n# here\n");
+  CHECK(throws_as<std::runtime_error>([&] { gpu::read_tns(comments); }));
+  auto e = gpu::read_tns(comments, std::vector<Index>{3, 2});
+  CHECK(e.order() == 2 && e.nnz() == 0 && e.dims == std::vector<Index>({3, 2}));
+  CHECK(throws_as<std::invalid_argument>([&] { gpu::read_tns(basic, std::vector<Index>{}); }));
+  CHECK(throws_as<std::runtime_error>([&] { gpu::read_tns("/nonexistent/x.tns"); }));
+  const char* malformed[] = {
+      "1 2 3 1.0\n1 2 1.0\n",     "1 2 3 1.0\n1 2 3 4 1.0\n", "1 2 3 1.0\nx 2 3 1.0\n",
+      "1 2 3 1.0\n0 2 3 1.0\n",   "1 2 3 1.0\n-1 2 3 1.0\n",  "1 2 3 1.0\n5000000000 2 3 1.0\n",
+      "1 2 3 1.0\n1 2 3\n",       "1 2 3 1.0\n1 2 3 4..5\n",  "1 2 3 1.0\n1 2 3 1e999\n",
+      "1 2 3 1.0\n1 2 3 --4\n"};
+  int k = 0;
+  for (const char* body : malformed) {
+    const std::string p = write_file("bad" + std::to_string(k++) + ".tns", body);
+    std::string want, got;
+    try {
+      read_tns<float>(p);
+    } catch (const std::runtime_error& ex) {
+      want = ex.what();
+    }
+    try {
+      gpu::read_tns(p);
+    } catch (const std::runtime_error& ex) {
+      got = ex.what();
+    }
+    CHECK(!want.empty() && got == want);
+    std::remove(p.c_str());
+  }
+  // write/read round trips (test_io.cpp:84-110, acceptance.cpp:440-470)
+  std::mt19937_64 rng(8000);
+  for (int i = 0; i < 20; ++i) {
+    auto x = rand_instance(rng);
+    x.values[0] = 0.0f;
+    if (x.nnz() > 1) x.values[1] = std::numeric_limits<float>::denorm_min();
+    if (x.nnz() > 2) x.values[2] = 1.0f / 3.0f;
+    const std::string p = write_file("rt" + std::to_string(i) + ".tns", "");
+    write_tns(x, p);
+    auto back = gpu::read_tns(p, x.dims);
+    x.sort_order.reset();
+    x.coalesced = false;
+    CHECK(bit_identical(back, x));
+    CHECK(bit_identical(gpu::read_tns(p), read_tns<float>(p)));
+    std::remove(p.c_str());
+  }
+  for (const auto& p : {basic, padded, outside, comments}) std::remove(p.c_str());
+}
 }  // namespace
 
 int main() {
   kats();
+  read_tns_parity();
   random_parity();
   rank1_ttm_is_ttv();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);

@@ -91,3 +91,15 @@ def test_default_workload_is_c5():
     import bench
     assert bench.DEFAULT_WORKLOAD == "c5"
     assert json.dumps(bench.host_record())
+
+
+def test_tns_leg_reads_the_sample_file():
+    import bench
+    rng = np.random.default_rng(2)
+    lines = [f"{a} {b} {c} {v:.6f}" for a, b, c, v in
+             zip(rng.integers(1, 50, 5000), rng.integers(1, 40, 5000), rng.integers(1, 30, 5000),
+                 rng.uniform(0.5, 1.5, 5000))]
+    text = np.frombuffer(("\n".join(lines) + "\n").encode(), np.uint8)
+    meta = {"dims": [49, 39, 29], "sample_nnz": 5000, "sample": "t"}
+    res = bench.run_cpu_leg("tns", {"text": text}, meta, steps=2, warmup=1)
+    assert res["value"] > 0 and "seq" not in res

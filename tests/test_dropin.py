@@ -19,7 +19,7 @@ def test_dropin_library_links_the_c_abi():
                          check=True).stdout
     for sym in ("spten::gpu::mttkrp", "spten::gpu::tew_eq", "spten::gpu::tew", "spten::gpu::ts",
                 "spten::gpu::ttv", "spten::gpu::ttm", "spten::gpu::sort_lexicographic",
-                "spten::gpu::coalesce", "spten::gpu::build_fiber_index"):
+                "spten::gpu::coalesce", "spten::gpu::build_fiber_index", "spten::gpu::read_tns"):
         assert sym in out, sym
     und = subprocess.run(["nm", "-D", "--undefined-only", LIB], capture_output=True, text=True,
                          check=True).stdout
