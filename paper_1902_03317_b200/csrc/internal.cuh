@@ -185,7 +185,14 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
+// try_wait's suspend-time hint: a waiting warp sleeps until the phase flips
+// (or this many ns pass) instead of re-issuing the test in a tight loop.
+#ifndef SPT_MBAR_SUSPEND_NS
+#define SPT_MBAR_SUSPEND_NS 0x10000
+#endif
+constexpr uint32_t kMbarSuspendNs = SPT_MBAR_SUSPEND_NS;
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+#if SPT_MBAR_SUSPEND_NS == 0
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -195,6 +202,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       "}\n" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+#else
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SPT_MBAR_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra SPT_MBAR_WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"(kMbarSuspendNs)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          unsigned long long* bar) {

@@ -344,7 +344,7 @@ struct StageInfo {
   uint32_t tile, nxt, nyt, _pad;
   uint32_t xoff[SPT_MAX_ORDER + 1], yoff[SPT_MAX_ORDER + 1];
   unsigned long long x_before, y_after;
-  unsigned long long b0;
+  unsigned long long a0, b0;  // the tile's first x / y entry
   uint32_t yv_after, _pad2;  // value of the first y after the tile (matches across the edge)
 };
 
@@ -479,7 +479,8 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
       // lane q <= N: x run of array q (q == N: values); lane 16+q: y run.
       const bool is_y = lane >= 16;
       const uint32_t q = lane & 15u;
-      if (q <= static_cast<uint32_t>(N)) {
+      // mul stages no values: only its (few) matches read them, from global
+      if (q < static_cast<uint32_t>(N) || (q == static_cast<uint32_t>(N) && OP != SPT_MUL)) {
         const uint32_t* xs =
             q < static_cast<uint32_t>(N) ? p.xi[q] : reinterpret_cast<const uint32_t*>(p.xv);
         const uint32_t* ys =
@@ -504,6 +505,7 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
         inf.tile = static_cast<uint32_t>(t);
         inf.nxt = nxt;
         inf.nyt = nyt;
+        inf.a0 = a0;
         inf.b0 = b0;
         inf.y_after = (b1 < p.ny) ? pack_g<N>(p.yi, p, b1) : ~0ull;
         inf.x_before = (a0 > 0) ? pack_g<N>(p.xi, p, a0 - 1) : ~0ull;
@@ -621,6 +623,8 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
     }
     const int nxt = static_cast<int>(inf.nxt), nyt = static_cast<int>(inf.nyt);
     const unsigned long long x_before = inf.x_before, y_after = inf.y_after;
+    const unsigned long long inf_a0 = inf.a0, inf_b0 = inf.b0;
+    const uint32_t yv_after = inf.yv_after;
     const int len = nxt + nyt;
     const int Y0 = nxt + 1;  // key slot of y entry 0
     {
@@ -639,12 +643,12 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
           k |= (unsigned long long)st0[q * kSeg + (isx ? xo[q] : yo[q]) + i] << p.shift[q];
         const int slot_i = isx ? i : i + 1;
         sk[pad64(slot_i)] = k;
-        sv[pad(slot_i)] = st0[N * kSeg + (isx ? xo[N] : yo[N]) + i];
+        if (OP != SPT_MUL) sv[pad(slot_i)] = st0[N * kSeg + (isx ? xo[N] : yo[N]) + i];
       }
       if (tid == 0) {
         sk[pad64(nxt)] = ~0ull;
         sk[pad64(Y0 + nyt)] = ~0ull;
-        sv[pad(Y0 + nyt)] = inf.yv_after;
+        if (OP != SPT_MUL) sv[pad(Y0 + nyt)] = inf.yv_after;
       }
     }
     __syncwarp();
@@ -676,11 +680,18 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
       const bool take_x = xin && (!yin || kx <= ky);
       const bool mx = kx == (yin ? ky : y_after);  // x matched by the following y
       const bool my = px == ky;                    // y matched by the preceding x
-      float v = __uint_as_float(sv[take_x ? pad(i) : pad(Y0 + j)]);
-      if (take_x && mx) {
-        // the y head's value; past the run, the sentinel slot holds the next y's
-        const float w = __uint_as_float(sv[pad(Y0 + j)]);
-        v = OP == SPT_ADD ? v + w : (OP == SPT_SUB ? v - w : v * w);
+      float v = 0.f;
+      if (OP == SPT_MUL) {
+        if (take_x && mx)  // the y head; past the run, the first y after the tile
+          v = __ldg(p.xv + inf_a0 + i) *
+              (j < nyt ? __ldg(p.yv + inf_b0 + j) : __uint_as_float(yv_after));
+      } else {
+        v = __uint_as_float(sv[take_x ? pad(i) : pad(Y0 + j)]);
+        if (take_x && mx) {
+          // the y head's value; past the run, the sentinel slot holds the next y's
+          const float w = __uint_as_float(sv[pad(Y0 + j)]);
+          v = OP == SPT_ADD ? v + w : v - w;
+        }
       }
       if (OP == SPT_SUB && !take_x) v = -v;
       const bool e = valid && (take_x ? (OP != SPT_MUL || mx) : (OP != SPT_MUL && !my));
