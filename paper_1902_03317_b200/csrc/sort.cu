@@ -4,7 +4,8 @@
 // permutation under compare_entries, then gather_entries :39-50), coalesce
 // P/src/tensor.cpp:66-90, build_fiber_index P/src/tensor.cpp:92-120.
 //
-// Sort = stable LSD radix over the modes of the sort order. Modes are packed,
+// Sort = stable LSD radix over the modes of the sort order (the hand-written
+// single-sweep passes of radix.cu). Modes are packed,
 // least significant first, into <=64-bit chunk keys using log2(dims[d]) bits
 // each (indices must be < dims, as validate() requires, P/src/tensor.cpp:190-215);
 // each chunk is one stable radix sort of (key, permutation) pairs over only
@@ -21,14 +22,12 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "radix.cuh"
 
 namespace {
 
-struct PackSpec {
-  const uint32_t* idx[SPT_MAX_ORDER];
-  uint32_t shift[SPT_MAX_ORDER];
-  int n;
-};
+using spt::radix::PackSpec;
+using spt::radix::UnpackSpec;
 
 __host__ __device__ inline uint32_t bits_for(uint32_t extent) {
   if (extent <= 1) return 0;
@@ -38,21 +37,6 @@ __host__ __device__ inline uint32_t bits_for(uint32_t extent) {
     v >>= 1;
   }
   return b;
-}
-
-// key[i] = packed chunk of entry perm[i] (perm == nullptr: identity).
-template <typename K>
-__global__ void pack_keys_kernel(PackSpec spec, const uint32_t* perm, K* keys, uint32_t* iota,
-                                 uint64_t n) {
-  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) {
-    const uint64_t src = perm ? perm[i] : i;
-    K k = 0;
-    for (int j = 0; j < spec.n; ++j) k |= static_cast<K>(spec.idx[j][src]) << spec.shift[j];
-    keys[i] = k;
-    if (iota) iota[i] = static_cast<uint32_t>(i);
-  }
 }
 
 template <typename T>
@@ -76,27 +60,6 @@ __global__ void head_flags_kernel(TupleCmp t, uint32_t* flags, uint64_t n) {
     uint32_t f = (m == 0);
     for (int j = 0; j < t.n && !f; ++j) f = t.idx[j][m] != t.idx[j][m - 1];
     flags[m] = f;
-  }
-}
-
-// Inverse of pack_keys_kernel for a tuple that fits one key: idx[d][i] from
-// the sorted key (constant modes -> 0), values from the co-sorted payload.
-struct UnpackSpec {
-  uint32_t* idx[SPT_MAX_ORDER];
-  uint32_t shift[SPT_MAX_ORDER];
-  uint32_t mask[SPT_MAX_ORDER];
-  int n;
-};
-template <typename K>
-__global__ void unpack_keys_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
-                                   UnpackSpec spec, uint32_t* __restrict__ out_val, uint64_t n) {
-  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) {
-    const K k = keys[i];
-    for (int j = 0; j < spec.n; ++j)
-      spt::st_stream(spec.idx[j] + i, static_cast<uint32_t>(k >> spec.shift[j]) & spec.mask[j]);
-    if (out_val != vals) spt::st_stream(out_val + i, vals[i]);
   }
 }
 
@@ -173,62 +136,11 @@ int sort_tuples(spt_ctx* ctx, const spt_coo* x, const uint32_t* mo, uint32_t* d_
     chunks.push_back(PackSpec{});
     chunk_bits.push_back(1);
   }
-  // Scratch: keys (2x u64), perm alt buffer, CUB temp.
-  size_t temp64 = 0, temp32 = 0;
-  {
-    cub::DoubleBuffer<unsigned long long> k64(nullptr, nullptr);
-    cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
-    SPT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp64, k64, v, static_cast<int64_t>(n), 0,
-                                             64, st));
-    cub::DoubleBuffer<uint32_t> k32(nullptr, nullptr);
-    SPT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp32, k32, v, static_cast<int64_t>(n), 0,
-                                             32, st));
-  }
-  const size_t kb = align_up(n * sizeof(unsigned long long));
-  const size_t pb = align_up(n * sizeof(uint32_t));
-  const size_t tb = align_up(std::max(temp64, temp32));
-  void* scratch;
-  SPT_TRY(ctx_scratch(ctx, 2 * kb + pb + tb, &scratch));
-  char* base = static_cast<char*>(scratch);
-  unsigned long long* key_a = reinterpret_cast<unsigned long long*>(base);
-  unsigned long long* key_b = reinterpret_cast<unsigned long long*>(base + kb);
-  uint32_t* perm_b = reinterpret_cast<uint32_t*>(base + 2 * kb);
-  void* temp = base + 2 * kb + pb;
-
-  uint32_t* perm_cur = d_perm_out;  // holds the running permutation
-  for (size_t c = 0; c < chunks.size(); ++c) {
-    const bool first = c == 0;
-    const uint32_t nb = chunk_bits[c];
-    // Keys for entry perm[i]; the first chunk also writes the identity perm.
-    if (nb <= 32) {
-      uint32_t* k32a = reinterpret_cast<uint32_t*>(key_a);
-      uint32_t* k32b = reinterpret_cast<uint32_t*>(key_b);
-      pack_keys_kernel<uint32_t><<<grid_of(ctx, n), 256, 0, st>>>(
-          chunks[c], first ? nullptr : perm_cur, k32a, first ? perm_cur : nullptr, n);
-      SPT_LAUNCHED(ctx);
-      cub::DoubleBuffer<uint32_t> keys(k32a, k32b);
-      cub::DoubleBuffer<uint32_t> vals(perm_cur, perm_cur == d_perm_out ? perm_b : d_perm_out);
-      size_t tbytes = tb;
-      SPT_CUDA(cub::DeviceRadixSort::SortPairs(temp, tbytes, keys, vals, static_cast<int64_t>(n),
-                                               0, static_cast<int>(nb), st));
-      ctx->launches += (nb + 7) / 8 + 2;
-      perm_cur = vals.Current();
-    } else {
-      pack_keys_kernel<unsigned long long><<<grid_of(ctx, n), 256, 0, st>>>(
-          chunks[c], first ? nullptr : perm_cur, key_a, first ? perm_cur : nullptr, n);
-      SPT_LAUNCHED(ctx);
-      cub::DoubleBuffer<unsigned long long> keys(key_a, key_b);
-      cub::DoubleBuffer<uint32_t> vals(perm_cur, perm_cur == d_perm_out ? perm_b : d_perm_out);
-      size_t tbytes = tb;
-      SPT_CUDA(cub::DeviceRadixSort::SortPairs(temp, tbytes, keys, vals, static_cast<int64_t>(n),
-                                               0, static_cast<int>(nb), st));
-      ctx->launches += (nb + 7) / 8 + 2;
-      perm_cur = vals.Current();
-    }
-  }
-  if (perm_cur != d_perm_out)
-    SPT_CUDA(cudaMemcpyAsync(d_perm_out, perm_cur, n * sizeof(uint32_t),
-                             cudaMemcpyDeviceToDevice, st));
+  // One stable radix sort per chunk; the first packs its keys from the index
+  // arrays in entry order, the later ones through the running permutation.
+  for (size_t c = 0; c < chunks.size(); ++c)
+    SPT_TRY(radix::sort_chunk_perm(ctx, chunks[c], c == 0 ? nullptr : d_perm_out, d_perm_out, n,
+                                   chunk_bits[c], st));
   return SPT_OK;
 }
 
@@ -273,53 +185,8 @@ int spt_sort_f32(spt_ctx* ctx, spt_coo* x, const uint32_t* mode_order, unsigned 
       spec.n++;
       used += b;
     }
-    const int nb = static_cast<int>(std::max<uint32_t>(used, 1));
-    const bool k32 = used <= 32;
-    size_t temp = 0;
-    {
-      cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
-      if (k32) {
-        cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
-        SPT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k, v, static_cast<int64_t>(n), 0,
-                                                 nb, st));
-      } else {
-        cub::DoubleBuffer<unsigned long long> k(nullptr, nullptr);
-        SPT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k, v, static_cast<int64_t>(n), 0,
-                                                 nb, st));
-      }
-    }
-    const size_t kb = align_up(n * (k32 ? 4 : 8)), vb = align_up(n * 4);
-    void* scratch;
-    SPT_TRY(spt::ctx_scratch(ctx, 2 * kb + vb + align_up(temp), &scratch));
-    char* base = static_cast<char*>(scratch);
-    uint32_t* val_b = reinterpret_cast<uint32_t*>(base + 2 * kb);
-    void* tmp = base + 2 * kb + vb;
-    uint32_t* xv = reinterpret_cast<uint32_t*>(x->val);
-    const unsigned g = grid_of(ctx, n);
-    if (k32) {
-      uint32_t* ka = reinterpret_cast<uint32_t*>(base);
-      pack_keys_kernel<uint32_t><<<g, 256, 0, st>>>(spec, nullptr, ka, nullptr, n);
-      SPT_LAUNCHED(ctx);
-      cub::DoubleBuffer<uint32_t> keys(ka, reinterpret_cast<uint32_t*>(base + kb));
-      cub::DoubleBuffer<uint32_t> vals(xv, val_b);
-      SPT_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, keys, vals, static_cast<int64_t>(n), 0,
-                                               nb, st));
-      ctx->launches += (nb + 7) / 8 + 2;
-      unpack_keys_kernel<uint32_t><<<g, 256, 0, st>>>(keys.Current(), vals.Current(), un, xv, n);
-    } else {
-      auto* ka = reinterpret_cast<unsigned long long*>(base);
-      pack_keys_kernel<unsigned long long><<<g, 256, 0, st>>>(spec, nullptr, ka, nullptr, n);
-      SPT_LAUNCHED(ctx);
-      cub::DoubleBuffer<unsigned long long> keys(ka,
-                                                 reinterpret_cast<unsigned long long*>(base + kb));
-      cub::DoubleBuffer<uint32_t> vals(xv, val_b);
-      SPT_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, keys, vals, static_cast<int64_t>(n), 0,
-                                               nb, st));
-      ctx->launches += (nb + 7) / 8 + 2;
-      unpack_keys_kernel<unsigned long long><<<g, 256, 0, st>>>(keys.Current(), vals.Current(),
-                                                                un, xv, n);
-    }
-    SPT_LAUNCHED(ctx);
+    SPT_TRY(spt::radix::sort_tuple_inplace(ctx, spec, un, reinterpret_cast<uint32_t*>(x->val), n,
+                                           std::max<uint32_t>(used, 1), st));
   } else if (n > 1) {
     // perm lives in its own allocation (sort_tuples uses the ctx scratch).
     uint32_t* perm = nullptr;

@@ -342,6 +342,43 @@ def test_sort_wide_keys_and_stability(sp):
         assert same(host(ops.coalesce(dx)), O.coalesce(ox))
 
 
+@pytest.mark.parametrize("dims,n", [
+    ([2, 1, 2], 5000),            # 2-bit key: two passes of one bit
+    ([1, 1, 1], 300),             # no significant bit at all
+    ([1, 2, 1], 4609),            # one-bit key, one entry past a u32-key tile
+    ([300, 200, 100], 6144),      # u32 key (25 bits), exactly one tile
+    ([300, 200, 100], 6145),
+    ([300, 200, 100], 100_003),
+    ([70000, 70000, 3], 4608),    # u64 key (36 bits), exactly one tile
+    ([70000, 70000, 3], 4607),
+    ([70000, 70000, 3], 150_001),
+    ([4, 3, 2], 120_000),         # 24 distinct tuples: long duplicate runs, stability
+    ([1 << 20, 1 << 20, 1 << 20, 16], 50_000),  # 64-bit key exactly
+    ([3, 2], 1), ([3, 2], 2), ([3, 2], 3),
+])
+def test_sort_radix_edges(sp, dims, n):
+    """The hand-written radix passes at their edges: key widths 0..64 bits,
+    tile boundaries, duplicate runs (stability), sorted and reversed inputs."""
+    ops = sp[0]
+    rng = np.random.default_rng(len(dims) * 1000 + n)
+    idx = [rng.integers(0, d, n).astype(np.uint32) for d in dims]
+    x = HostTensor(dims, idx, rng.uniform(-1, 1, n).astype(np.float32), None, False)
+    N = len(dims)
+    orders = [list(range(N)), list(range(N))[::-1], [(k + 1) % N for k in range(N)]]
+    for mo in orders:
+        dx = dev(sp, x)
+        ops.sort_lexicographic(dx, mo)
+        ox = x.copy()
+        O.sort_lexicographic(ox, mo)
+        assert same(host(dx), ox), (dims, n, mo)
+        # sorted input (every warp's digits agree in the high passes) and a
+        # second order from it
+        mo2 = mo[::-1]
+        ops.sort_lexicographic(dx, mo2)
+        O.sort_lexicographic(ox, mo2)
+        assert same(host(dx), ox), (dims, n, mo, "resort")
+
+
 def test_tew_merge_large(sp):
     ops = sp[0]
     rng = np.random.default_rng(9)
