@@ -10,8 +10,8 @@
 //   scan_kernel      exclusive scan of each digit's 256 bins (the bin bases);
 //   onesweep_kernel  one pass: a CTA takes tile tickets in order, loads
 //                    THREADS x ITEMS pairs warp-striped (coalesced), ranks them
-//                    stably per warp with match.any on the digit (one private
-//                    counter row per warp, no atomics), scans the rows over the
+//                    stably per warp (peer masks from shared-memory atomicOr,
+//                    one private counter row per warp), scans the rows over the
 //                    warps and bins, publishes the tile's bin counts and finds
 //                    its bins' global offsets by a decoupled look-back over
 //                    epoch-tagged 64-bit words (count and flag in one word, so
@@ -30,7 +30,22 @@ namespace {
 
 constexpr int kBins = 256;
 constexpr int kMaxPasses = 8;
-constexpr int kThreads = 384;
+// Tile shape (tuning knobs): threads per CTA, resident CTAs per SM the
+// register budget is set for, pairs per thread for 8- and 4-byte keys.
+#ifndef SPT_RADIX_THREADS
+#define SPT_RADIX_THREADS 384
+#endif
+#ifndef SPT_RADIX_MINB
+#define SPT_RADIX_MINB 2
+#endif
+#ifndef SPT_RADIX_ITEMS64
+#define SPT_RADIX_ITEMS64 12
+#endif
+#ifndef SPT_RADIX_ITEMS32
+#define SPT_RADIX_ITEMS32 16
+#endif
+constexpr int kThreads = SPT_RADIX_THREADS;
+static_assert(kThreads >= kBins && kThreads % 32 == 0, "one thread per bin");
 
 enum Src { SRC_ARRAYS = 0, SRC_PACK_VAL = 1, SRC_PACK_IOTA = 2 };
 enum Dst { DST_ARRAYS = 0, DST_UNPACK = 1, DST_PAY = 2 };
@@ -79,24 +94,58 @@ __global__ void __launch_bounds__(256) hist_kernel(SrcDesc s, uint64_t n, Digits
   __shared__ uint32_t h[kMaxPasses * kBins];
   for (int j = threadIdx.x; j < dg.passes * kBins; j += blockDim.x) h[j] = 0;
   __syncthreads();
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  constexpr int U = 4;  // keys per thread and step: U loads per array in flight
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * U;
   const unsigned lane = threadIdx.x & 31u;
-  for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x; b < n; b += stride) {
-    const uint64_t i = b + threadIdx.x;
-    const bool ok = i < n;
-    const K key = ok ? load_key<K, SRC>(s, i) : K(0);
-    const bool full = __all_sync(0xffffffffu, ok);
+  for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x * U; b < n; b += stride) {
+    K key[U];
+    bool ok[U];
 #pragma unroll
-    for (int p = 0; p < kMaxPasses; ++p) {
-      if (p >= dg.passes) continue;
-      const uint32_t d = static_cast<uint32_t>(key >> dg.shift[p]) & ((1u << dg.bits[p]) - 1u);
-      // a warp whose 32 keys share the digit (sorted or constant high bits)
-      // adds once instead of serialising 32 same-address atomics
-      const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
-      if (full && __all_sync(0xffffffffu, d == d0)) {
-        if (lane == 0) atomicAdd(&h[p * kBins + d0], 32u);
-      } else if (ok) {
-        atomicAdd(&h[p * kBins + d], 1u);
+    for (int u = 0; u < U; ++u) {
+      ok[u] = b + u * blockDim.x + threadIdx.x < n;
+      key[u] = 0;
+    }
+    if (SRC == SRC_ARRAYS) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) key[u] = __ldcs(static_cast<const K*>(s.keys) + b + u * blockDim.x + threadIdx.x);
+    } else {
+#pragma unroll
+      for (int j = 0; j < SPT_MAX_ORDER; ++j) {
+        if (j < s.pack.n) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u])
+              key[u] |= static_cast<K>(__ldcs(s.pack.idx[j] + b + u * blockDim.x + threadIdx.x))
+                        << s.pack.shift[j];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool full = __all_sync(0xffffffffu, ok[u]);
+#pragma unroll
+      for (int p = 0; p < kMaxPasses; ++p) {
+        if (p >= dg.passes) continue;
+        const uint32_t d =
+            static_cast<uint32_t>(key[u] >> dg.shift[p]) & ((1u << dg.bits[p]) - 1u);
+        // a warp whose 32 keys share the digit (sorted or constant high bits)
+        // adds once instead of serialising 32 same-address atomics
+        const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+        if (dg.bits[p] <= 2) {
+          // <= 4 bins: one ballot per bin, lane b adds bin b's count
+          uint32_t mine = 0;
+#pragma unroll
+          for (uint32_t b4 = 0; b4 < 4; ++b4) {
+            const uint32_t c = __popc(__ballot_sync(0xffffffffu, ok[u] && d == b4));
+            if (lane == b4) mine = c;
+          }
+          if (lane < 4 && mine) atomicAdd(&h[p * kBins + lane], mine);
+        } else if (full && __all_sync(0xffffffffu, d == d0)) {
+          if (lane == 0) atomicAdd(&h[p * kBins + d0], 32u);
+        } else if (ok[u]) {
+          atomicAdd(&h[p * kBins + d], 1u);
+        }
       }
     }
   }
@@ -132,12 +181,14 @@ __device__ __forceinline__ unsigned long long tag(uint32_t epoch, uint32_t flag,
 template <typename K, int ITEMS>
 constexpr size_t onesweep_smem() {
   return static_cast<size_t>(kThreads) * ITEMS * (sizeof(K) + 4) +
-         (kThreads / 32) * kBins * 4 + 2 * kBins * 4;
+         (kThreads / 32) * kBins * 8 + 2 * kBins * 4;
 }
 
-template <typename K, int SRC, int DST, int ITEMS>
-__global__ void __launch_bounds__(kThreads, 2)
-    onesweep_kernel(SrcDesc s, DstDesc d, uint64_t n, uint32_t shift, uint32_t bits,
+// CB: the digit width when it is the full 8 bits (ballots fully unrolled),
+// 0 = any width, read from `bits`.
+template <typename K, int SRC, int DST, int ITEMS, int CB>
+__global__ void __launch_bounds__(kThreads, SPT_RADIX_MINB)
+    onesweep_kernel(SrcDesc s, DstDesc d, uint64_t n, uint32_t shift, uint32_t bits_rt,
                     const uint32_t* __restrict__ base, unsigned long long* status, uint32_t epoch,
                     uint32_t* ticket) {
   constexpr int WARPS = kThreads / 32;
@@ -145,15 +196,17 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ __align__(16) unsigned char smem[];
   K* keys_s = reinterpret_cast<K*>(smem);
   uint32_t* pay_s = reinterpret_cast<uint32_t*>(keys_s + TILE);
-  uint32_t* cnt = pay_s + TILE;             // [WARPS][kBins]
-  uint32_t* bin_start = cnt + WARPS * kBins;  // tile-local start of each bin
+  uint2* pairs = reinterpret_cast<uint2*>(pay_s + TILE);  // [WARPS][kBins] {mask, count}
+  uint32_t* bin_start = reinterpret_cast<uint32_t*>(pairs + WARPS * kBins);  // tile-local
   uint32_t* gbase = bin_start + kBins;        // global position of the bin's shared slot 0
   __shared__ uint32_t s_tile;
   __shared__ uint32_t warp_tot[kBins / 32];
 
   const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t bits = CB ? CB : bits_rt;
   if (tid == 0) s_tile = atomicAdd(ticket, 1u);
-  for (int j = tid; j < WARPS * kBins; j += kThreads) cnt[j] = 0;
+  for (int j = tid; j < WARPS * kBins / 2; j += kThreads)
+    reinterpret_cast<uint4*>(pairs)[j] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t tile_base = static_cast<uint64_t>(tile) * TILE;
@@ -166,49 +219,69 @@ __global__ void __launch_bounds__(kThreads, 2)
   K key[ITEMS];
   uint32_t pay[ITEMS];
   const uint32_t wloc = warp * 32u * ITEMS + lane;
+  if (SRC == SRC_ARRAYS) {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t loc = wloc + k * 32u;
+      key[k] = loc < valid ? __ldcs(static_cast<const K*>(s.keys) + tile_base + loc) : ~K(0);
+    }
+  } else {
+    // one index array at a time: ITEMS independent loads in flight per array
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) key[k] = wloc + k * 32u < valid ? K(0) : ~K(0);
+#pragma unroll
+    for (int j = 0; j < SPT_MAX_ORDER; ++j) {
+      if (j < s.pack.n) {
+        const uint32_t* a = s.pack.idx[j] + tile_base;
+        const uint32_t sh = s.pack.shift[j];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          const uint32_t loc = wloc + k * 32u;
+          if (loc < valid) key[k] |= static_cast<K>(__ldcs(a + loc)) << sh;
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t loc = wloc + k * 32u;
-    if (loc < valid) {
-      key[k] = load_key<K, SRC>(s, tile_base + loc);
-      pay[k] = load_pay<SRC>(s, tile_base + loc);
-    } else {
-      key[k] = ~K(0);
-      pay[k] = 0;
-    }
+    pay[k] = loc < valid ? load_pay<SRC>(s, tile_base + loc) : 0u;
   }
 
-  // Stable rank inside the warp: lanes holding the same digit form a group;
-  // the group's first lane bumps the warp's private counter.
+  // Stable rank inside the warp. Each (warp, digit) owns a pair of words
+  // {mask of the lanes holding the digit in this item, count in the earlier
+  // items}: every lane ORs its bit into the mask and reads the pair back with
+  // one 64-bit load -- its rank is count + lower peers -- and the group's first
+  // lane stores {0, count + group size}. (8 ballots per item cost 3x the
+  // instructions; match.any ~1000 cycles per warp-instruction under load.)
   uint32_t rank[ITEMS];
-  uint32_t* wc = cnt + warp * kBins;
+  uint2* wp = pairs + warp * kBins;
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t dgt = static_cast<uint32_t>(key[k] >> shift) & mask;
-    const uint32_t m = __match_any_sync(0xffffffffu, dgt);
-    const int leader = __ffs(m) - 1;
-    uint32_t old = 0;
-    if (static_cast<int>(lane) == leader) {
-      old = wc[dgt];
-      wc[dgt] = old + __popc(m);
-    }
-    old = __shfl_sync(0xffffffffu, old, leader);
-    rank[k] = old + __popc(m & lt);
+    atomicOr(&wp[dgt].x, 1u << lane);
+    __syncwarp();
+    const uint2 mc = wp[dgt];
+    __syncwarp();
+    rank[k] = mc.y + __popc(mc.x & lt);
+    if ((mc.x & lt) == 0) wp[dgt] = make_uint2(0u, mc.y + __popc(mc.x));
     __syncwarp();
   }
   __syncthreads();
 
-  // Bin b = thread b: exclusive scan of its counts over the warps, then over
-  // the bins; publish the tile's count of the bin.
-  uint32_t total = 0;
+  // Bin b = thread b: its count in the tile goes out at once (the successors'
+  // look-back waits for it), then the exclusive scan over the bins and, per
+  // bin, over the warps: pairs[w][b].y becomes the tile-local slot of warp w's
+  // first item of bin b.
+  uint32_t total = 0, vcount = 0;
   if (tid < kBins) {
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) {
-      const uint32_t c = cnt[w * kBins + tid];
-      cnt[w * kBins + tid] = total;
-      total += c;
-    }
+    for (int w = 0; w < WARPS; ++w) total += pairs[w * kBins + tid].y;
+    vcount = total - (tid == mask ? static_cast<uint32_t>(TILE) - valid : 0u);
+    if (tid <= mask)
+      st_relaxed64(status + static_cast<size_t>(tile) * kBins + tid,
+                   tag(epoch, tile == 0 ? 2u : 1u, vcount));
   }
   uint32_t inc = total;
 #pragma unroll
@@ -218,15 +291,16 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   if (tid < kBins && lane == 31) warp_tot[warp] = inc;
   __syncthreads();
-  uint32_t vcount = 0;
   if (tid < kBins) {
-    uint32_t pre = 0;
-    for (unsigned w = 0; w < warp; ++w) pre += warp_tot[w];
-    bin_start[tid] = pre + inc - total;
-    vcount = total - (tid == mask ? static_cast<uint32_t>(TILE) - valid : 0u);
-    if (tid <= mask)
-      st_relaxed64(status + static_cast<size_t>(tile) * kBins + tid,
-                   tag(epoch, tile == 0 ? 2u : 1u, vcount));
+    uint32_t run = inc - total;
+    for (unsigned w = 0; w < warp; ++w) run += warp_tot[w];
+    bin_start[tid] = run;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      const uint32_t c = pairs[w * kBins + tid].y;
+      pairs[w * kBins + tid].y = run;
+      run += c;
+    }
   }
   __syncthreads();
 
@@ -234,25 +308,48 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t dgt = static_cast<uint32_t>(key[k] >> shift) & mask;
-    const uint32_t pos = bin_start[dgt] + wc[dgt] + rank[k];
+    const uint32_t pos = wp[dgt].y + rank[k];
     keys_s[pos] = key[k];
     pay_s[pos] = pay[k];
   }
 
-  // Decoupled look-back per bin: counts of the bin in all earlier tiles.
+  // Decoupled look-back per bin: counts of the bin in all earlier tiles. A
+  // whole wave of tiles publishes its aggregates at about the same time, so
+  // the nearest inclusive prefix sits many tiles back; each thread therefore
+  // reads kLook predecessors per round trip (independent loads, each a
+  // coalesced 256-byte request per warp) instead of one.
   if (tid <= mask) {
     uint32_t before = 0;
     if (tile > 0) {
-      int64_t t = static_cast<int64_t>(tile) - 1;
-      while (true) {
-        const unsigned long long w = ld_relaxed64(status + static_cast<size_t>(t) * kBins + tid);
-        if ((w >> 34) != epoch) {
-          __nanosleep(20);
-          continue;
+      constexpr int kLook = 8;
+      int64_t t = static_cast<int64_t>(tile) - 1;  // next predecessor to consume
+      bool done = false;
+      while (!done) {
+        unsigned long long w[kLook];
+#pragma unroll
+        for (int i = 0; i < kLook; ++i)
+          w[i] = t - i >= 0 ? ld_relaxed64(status + static_cast<size_t>(t - i) * kBins + tid)
+                            : tag(epoch, 2u, 0u);
+        bool stall = false;
+#pragma unroll
+        for (int i = 0; i < kLook; ++i) {
+          if (done || stall) continue;
+          if ((w[i] >> 34) != epoch) {
+            stall = true;  // not published yet: poll again from here
+          } else {
+            before += static_cast<uint32_t>(w[i]);
+            done = ((w[i] >> 32) & 3u) == 2u;
+          }
         }
-        before += static_cast<uint32_t>(w);
-        if (((w >> 32) & 3u) == 2u) break;
-        --t;
+        if (!done) {
+          // consumed entries: every ready one before the first unpublished
+          int used = 0;
+#pragma unroll
+          for (int i = kLook - 1; i >= 0; --i)
+            if ((w[i] >> 34) != epoch) used = i;
+          t -= stall ? used : kLook;
+          if (stall) __nanosleep(20);
+        }
       }
       st_relaxed64(status + static_cast<size_t>(tile) * kBins + tid,
                    tag(epoch, 2u, before + vcount));
@@ -263,21 +360,36 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   // Each bin's run goes out contiguous: consecutive slots -> consecutive
   // global positions.
-  for (uint32_t j = tid; j < valid; j += kThreads) {
-    const K kk = keys_s[j];
-    const uint32_t dgt = static_cast<uint32_t>(kk >> shift) & mask;
-    const uint32_t pos = gbase[dgt] + j;
-    if (DST == DST_ARRAYS) {
-      __stcs(static_cast<K*>(d.keys) + pos, kk);
-      __stcs(d.pay + pos, pay_s[j]);
-    } else if (DST == DST_UNPACK) {
+  {
+    K kk[ITEMS];
+    uint32_t pp[ITEMS];
 #pragma unroll
-      for (int q = 0; q < SPT_MAX_ORDER; ++q)
-        if (q < d.un.n)
-          __stcs(d.un.idx[q] + pos, static_cast<uint32_t>(kk >> d.un.shift[q]) & d.un.mask[q]);
-      __stcs(d.pay + pos, pay_s[j]);
-    } else {
-      __stcs(d.pay + pos, pay_s[j]);
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t j = tid + k * kThreads;
+      if (j < valid) {
+        kk[k] = keys_s[j];
+        pp[k] = pay_s[j];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t j = tid + k * kThreads;
+      if (j >= valid) continue;
+      const uint32_t dgt = static_cast<uint32_t>(kk[k] >> shift) & mask;
+      const uint32_t pos = gbase[dgt] + j;
+      if (DST == DST_ARRAYS) {
+        __stcs(static_cast<K*>(d.keys) + pos, kk[k]);
+        __stcs(d.pay + pos, pp[k]);
+      } else if (DST == DST_UNPACK) {
+#pragma unroll
+        for (int q = 0; q < SPT_MAX_ORDER; ++q)
+          if (q < d.un.n)
+            __stcs(d.un.idx[q] + pos,
+                   static_cast<uint32_t>(kk[k] >> d.un.shift[q]) & d.un.mask[q]);
+        __stcs(d.pay + pos, pp[k]);
+      } else {
+        __stcs(d.pay + pos, pp[k]);
+      }
     }
   }
 }
@@ -301,16 +413,17 @@ __global__ void pack_perm_kernel(PackSpec spec, const uint32_t* __restrict__ per
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 Digits plan_digits(uint32_t nbits) {
-  // equal digits of <= 8 bits; at least two passes, so that the first pass
+  // digits of <= 8 bits; at least two passes, so that the first pass
   // (which reads the caller's arrays) never writes into them
   Digits dg{};
   if (nbits == 0) nbits = 1;
   int passes = static_cast<int>((nbits + 7) / 8);
   if (passes < 2) passes = 2;
   dg.passes = passes;
+  // full 8-bit digits (their ballots unroll) and the remainder in the last
   uint32_t at = 0;
   for (int p = 0; p < passes; ++p) {
-    const uint32_t w = nbits / passes + (static_cast<uint32_t>(p) < nbits % passes ? 1u : 0u);
+    const uint32_t w = std::min<uint32_t>(8u, nbits - at);
     dg.shift[p] = at;
     dg.bits[p] = w;
     at += w;
@@ -320,7 +433,7 @@ Digits plan_digits(uint32_t nbits) {
 
 template <typename K>
 constexpr int items_for() {
-  return sizeof(K) == 8 ? 12 : 16;
+  return sizeof(K) == 8 ? SPT_RADIX_ITEMS64 : SPT_RADIX_ITEMS32;
 }
 
 template <typename K, int SRC, int DST>
@@ -328,7 +441,8 @@ int launch_pass(spt_ctx* ctx, const SrcDesc& s, const DstDesc& d, uint64_t n, ui
                 uint32_t bits, const uint32_t* base, uint32_t* ticket, cudaStream_t st) {
   constexpr int ITEMS = items_for<K>();
   constexpr size_t smem = onesweep_smem<K, ITEMS>();
-  auto kern = onesweep_kernel<K, SRC, DST, ITEMS>;
+  auto kern = bits == 8 ? onesweep_kernel<K, SRC, DST, ITEMS, 8>
+                        : onesweep_kernel<K, SRC, DST, ITEMS, 0>;
   SPT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));  // per device, cheap
   const uint64_t tile = static_cast<uint64_t>(kThreads) * ITEMS;
