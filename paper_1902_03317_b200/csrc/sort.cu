@@ -19,6 +19,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -90,6 +91,157 @@ __global__ void fptr_tail_kernel(uint32_t* fptr, const uint32_t* d_count32,
 __global__ void count_from_scan_kernel(const uint32_t* flags, const uint32_t* pos, uint64_t n,
                                        unsigned long long* out) {
   *out = n ? (unsigned long long)pos[n - 1] + flags[n - 1] : 0ull;
+}
+
+// build_fiber_index in one launch (P/src/tensor.cpp:92-120). The grid is a
+// few CTAs per SM; CTA r (ticket order) owns a contiguous range of 4096-entry
+// tiles. Sweep 1 counts the range's fiber heads, the CTA publishes the count
+// and gets its offset from one decoupled look-back over epoch-tagged 64-bit
+// count words (a per-tile look-back chain held 54% of the warps at the
+// barrier); sweep 2 re-reads the range (L2 hits: a range is ~100-200 KB),
+// scans each tile's head counts, compacts the head positions in shared memory
+// and writes them out coalesced. A tile is read as four warp-striped sweeps of
+// 128-bit loads over each non-mode index array; a lane's first entry is
+// compared with the previous lane's last by shuffle. The last range appends
+// fptr[nfibs] = nnz.
+constexpr int kFibThreads = 256, kFibQuads = 4, kFibTile = kFibThreads * kFibQuads * 4;
+
+template <bool VEC>
+__device__ __forceinline__ void fiber_tile_heads(const TupleCmp& t, uint64_t n, uint64_t tbase,
+                                                 unsigned tid, unsigned lane,
+                                                 uint32_t (&hd)[kFibQuads]) {
+#pragma unroll
+  for (int q = 0; q < kFibQuads; ++q) hd[q] = 0;
+#pragma unroll
+  for (int j = 0; j < SPT_MAX_ORDER; ++j) {
+    if (j >= t.n) continue;
+    const uint32_t* a = t.idx[j];
+    uint32_t v[kFibQuads][4];
+#pragma unroll
+    for (int q = 0; q < kFibQuads; ++q) {
+      const uint64_t e0 = tbase + q * (kFibThreads * 4) + tid * 4;
+      if (VEC && e0 + 4 <= n) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(a + e0));
+        v[q][0] = u.x, v[q][1] = u.y, v[q][2] = u.z, v[q][3] = u.w;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[q][c] = e0 + c < n ? a[e0 + c] : 0u;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kFibQuads; ++q) {
+      const uint64_t e0 = tbase + q * (kFibThreads * 4) + tid * 4;
+      uint32_t prev = __shfl_up_sync(0xffffffffu, v[q][3], 1);
+      if (lane == 0) prev = (e0 > 0 && e0 < n) ? __ldg(a + e0 - 1) : ~v[q][0];
+      hd[q] |= (v[q][0] != prev ? 1u : 0u) | (v[q][1] != v[q][0] ? 2u : 0u) |
+               (v[q][2] != v[q][1] ? 4u : 0u) | (v[q][3] != v[q][2] ? 8u : 0u);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kFibQuads; ++q) {
+    const uint64_t e0 = tbase + q * (kFibThreads * 4) + tid * 4;
+    const uint32_t vq = e0 >= n ? 0u : (n - e0 < 4 ? static_cast<uint32_t>(n - e0) : 4u);
+    if (e0 == 0 && vq) hd[q] |= 1u;  // entry 0 always starts a fiber
+    hd[q] &= (1u << vq) - 1u;
+  }
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kFibThreads)
+    fiber_index_kernel(TupleCmp t, uint64_t n, uint32_t ntiles, uint32_t tiles_per_cta,
+                       uint32_t* __restrict__ fptr, unsigned long long* status, uint32_t epoch,
+                       unsigned long long* tile_ctr, unsigned long long* d_count) {
+  constexpr int WARPS = kFibThreads / 32;
+  __shared__ uint32_t s_rank;
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t wsum[kFibQuads][WARPS];
+  __shared__ uint32_t out_s[kFibTile];
+  const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (tid == 0) {
+    const unsigned long long tk = atomicAdd(tile_ctr, 1ull);
+    if (tk == gridDim.x - 1) atomicExch(tile_ctr, 0ull);  // last ticket of this launch
+    s_rank = static_cast<uint32_t>(tk);
+  }
+  __syncthreads();
+  const uint32_t r = s_rank;
+  const uint32_t tile_lo = min(r * tiles_per_cta, ntiles);
+  const uint32_t tile_hi = min(tile_lo + tiles_per_cta, ntiles);
+  uint32_t hd[kFibQuads];
+
+  // sweep 1: the range's head count
+  uint32_t mine = 0;
+  for (uint32_t tile = tile_lo; tile < tile_hi; ++tile) {
+    fiber_tile_heads<VEC>(t, n, static_cast<uint64_t>(tile) * kFibTile, tid, lane, hd);
+#pragma unroll
+    for (int q = 0; q < kFibQuads; ++q) mine += __popc(hd[q]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if (lane == 0) wsum[0][warp] = mine;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t range_total = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) range_total += wsum[0][w];
+    const unsigned long long ep = static_cast<unsigned long long>(epoch) << 34;
+    if (lane == 0)
+      spt::st_relaxed64(status + r, ep | ((r == 0 ? 2ull : 1ull) << 32) | range_total);
+    unsigned long long base = 0;
+    if (r > 0) {
+      base = spt::lookback_count64_wide<8>(status, r, epoch);
+      if (lane == 0) spt::st_relaxed64(status + r, ep | (2ull << 32) | (base + range_total));
+    }
+    if (lane == 0) {
+      s_base = base;
+      if (r == gridDim.x - 1) {
+        fptr[base + range_total] = static_cast<uint32_t>(n);
+        if (d_count) *d_count = base + range_total;
+      }
+    }
+  }
+  __syncthreads();
+  unsigned long long base = s_base;
+
+  // sweep 2: positions
+  for (uint32_t tile = tile_lo; tile < tile_hi; ++tile) {
+    const uint64_t tbase = static_cast<uint64_t>(tile) * kFibTile;
+    fiber_tile_heads<VEC>(t, n, tbase, tid, lane, hd);
+    uint32_t inc[kFibQuads], cnt[kFibQuads];
+#pragma unroll
+    for (int q = 0; q < kFibQuads; ++q) {
+      cnt[q] = __popc(hd[q]);
+      inc[q] = cnt[q];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc[q], o);
+        if (lane >= o) inc[q] += u;
+      }
+      if (lane == 31) wsum[q][warp] = inc[q];
+    }
+    __syncthreads();
+    uint32_t total = 0;
+#pragma unroll
+    for (int q = 0; q < kFibQuads; ++q) {
+      uint32_t pre = total;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        if (w < static_cast<int>(warp)) pre += wsum[q][w];
+        total += wsum[q][w];
+      }
+      uint32_t pos = pre + inc[q] - cnt[q];
+      const uint32_t e0 = static_cast<uint32_t>(tbase) + q * (kFibThreads * 4) + tid * 4;
+      uint32_t h = hd[q];
+      while (h) {
+        out_s[pos++] = e0 + (__ffs(h) - 1);
+        h &= h - 1;
+      }
+    }
+    __syncthreads();
+    uint32_t* dst = fptr + base;
+    for (uint32_t i = tid; i < total; i += kFibThreads) spt::st_stream(dst + i, out_s[i]);
+    base += total;
+    __syncthreads();  // out_s and wsum are reused by the next tile
+  }
 }
 
 inline unsigned grid_of(spt_ctx* ctx, uint64_t n) {
@@ -299,32 +451,34 @@ int spt_fiber_index(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint32_t* d_f
   TupleCmp t{};
   for (uint32_t d = 0; d < x->order; ++d)
     if (d != mode) t.idx[t.n++] = x->idx[d];
-  size_t temp = 0;
-  thrust::counting_iterator<uint32_t> it(0);
-  SPT_CUDA(cub::DeviceSelect::Flagged(nullptr, temp, it, (uint32_t*)nullptr, d_fptr,
-                                      (uint32_t*)nullptr, static_cast<int64_t>(n), st));
-  const size_t fb = align_up((n ? n : 1) * 4);
   void* scratch;
-  SPT_TRY(spt::ctx_scratch(ctx, fb + align_up(temp) + 256, &scratch));
-  char* base = static_cast<char*>(scratch);
-  uint32_t* flags_d = reinterpret_cast<uint32_t*>(base);
-  void* tmp = base + fb;
-  uint32_t* cnt32 = reinterpret_cast<uint32_t*>(base + fb + align_up(temp));
+  SPT_TRY(spt::ctx_scratch(ctx, 256, &scratch));
+  uint32_t* cnt32 = static_cast<uint32_t*>(scratch);
   unsigned long long* cnt64 = reinterpret_cast<unsigned long long*>(cnt32 + 2);
+  unsigned long long* count_out =
+      d_nfibs ? reinterpret_cast<unsigned long long*>(d_nfibs) : cnt64;
   if (n > 0) {
-    head_flags_kernel<<<grid_of(ctx, n), 256, 0, st>>>(t, flags_d, n);
+    const uint32_t ntiles = static_cast<uint32_t>((n + kFibTile - 1) / kFibTile);
+    const uint32_t grid = std::min<uint32_t>(ntiles, static_cast<uint32_t>(ctx->num_sms) * 5u);
+    const uint32_t tpc = (ntiles + grid - 1) / grid;
+    unsigned long long* status;
+    SPT_TRY(spt::ctx_status64(ctx, grid, &status));
+    uint32_t epoch;
+    SPT_TRY(spt::ctx_lookback(ctx, 0, 0, &epoch));
+    bool vec = true;
+    for (int j = 0; j < t.n; ++j) vec = vec && spt::aligned16(t.idx[j]);
+    if (vec)
+      fiber_index_kernel<true><<<grid, kFibThreads, 0, st>>>(t, n, ntiles, tpc, d_fptr, status,
+                                                            epoch, ctx->d_tile_ctr, count_out);
+    else
+      fiber_index_kernel<false><<<grid, kFibThreads, 0, st>>>(t, n, ntiles, tpc, d_fptr, status,
+                                                             epoch, ctx->d_tile_ctr, count_out);
     SPT_LAUNCHED(ctx);
-    SPT_CUDA(cub::DeviceSelect::Flagged(tmp, temp, it, flags_d, d_fptr, cnt32,
-                                        static_cast<int64_t>(n), st));
-    ctx->launches += 2;
   } else {
     SPT_CUDA(cudaMemsetAsync(cnt32, 0, 4, st));
+    fptr_tail_kernel<<<1, 1, 0, st>>>(d_fptr, cnt32, count_out, n);
+    SPT_LAUNCHED(ctx);
   }
-  fptr_tail_kernel<<<1, 1, 0, st>>>(d_fptr, cnt32,
-                                    d_nfibs ? reinterpret_cast<unsigned long long*>(d_nfibs)
-                                            : cnt64,
-                                    n);
-  SPT_LAUNCHED(ctx);
   if (h_nfibs) {
     SPT_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_nfibs ? (void*)d_nfibs : (void*)cnt64, 8,
                              cudaMemcpyDeviceToHost, st));
