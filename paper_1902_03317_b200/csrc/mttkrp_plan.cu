@@ -46,6 +46,8 @@
 // memset and every element is written exactly once.
 #include <cub/cub.cuh>
 
+#include <type_traits>
+
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -144,6 +146,19 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "r"(a));
   return v;
+}
+
+// mbar_wait on a precomputed shared-space address.
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SPT_PLAN_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra SPT_PLAN_WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(spt::kMbarSuspendNs)
+      : "memory");
 }
 
 // Lane 0 of a warp: stage block c of each of the warp's lane groups (one
@@ -262,6 +277,7 @@ __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(P
   for (int i = tid; i <= C::GROUPS; i += C::THREADS)
     s_bnd[i] = gbound<CH>(p.nnz, p.total_groups, blockIdx.x * C::GROUPS + i);
   unsigned long long* wbar = bars + warp * kNB;
+  const uint32_t wbar_a = spt::smem_addr(wbar);  // hoisted: no cvta in the loop
   if (lane == 0) {
 #pragma unroll
     for (int b = 0; b < kNB; ++b) spt::mbar_init(&wbar[b], 1);
@@ -345,12 +361,13 @@ __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(P
 
   const uint32_t niter = (mlen + U - 1) / U;
   const uint32_t gbase = wring + g * GS * 4;
-  for (uint32_t it = 0; it < niter; ++it) {
+  // FULL: every group of the warp has all U entries of this iteration (true
+  // except in the ranges' last iterations): the validity tests drop out.
+  auto iterate = [&](uint32_t it, auto full_c) {
+    constexpr bool FULL = decltype(full_c)::value;
     const uint32_t e0 = it * U;
     const uint32_t c = e0 / CH, o = e0 % CH, b = c % kNB;
-    if (o == 0) {
-      spt::mbar_wait(&wbar[b], (c / kNB) & 1u);
-    }
+    if (o == 0) mbar_wait_a(wbar_a + b * 8, (c / kNB) & 1u);
     const uint32_t sb = gbase + b * GPW * GS * 4 + o * 4;
     uint32_t rr[U], id[NM1][U];
     float vv[U];
@@ -371,7 +388,7 @@ __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(P
     bool ok[U], nr[U], nm[NMID][U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ok[u] = e0 + u < len;
+      ok[u] = FULL || e0 + u < len;
       nr[u] = rr[u] != (u ? rr[u - 1] : prow);
       bool ch = nr[u];
 #pragma unroll
@@ -395,7 +412,7 @@ __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(P
         M[j][u] = gather_row<CB, HOT>(ok[u] && nm[j][u], id[j][u], hot_q, fb[j], rb);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (!ok[u]) break;
+      if (!FULL && !ok[u]) break;
       if (nr[u]) {  // row change: the finished row goes out
         fold();
         if (cur != kNoRow) {
@@ -426,7 +443,13 @@ __global__ void __launch_bounds__(PCfg<NM1, G>::THREADS, 1) mttkrp_plan_kernel(P
         stage_chunk<NM1, G>(p, wring + b * GPW * GS * 4, &wbar[b], wbnd, c + kNB, pol);
       }
     }
-  }
+  };
+  uint32_t minlen = len;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) minlen = min(minlen, __shfl_xor_sync(0xffffffffu, minlen, o));
+  const uint32_t nfull = minlen / U;
+  for (uint32_t it = 0; it < nfull; ++it) iterate(it, std::true_type{});
+  for (uint32_t it = nfull; it < niter; ++it) iterate(it, std::false_type{});
   uint32_t trow = kNoRow;
   if (cur != kNoRow) {
     if (first) {

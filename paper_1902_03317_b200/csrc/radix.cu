@@ -466,19 +466,19 @@ struct Buffers {
 };
 
 template <typename K>
-int carve(spt_ctx* ctx, uint64_t n, Buffers* b, cudaStream_t st) {
+int carve(spt_ctx* ctx, uint64_t n, int npay, Buffers* b, cudaStream_t st) {
   const size_t kb = align_up(n * sizeof(K)), pb = align_up(n * 4);
   const size_t hb = align_up(kMaxPasses * kBins * 4);
   void* scratch;
-  SPT_TRY(ctx_scratch(ctx, 2 * kb + 2 * pb + 2 * hb + 256, &scratch));
+  SPT_TRY(ctx_scratch(ctx, 2 * kb + npay * pb + 2 * hb + 256, &scratch));
   char* p = static_cast<char*>(scratch);
   b->key[0] = p;
   b->key[1] = p + kb;
   b->pay[0] = reinterpret_cast<uint32_t*>(p + 2 * kb);
-  b->pay[1] = reinterpret_cast<uint32_t*>(p + 2 * kb + pb);
-  b->hist = reinterpret_cast<uint32_t*>(p + 2 * kb + 2 * pb);
-  b->base = reinterpret_cast<uint32_t*>(p + 2 * kb + 2 * pb + hb);
-  b->ticket = reinterpret_cast<uint32_t*>(p + 2 * kb + 2 * pb + 2 * hb);
+  b->pay[1] = npay > 1 ? reinterpret_cast<uint32_t*>(p + 2 * kb + pb) : nullptr;
+  b->hist = reinterpret_cast<uint32_t*>(p + 2 * kb + npay * pb);
+  b->base = reinterpret_cast<uint32_t*>(p + 2 * kb + npay * pb + hb);
+  b->ticket = reinterpret_cast<uint32_t*>(p + 2 * kb + npay * pb + 2 * hb);
   // hist and ticket are adjacent to base: one memset clears hist; tickets apart
   SPT_CUDA(cudaMemsetAsync(b->hist, 0, hb, st));
   SPT_CUDA(cudaMemsetAsync(b->ticket, 0, 256, st));
@@ -501,7 +501,7 @@ int tuple_inplace(spt_ctx* ctx, const PackSpec& pack, const UnpackSpec& unpack, 
                   uint64_t n, uint32_t nbits, cudaStream_t st) {
   const Digits dg = plan_digits(nbits);
   Buffers b;
-  SPT_TRY(carve<K>(ctx, n, &b, st));
+  SPT_TRY(carve<K>(ctx, n, 2, &b, st));
   SrcDesc s0{};
   s0.pack = pack;
   s0.pay = vals;
@@ -543,10 +543,20 @@ template <typename K>
 int chunk_perm(spt_ctx* ctx, const PackSpec& pack, const uint32_t* perm_in, uint32_t* perm_out,
                uint64_t n, uint32_t nbits, cudaStream_t st) {
   const Digits dg = plan_digits(nbits);
+  const int P = dg.passes;
+  // Payload targets, chosen backwards from the last pass (-> perm_out): the
+  // passes alternate between perm_out itself and one scratch array, so a
+  // 1B-entry sort keeps one 4 GB payload buffer instead of two. Only a later
+  // chunk (perm_in == perm_out is read by pass 0) with an odd pass count needs
+  // a second one, for pass 0's output.
+  const bool hazard = perm_in != nullptr && (P - 1) % 2 == 0;
   Buffers b;
-  SPT_TRY(carve<K>(ctx, n, &b, st));
+  SPT_TRY(carve<K>(ctx, n, hazard ? 2 : 1, &b, st));
+  auto pay_target = [&](int p) -> uint32_t* {
+    if (p == 0 && hazard) return b.pay[1];
+    return (P - 1 - p) % 2 == 0 ? perm_out : b.pay[0];
+  };
   SrcDesc s0{};
-  int cur = 0;
   if (perm_in) {
     // later chunk: the keys of the entries in their current order (one
     // gather), then plain passes carrying the permutation
@@ -560,22 +570,18 @@ int chunk_perm(spt_ctx* ctx, const PackSpec& pack, const uint32_t* perm_in, uint
     s0.pack = pack;
     SPT_TRY((histogram<K, SRC_PACK_IOTA>(ctx, s0, n, dg, b, st)));
   }
-  for (int p = 0; p < dg.passes; ++p) {
-    const bool first = p == 0, last = p == dg.passes - 1;
+  for (int p = 0; p < P; ++p) {
+    const bool first = p == 0, last = p == P - 1;
     SrcDesc s{};
     DstDesc d{};
     if (first) {
       s = s0;
     } else {
-      s.keys = b.key[cur ^ 1];
-      s.pay = b.pay[cur ^ 1];
+      s.keys = b.key[(p - 1) & 1];
+      s.pay = pay_target(p - 1);
     }
-    if (last) {
-      d.pay = perm_out;
-    } else {
-      d.keys = b.key[cur];
-      d.pay = b.pay[cur];
-    }
+    d.keys = last ? nullptr : b.key[p & 1];
+    d.pay = pay_target(p);
     const uint32_t* base = b.base + p * kBins;
     if (first && !perm_in)
       SPT_TRY((launch_pass<K, SRC_PACK_IOTA, DST_ARRAYS>(ctx, s, d, n, dg.shift[p], dg.bits[p],
@@ -586,7 +592,6 @@ int chunk_perm(spt_ctx* ctx, const PackSpec& pack, const uint32_t* perm_in, uint
     else
       SPT_TRY((launch_pass<K, SRC_ARRAYS, DST_ARRAYS>(ctx, s, d, n, dg.shift[p], dg.bits[p], base,
                                                       b.ticket + p, st)));
-    cur ^= 1;
   }
   return SPT_OK;
 }
