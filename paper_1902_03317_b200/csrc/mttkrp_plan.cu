@@ -70,6 +70,11 @@ struct spt_mttkrp_plan {
   uint32_t* gprow = nullptr;
   unsigned int* done = nullptr;
   uint32_t grid = 0;
+  // The arrays come from the context's stream-ordered pool and are released
+  // on the stream that used the plan last: creating and destroying a plan
+  // never synchronises the device (a host caller's copies on other streams
+  // keep running under the plan builds).
+  mutable cudaStream_t last = nullptr;
 };
 
 namespace {
@@ -684,7 +689,7 @@ int plan_select_hot(spt_ctx* ctx, spt_mttkrp_plan* pl, const uint32_t* row, uint
     uint2* dsel = nullptr;
     SPT_CUDA(spt::tmp_alloc(ctx, &dsel, nsel * sizeof(uint2), st));
     SPT_CUDA(cudaMemcpyAsync(dsel, sel.data(), nsel * sizeof(uint2), cudaMemcpyHostToDevice, st));
-    SPT_CUDA(cudaMalloc(&pl->hot, pl->nhot * sizeof(uint2)));
+    SPT_CUDA(spt::tmp_alloc(ctx, &pl->hot, pl->nhot * sizeof(uint2), st));
     SPT_CUDA(cudaMemcpyAsync(pl->hot, dsel, pl->nhot * sizeof(uint2), cudaMemcpyDeviceToDevice,
                              st));
     // id -> encoded id maps reuse the histogram words (the sort left them permuted)
@@ -703,13 +708,16 @@ int plan_select_hot(spt_ctx* ctx, spt_mttkrp_plan* pl, const uint32_t* row, uint
 
 void plan_free(spt_mttkrp_plan* pl) {
   if (!pl) return;
-  if (pl->blk) cudaFree(pl->blk);
-  if (pl->hot) cudaFree(pl->hot);
-  if (pl->part) cudaFree(pl->part);
-  if (pl->part_row) cudaFree(pl->part_row);
-  if (pl->gpart) cudaFree(pl->gpart);
-  if (pl->gprow) cudaFree(pl->gprow);
-  if (pl->done) cudaFree(pl->done);
+  // wait for the plan's last user only; an invalid (destroyed) stream falls
+  // back to the whole device and the legacy stream
+  if (cudaStreamSynchronize(pl->last) != cudaSuccess) {
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    pl->last = nullptr;
+  }
+  void* arrays[] = {pl->blk, pl->hot, pl->part, pl->part_row, pl->gpart, pl->gprow, pl->done};
+  for (void* a : arrays)
+    if (a) cudaFreeAsync(a, pl->last);
   delete pl;
 }
 
@@ -818,12 +826,15 @@ extern "C" int spt_mttkrp_plan_create(spt_ctx* ctx, const spt_coo* x, uint32_t m
   pl->nblk = (x->nnz + pl->CH - 1) / pl->CH;
   pl->grid = static_cast<uint32_t>(std::min(ctx->num_sms, kFoldCap / 2));
   const size_t groups = (size_t)pl->grid * v.groups;
-  if ((pl->nblk && cudaMalloc(&pl->blk, pl->nblk * pl->NA * pl->CH * 4) != cudaSuccess) ||
-      cudaMalloc(&pl->part, (size_t)2 * pl->grid * pl->CB * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&pl->part_row, (size_t)2 * pl->grid * 4) != cudaSuccess ||
-      cudaMalloc(&pl->gpart, 2 * groups * pl->CB * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&pl->gprow, 2 * groups * 4) != cudaSuccess ||
-      cudaMalloc(&pl->done, 4) != cudaSuccess) {
+  pl->last = st;
+  if ((pl->nblk &&
+       spt::tmp_alloc(ctx, &pl->blk, pl->nblk * pl->NA * pl->CH * 4, st) != cudaSuccess) ||
+      spt::tmp_alloc(ctx, &pl->part, (size_t)2 * pl->grid * pl->CB * sizeof(double), st) !=
+          cudaSuccess ||
+      spt::tmp_alloc(ctx, &pl->part_row, (size_t)2 * pl->grid * 4, st) != cudaSuccess ||
+      spt::tmp_alloc(ctx, &pl->gpart, 2 * groups * pl->CB * sizeof(double), st) != cudaSuccess ||
+      spt::tmp_alloc(ctx, &pl->gprow, 2 * groups * 4, st) != cudaSuccess ||
+      spt::tmp_alloc(ctx, &pl->done, 4, st) != cudaSuccess) {
     cudaGetLastError();
     plan_free(pl);
     return spt::set_error(SPT_ENOMEM, "mttkrp_plan: out of device memory");
@@ -845,7 +856,6 @@ extern "C" int spt_mttkrp_plan_create(spt_ctx* ctx, const spt_coo* x, uint32_t m
 extern "C" void spt_mttkrp_plan_destroy(spt_mttkrp_plan* plan) {
   if (!plan) return;
   cudaSetDevice(plan->device);
-  cudaDeviceSynchronize();
   plan_free(plan);
 }
 
@@ -885,6 +895,7 @@ extern "C" int spt_mttkrp_plan_exec(spt_ctx* ctx, const spt_mttkrp_plan* pl,
   if (!spt::aligned16(d_out))
     return spt::set_error(SPT_EINVAL, "mttkrp: plan path needs a 16-byte-aligned output");
   cudaStream_t st = spt::as_stream(stream);
+  pl->last = st;
   if (I == 0) return SPT_OK;
   if (pl->nnz == 0) {
     SPT_CUDA(cudaMemsetAsync(d_out, 0, (size_t)I * pl->R * sizeof(float), st));

@@ -2,7 +2,8 @@
 (the reference's situation: SparseTensorCOO<float> lives in std::vectors).
 
 `PinnedCOO` is a page-locked host mirror of a COO tensor; `Pipeline` owns
-three CUDA streams (H2D copy, kernels, D2H copy) so that, with chunked
+the CUDA streams (H2D copy, kernels -- a second kernel stream for work that
+is independent of the first -- and D2H copy) so that, with chunked
 uploads, PCIe host->device, the kernels and PCIe device->host all run at
 once (PCIe is full duplex). Only copies live here; every kernel still goes
 through `ops` / the C-ABI.
@@ -96,16 +97,17 @@ class Pipeline:
         self.device = torch.device("cuda", device) if isinstance(device, int) else device
         self.h2d = torch.cuda.Stream(self.device)
         self.cmp = torch.cuda.Stream(self.device)
+        self.cmp2 = torch.cuda.Stream(self.device)
         self.d2h = torch.cuda.Stream(self.device)
 
     def begin(self) -> None:
         cur = torch.cuda.current_stream(self.device)
-        for s in (self.h2d, self.cmp, self.d2h):
+        for s in (self.h2d, self.cmp, self.cmp2, self.d2h):
             s.wait_stream(cur)
 
     def end(self) -> None:
         cur = torch.cuda.current_stream(self.device)
-        for s in (self.h2d, self.cmp, self.d2h):
+        for s in (self.h2d, self.cmp, self.cmp2, self.d2h):
             cur.wait_stream(s)
 
     @staticmethod
