@@ -81,7 +81,10 @@ namespace {
 
 constexpr uint32_t kHot = 0x80000000u;  // id field holds a shared-memory slot
 constexpr uint32_t kNoRow = 0xFFFFFFFFu;
-constexpr int kW = 16;  // warps per CTA: 128 registers, no spilled gather
+#ifndef SPT_PLAN_WARPS
+#define SPT_PLAN_WARPS 16
+#endif
+constexpr int kW = SPT_PLAN_WARPS;  // warps per CTA: 128 registers, no spilled gather
 // (L2 prefetching of the next block's rows -- per-lane prefetch.global.L2, or
 // a dedicated warp issuing cp.async.cg L2::128B fills -- measured slower: C5
 // 25.7 vs 20.6 ms, C4 3.55 vs 2.53 ms.)
