@@ -65,7 +65,7 @@ typedef enum spt_mttkrp_strategy {
                                (R % 16 == 0) or a mode-leading sorted copy: always
                                deterministic, fp64 accumulation (the 1e-5 contract) */
   SPT_MTTKRP_SEGMENTED = 0, /* mode-sorted input; one writer per output row; deterministic;
-                               tile shape (CTA / warp) picked by size */
+                               launch shape (one wave / warp tiles / CTA tiles) picked by size */
   SPT_MTTKRP_ATOMIC = 1,    /* any order; vector red.global.add into a zeroed output
                                (fp32 sums in arrival order: the 1e-4 class, only on request) */
   SPT_MTTKRP_SEGMENTED_CTA = 2,  /* segmented, forced 2048-entry CTA tiles */

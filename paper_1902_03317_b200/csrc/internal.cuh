@@ -109,6 +109,12 @@ int mttkrp_sorted_copy(spt_ctx* ctx, const spt_coo* x, const float* const* d_fac
                        const uint64_t* rows, const uint64_t* cols, uint32_t mode, float* d_out,
                        unsigned flags, void* stream);
 
+// One-wave segmented MTTKRP for small mode-sorted inputs (mttkrp_ow.cu).
+bool mttkrp_onewave_ok(const spt_coo* x, uint64_t R, const float* const* d_factors, uint32_t mode,
+                       const float* d_out);
+int mttkrp_onewave(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors, uint32_t mode,
+                   uint32_t R, float* d_out, cudaStream_t st);
+
 }  // namespace spt
 
 // ---------------------------------------------------------------------------

@@ -2098,6 +2098,13 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
   // Warp tiles win in the latency-bound small-problem regime (C1: 1M nnz,
   // 29 vs 37 us); from ~2M nnz the persistent CTA-tile kernel wins (4M: 82 vs
   // 94 us, C4 shape at 8M: 301 vs 528 us).
+  // Small inputs: one resident wave, a contiguous share per warp, no tile
+  // look-back (mttkrp_ow.cu; C1: ~2x the warp tiles).
+  if (strategy == SPT_MTTKRP_SEGMENTED && spt::mttkrp_onewave_ok(x, R, d_factors, mode, d_out)) {
+    SPT_TRY(spt::mttkrp_onewave(ctx, x, d_factors, mode, static_cast<uint32_t>(R), d_out, st));
+    if (flags & SPT_FLAG_ASYNC) return SPT_OK;
+    return spt::sync_and_check(ctx, st);
+  }
   if (strategy == SPT_MTTKRP_SEGMENTED)
     strategy = x->nnz <= 1500000 ? SPT_MTTKRP_SEGMENTED_WARP : SPT_MTTKRP_SEGMENTED_CTA;
 

@@ -1,0 +1,381 @@
+// One-wave segmented MTTKRP for small inputs (C1: 1M nonzeros, R = 16).
+//
+// Reference: seq::mttkrp / par::mttkrp (P/src/kernels_seq.cpp:153-174,
+// P/src/kernel_detail.hpp:176-188), input sorted with the output mode leading.
+//
+// At this size the tiled kernels of mttkrp.cu are a latency chain (ticket ->
+// staging -> 8 dependent gather batches -> fold -> look-back, ~28 us for a
+// 5 us transfer). Here the whole grid is one resident wave and every warp owns
+// one contiguous, equal share of the entries -- no tickets, no tile look-back:
+//   * a warp first pulls its whole share of entry words into shared memory
+//     with cp.async (every word in flight at once: one DRAM round trip instead
+//     of one per iteration), in chunks of kOwChunk entries for larger inputs;
+//   * a warp step covers 32/G entries (G lanes per factor row, one or two
+//     float4 slices each); U steps are gathered at once (one L1/L2 round trip
+//     per iteration);
+//   * each term is val * F_d0 * F_d1 ... in fp32, d ascending, exactly the
+//     reference's product; a lane group accumulates its entries of the current
+//     row in fp64 (fp32 across the <= U terms of one iteration);
+//   * when a step's entries are not all of the current row (rare: a warp's
+//     share holds a few rows), the step is replayed entry by entry and finished
+//     rows are reduced over the lane groups by a fixed shuffle tree;
+//   * rows strictly inside a warp's share are written once; its first and last
+//     row go to two fp64 partial slots (slot 0 flagged when the row continues
+//     the previous share's), and a second small kernel sums each row's run of
+//     slots in slot order. Rows without entries are zero-filled
+//     by the warp whose share spans the gap. Deterministic: the split and both
+//     summation orders are fixed by (nnz, grid).
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace {
+
+constexpr int kOwThreads = 256;
+constexpr int kOwWarps = kOwThreads / 32;
+constexpr int kOwU = 4;
+constexpr int kOwChunk = 288;  // entries of a share staged at a time (C1's share: 282)
+constexpr uint32_t kNoRow = 0xFFFFFFFFu;
+constexpr uint32_t kContinues = 0x80000000u;  // slot-0 row id flag: the row began in an earlier share
+
+struct OwParams {
+  const uint32_t* out_idx;
+  const uint32_t* oidx[SPT_MAX_ORDER - 1];
+  const float* ofac[SPT_MAX_ORDER - 1];
+  const float* val;
+  float* out;
+  uint32_t nnz, rows, R, nwarps;
+  double* part;    // [2 * nwarps][R]
+  uint32_t* prow;  // [2 * nwarps]
+  unsigned long long* err;
+};
+
+__device__ __forceinline__ uint32_t share_cut(uint32_t nnz, uint32_t shares, uint32_t w) {
+  if (w >= shares) return nnz;
+  return static_cast<uint32_t>(static_cast<uint64_t>(nnz) * w / shares) & ~3u;
+}
+
+__device__ __forceinline__ void ow_zero_rows(float* out, uint32_t r0, uint32_t r1, uint32_t R,
+                                             unsigned lane) {
+  if (r0 >= r1) return;
+  float4* o = reinterpret_cast<float4*>(out + static_cast<size_t>(r0) * R);
+  const size_t n4 = static_cast<size_t>(r1 - r0) * R / 4;
+  for (size_t i = lane; i < n4; i += 32) __stcs(o + i, make_float4(0.f, 0.f, 0.f, 0.f));
+}
+
+// G lanes per factor row, V float4 slices (4V columns) per lane: R = 4 G V.
+template <int NM1, int G, int V>
+__global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
+  constexpr int EPW = 32 / G;  // entries per warp step
+  constexpr int U = kOwU / V;  // steps gathered at once
+  constexpr int C2 = 2 * V;    // float2 pairs per lane
+  const unsigned lane = threadIdx.x & 31u, g = lane / G, q = lane % G;
+  const uint32_t w = blockIdx.x * kOwWarps + (threadIdx.x >> 5);
+  // equal shares cut at multiples of 4 entries: every array's piece of a share
+  // starts 16-byte aligned (16-byte cp.async.cg, which also keeps the entry
+  // stream out of L1 -- that is for the factor rows)
+  const uint32_t lo = share_cut(p.nnz, p.nwarps, w), hi = share_cut(p.nnz, p.nwarps, w + 1);
+  uint32_t* myrow = p.prow + 2 * w;
+  double* mypart = p.part + static_cast<size_t>(2 * w) * p.R + q * 4 * V;
+  if (lo >= hi) {
+    if (lane == 0) myrow[0] = myrow[1] = kNoRow;
+    return;
+  }
+  const float* fq[NM1];
+#pragma unroll
+  for (int j = 0; j < NM1; ++j) fq[j] = p.ofac[j] + q * 4 * V;
+
+  uint32_t cur = kNoRow;       // current row (warp-uniform)
+  int flushed = 0;             // rows finished so far
+  double acc[2 * C2];
+  float2 ra[C2];
+#pragma unroll
+  for (int c = 0; c < C2; ++c) {
+    acc[2 * c] = acc[2 * c + 1] = 0.0;
+    ra[c] = make_float2(0.f, 0.f);
+  }
+  // rows before the share's first row that no earlier share ends in
+  const uint32_t prev_row = lo ? __ldg(p.out_idx + lo - 1) : kNoRow;
+  uint32_t gap = lo ? prev_row + 1 : 0;
+  const bool first_continues = lo && prev_row == __ldg(p.out_idx + lo);
+
+  auto fold = [&]() {
+#pragma unroll
+    for (int c = 0; c < C2; ++c) {
+      acc[2 * c] += static_cast<double>(ra[c].x), acc[2 * c + 1] += static_cast<double>(ra[c].y);
+      ra[c] = make_float2(0.f, 0.f);
+    }
+  };
+  // The finished row `cur`: sum the lane groups' parts (fixed xor tree) and
+  // write it -- the share's first row to slot 0 (it may continue an earlier
+  // share's last row), later ones to the output.
+  auto finish = [&](bool last) {
+    fold();
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) {
+#pragma unroll
+      for (int c = 0; c < 2 * C2; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    }
+    if (flushed == 0 || last) {
+      const int slot = flushed == 0 ? 0 : 1;
+      if (g == 0) {
+        double* d = mypart + static_cast<size_t>(slot) * p.R;
+#pragma unroll
+        for (int c = 0; c < C2; ++c)
+          *reinterpret_cast<double2*>(d + 2 * c) = make_double2(acc[2 * c], acc[2 * c + 1]);
+      }
+      if (lane == 0) myrow[slot] = (slot == 0 && first_continues) ? (cur | kContinues) : cur;
+    } else if (g == 0) {
+      float* o = p.out + static_cast<size_t>(cur) * p.R + q * 4 * V;
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        __stcs(reinterpret_cast<float4*>(o) + k,
+               make_float4(static_cast<float>(acc[4 * k]), static_cast<float>(acc[4 * k + 1]),
+                           static_cast<float>(acc[4 * k + 2]),
+                           static_cast<float>(acc[4 * k + 3])));
+    }
+    ++flushed;
+#pragma unroll
+    for (int c = 0; c < 2 * C2; ++c) acc[c] = 0.0;
+  };
+
+  // the share's entry words, staged per warp: [row | ids.. | val][kOwChunk]
+  extern __shared__ __align__(16) uint32_t ow_smem[];
+  uint32_t* sw = ow_smem + (threadIdx.x >> 5) * (NM1 + 2) * kOwChunk;
+  const uint32_t sw_a = spt::smem_addr(sw);
+  for (uint32_t c0 = lo; c0 < hi; c0 += kOwChunk) {
+    const uint32_t n = min(static_cast<uint32_t>(kOwChunk), hi - c0);
+    __syncwarp();  // the previous chunk is consumed
+    for (uint32_t i = lane * 4; i < n; i += 128) {
+      const uint32_t d = sw_a + i * 4;
+      if (i + 4 <= n) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d),
+                     "l"(p.out_idx + c0 + i));
+#pragma unroll
+        for (int j = 0; j < NM1; ++j)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                           d + (1 + j) * kOwChunk * 4),
+                       "l"(p.oidx[j] + c0 + i));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         d + (NM1 + 1) * kOwChunk * 4),
+                     "l"(p.val + c0 + i));
+      } else {
+        for (uint32_t k = i; k < n; ++k) {
+          const uint32_t dk = sw_a + k * 4;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dk),
+                       "l"(p.out_idx + c0 + k));
+#pragma unroll
+          for (int j = 0; j < NM1; ++j)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             dk + (1 + j) * kOwChunk * 4),
+                         "l"(p.oidx[j] + c0 + k));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                           dk + (NM1 + 1) * kOwChunk * 4),
+                       "l"(p.val + c0 + k));
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    for (uint32_t b0 = 0; b0 < n; b0 += U * EPW) {
+      float4 F[NM1][U][V];
+      uint32_t r[U];
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = b0 + u * EPW + g;
+        const bool ok = i < n;
+        r[u] = ok ? sw[i] : kNoRow;
+        v[u] = ok ? __uint_as_float(sw[(NM1 + 1) * kOwChunk + i]) : 0.f;
+#pragma unroll
+        for (int j = 0; j < NM1; ++j) {
+          const float4* row = reinterpret_cast<const float4*>(
+              fq[j] + static_cast<size_t>(ok ? sw[(1 + j) * kOwChunk + i] : 0u) * p.R);
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            F[j][u][k] = ok ? __ldg(row + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        // val * F_d0 * F_d1 ... (d ascending): each term is bit-identical to
+        // the reference's (packed FMUL2/FFMA2 measured no faster here)
+        float2 t[C2];
+#pragma unroll
+        for (int c = 0; c < C2; ++c) t[c] = make_float2(v[u], v[u]);
+#pragma unroll
+        for (int j = 0; j < NM1; ++j)
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            t[2 * k].x *= F[j][u][k].x, t[2 * k].y *= F[j][u][k].y;
+            t[2 * k + 1].x *= F[j][u][k].z, t[2 * k + 1].y *= F[j][u][k].w;
+          }
+        const bool valid = r[u] != kNoRow;
+        if (__all_sync(0xffffffffu, !valid || r[u] == cur)) {
+          // invalid entries carry zero terms
+#pragma unroll
+          for (int c = 0; c < C2; ++c) ra[c].x += t[c].x, ra[c].y += t[c].y;
+        } else {
+          // a row boundary (or the share's first entry) inside this step
+          for (int e = 0; e < EPW; ++e) {
+            const uint32_t re = __shfl_sync(0xffffffffu, r[u], e * G);
+            if (re == kNoRow) break;
+            if (re != cur) {
+              if (cur != kNoRow) {
+                if (re < cur && lane == 0)
+                  atomicMin(p.err + 2, static_cast<unsigned long long>(c0 + b0 + u * EPW + e));
+                finish(false);
+                gap = cur + 1;
+              } else if (gap > re + 1 && lane == 0) {  // the previous share ends in a later row
+                atomicMin(p.err + 2, static_cast<unsigned long long>(lo));
+              }
+              ow_zero_rows(p.out, gap, re, p.R, lane);
+              cur = re;
+            }
+            if (static_cast<int>(g) == e) {
+#pragma unroll
+              for (int c = 0; c < C2; ++c) ra[c].x += t[c].x, ra[c].y += t[c].y;
+            }
+          }
+        }
+      }
+      fold();
+    }
+  }
+  finish(true);
+  if (flushed == 1 && lane == 0) myrow[1] = kNoRow;  // the whole share was one row
+  if (hi == p.nnz) ow_zero_rows(p.out, cur + 1, p.rows, p.R, lane);
+}
+
+// Sum each row's run of partial slots in slot order. One thread per (slot,
+// column); the run's first slot -- a slot 1, or a slot 0 whose row does not
+// continue the previous share's -- does the work: its own part plus the slot 0
+// of the following shares for as long as they continue the row (a share whose
+// slot 1 is used ends the run: its last row is another one).
+__global__ void ow_fold_kernel(const double* __restrict__ part, const uint32_t* __restrict__ prow,
+                               uint32_t nslots, uint32_t R, float* __restrict__ out) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / R;
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) % R;
+  if (i >= nslots) return;
+  const uint32_t tag = prow[i];
+  if (tag == kNoRow || (tag & kContinues)) return;
+  const uint32_t row = tag;
+  double s = part[static_cast<size_t>(i) * R + c];
+  // a slot 0 with its share's slot 1 in use is a complete run by itself
+  if ((i & 1u) || prow[i + 1] == kNoRow) {
+    constexpr int B = 4;  // following shares read per round trip
+    bool done = false;
+    for (uint32_t k0 = (i | 1u) + 1; k0 < nslots && !done; k0 += 2 * B) {
+      uint32_t t0[B], t1[B];
+      double v[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const uint32_t k = k0 + 2 * b;
+        const bool in = k < nslots;
+        t0[b] = in ? prow[k] : 0u;  // 0 without the flag: ends the run
+        t1[b] = in ? prow[k + 1] : 0u;
+        v[b] = in ? part[static_cast<size_t>(k) * R + c] : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (done) continue;
+        if (t0[b] == kNoRow && t1[b] == kNoRow) continue;  // an empty share (nnz < shares)
+        if (t0[b] != (row | kContinues)) {
+          done = true;
+          continue;
+        }
+        s += v[b];
+        if (t1[b] != kNoRow) done = true;
+      }
+    }
+  }
+  out[static_cast<size_t>(row) * R + c] = static_cast<float>(s);
+}
+
+using OwFn = void (*)(OwParams);
+template <int G, int V>
+OwFn pick_ow(int nm1) {
+  switch (nm1) {
+    case 1: return mttkrp_ow_kernel<1, G, V>;
+    case 2: return mttkrp_ow_kernel<2, G, V>;
+    case 3: return mttkrp_ow_kernel<3, G, V>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace
+
+namespace spt {
+
+// Inputs this path serves: R = 4G with G a power of two <= 32, orders 2..4,
+// 16-byte-aligned factors and output, at most kOwMaxNnz entries.
+bool mttkrp_onewave_ok(const spt_coo* x, uint64_t R, const float* const* d_factors, uint32_t mode,
+                       const float* d_out) {
+#ifndef SPT_OW_MAX_NNZ
+#define SPT_OW_MAX_NNZ 3000000ull
+#endif
+  if (x->nnz == 0 || x->nnz > SPT_OW_MAX_NNZ) return false;
+  if (x->order < 2 || x->order > 4) return false;
+  if (x->dims[mode] >= kContinues) return false;  // the slot tag's top bit is a flag
+  if (!(R == 8 || R == 16 || R == 32 || R == 64 || R == 128)) return false;
+  if (!aligned16(d_out) || !aligned16(x->val)) return false;
+  for (uint32_t d = 0; d < x->order; ++d) {
+    if (!aligned16(x->idx[d])) return false;
+    if (d != mode && !aligned16(d_factors[d])) return false;
+  }
+  return true;
+}
+
+int mttkrp_onewave(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors, uint32_t mode,
+                   uint32_t R, float* d_out, cudaStream_t st) {
+  const int nm1 = static_cast<int>(x->order) - 1;
+  // One float4 slice per lane. (Two slices per lane, V = 2, halve the index
+  // and address work per column but make the fp64 reduction over the lane
+  // groups at a row's end 5x longer -- 24 vs 16 us at C1.)
+  OwFn fn = nullptr;
+  switch (R) {
+    case 8: fn = pick_ow<2, 1>(nm1); break;
+    case 16: fn = pick_ow<4, 1>(nm1); break;
+    case 32: fn = pick_ow<8, 1>(nm1); break;
+    case 64: fn = pick_ow<16, 1>(nm1); break;
+    case 128: fn = pick_ow<32, 1>(nm1); break;
+  }
+  if (!fn) return set_error(SPT_EINVAL, "mttkrp: no one-wave kernel for this shape");
+  const size_t smem = static_cast<size_t>(kOwWarps) * (nm1 + 2) * kOwChunk * 4;
+  SPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  int per_sm = 0;
+  SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kOwThreads, smem));
+  const uint32_t grid = static_cast<uint32_t>(std::max(per_sm, 1) * ctx->num_sms);
+  OwParams p{};
+  p.out_idx = x->idx[mode];
+  int j = 0;
+  for (uint32_t d = 0; d < x->order; ++d) {
+    if (d == mode) continue;
+    p.oidx[j] = x->idx[d];
+    p.ofac[j] = d_factors[d];
+    ++j;
+  }
+  p.val = x->val;
+  p.out = d_out;
+  p.nnz = static_cast<uint32_t>(x->nnz);
+  p.rows = x->dims[mode];
+  p.R = R;
+  p.nwarps = grid * kOwWarps;
+  p.err = ctx->d_err;
+  const size_t slots = static_cast<size_t>(2) * p.nwarps;
+  const size_t pbytes = ((slots * R * sizeof(double) + 255) / 256) * 256;
+  void* scratch;
+  SPT_TRY(ctx_scratch(ctx, pbytes + slots * sizeof(uint32_t), &scratch));
+  p.part = static_cast<double*>(scratch);
+  p.prow = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + pbytes);
+  fn<<<grid, kOwThreads, smem, st>>>(p);
+  SPT_LAUNCHED(ctx);
+  const uint32_t threads = static_cast<uint32_t>(slots) * R;
+  ow_fold_kernel<<<(threads + 255) / 256, 256, 0, st>>>(p.part, p.prow,
+                                                        static_cast<uint32_t>(slots), R, d_out);
+  SPT_LAUNCHED(ctx);
+  return SPT_OK;
+}
+
+}  // namespace spt

@@ -146,6 +146,42 @@ def test_c4_mttkrp_full(lib, mode):
     _check_mttkrp(ops.mttkrp(plan, fs, mode), want)
 
 
+@pytest.mark.parametrize("dims,nnz,R,zipf", [
+    ([1000, 1000, 1000], 1_000_000, 16, [0, 0, 0]),        # C1: one staged chunk per share
+    ([5000, 3000, 700], 2_500_003, 16, [1.1, 0, 0]),        # several chunks per share, heavy rows
+    ([200_000, 900, 800], 700_001, 32, [0, 0, 0]),          # ~3.5 entries per row, empty rows
+    ([3, 50_000, 40_000], 1_200_000, 64, [0, 0, 0]),        # three rows spanning every share
+    ([40_000, 600, 500, 30], 900_000, 8, [1.1, 0, 0, 0]),   # order 4, R = 8
+    ([1000, 1000], 3000, 128, [0, 0]),                      # fewer entries than shares x 4
+])
+def test_mttkrp_onewave(lib, dims, nnz, R, zipf):
+    """The one-wave small-input MTTKRP (default segmented path up to 3M
+    entries) against the fp64 recomputation and the tiled kernel."""
+    ops, gen = lib
+    N = len(dims)
+    for mode in (0, N - 1):
+        order = [mode] + [d for d in range(N) if d != mode]
+        x = gen.coo(dims, nnz, 77, zipf, 0.0, 1.0, order)
+        fs = [gen.uniform((d, R), 77, 300 + k, 0.0, 1.0) for k, d in enumerate(dims)]
+        want = _mttkrp64(x, fs, mode)
+        got = ops.mttkrp(x, fs, mode, ops.MTTKRP_SEGMENTED)
+        _check_mttkrp(got, want)
+        again = ops.mttkrp(x, fs, mode, ops.MTTKRP_SEGMENTED)
+        assert torch.equal(got, again)  # fixed shares and summation orders
+        _check_mttkrp(ops.mttkrp(x, fs, mode, ops.MTTKRP_SEGMENTED_CTA), want)
+
+
+def test_mttkrp_onewave_unsorted(lib):
+    ops, gen = lib
+    x = gen.coo([500, 400, 300], 200_000, 5, [0, 0, 0], 0.0, 1.0, [0, 1, 2])
+    fs = [gen.uniform((d, 16), 5, 10 + k, 0.0, 1.0) for k, d in enumerate(x.dims)]
+    i0 = x.indices[0]
+    i0[100_000], i0[100_001] = i0[100_001].clone() + 3, i0[100_000].clone()
+    x.sort_order = [0, 1, 2]
+    with pytest.raises(Exception, match="sorted by the output mode"):
+        ops.mttkrp(x, fs, 0, ops.MTTKRP_SEGMENTED)
+
+
 @pytest.fixture(scope="module")
 def c5(lib):
     ops, gen = lib
