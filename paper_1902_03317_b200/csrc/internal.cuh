@@ -100,8 +100,10 @@ inline unsigned grid_for(uint64_t work_items, unsigned block, unsigned max_block
   } while (0)
 
 // Internal entry points implemented in the other translation units.
+// Stable; d_perm receives the permutation. nkeys < order sorts by the first
+// nkeys modes of mode_order only (ties keep the input order).
 int sort_tuples(spt_ctx* ctx, const spt_coo* x, const uint32_t* mode_order, uint32_t* d_perm,
-                cudaStream_t stream);  // stable; d_perm receives the permutation
+                cudaStream_t stream, uint32_t nkeys = SPT_MAX_ORDER);
 int gather_coo(spt_ctx* ctx, spt_coo* x, const uint32_t* d_perm, cudaStream_t stream);
 // MTTKRP plans (mttkrp_plan.cu) serve this input / rank.
 bool plan_supported(const spt_coo* x, uint64_t R);

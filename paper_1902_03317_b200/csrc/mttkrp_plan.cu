@@ -597,12 +597,15 @@ struct TileSrc {
 
 // SoA -> blocked AoSoA: block b holds NA arrays of CH entries; the padding
 // past nnz repeats the last entry (never consumed: the kernel stops at nnz).
-__global__ void plan_tile_kernel(TileSrc src, int na, uint32_t ch, uint64_t nnz, uint64_t nblk,
-                                 uint32_t* blk) {
+// perm != nullptr: entry e of the plan is entry perm[e] of the source arrays
+// (the sort permutation: no sorted SoA copy is materialised).
+__global__ void plan_tile_kernel(TileSrc src, const uint32_t* __restrict__ perm, int na,
+                                 uint32_t ch, uint64_t nnz, uint64_t nblk, uint32_t* blk) {
   const uint64_t total = nblk * ch;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const uint64_t s = e < nnz ? e : nnz - 1;
+    uint64_t s = e < nnz ? e : nnz - 1;
+    if (perm) s = perm[s];
     uint32_t* d = blk + (e / ch) * na * ch + e % ch;
     for (int a = 0; a < na; ++a) d[a * ch] = src.a[a][s];
   }
@@ -724,10 +727,78 @@ void plan_free(spt_mttkrp_plan* pl) {
   delete pl;
 }
 
-// Sorted SoA copy of x, hot rows chosen and encoded, tiled into pl->blk.
+// The plan's blocked copy of x in (mode, levels...) order. Without hot rows
+// (the default) nothing but the sort permutation is materialised: the tile
+// kernel gathers x through it, or reads x in place when it already has the
+// order; and when x is sorted such that a *stable* sort on the leading k modes
+// alone gives the plan's order (x in (0,1,2) order, plan (1,0,2) or (2,0,1):
+// k = 1), only those modes are sorted -- 24 key bits instead of 72 at C5.
+// With hot rows: a sorted SoA copy, hot ids encoded in place, then tiled.
 int plan_build(spt_ctx* ctx, spt_mttkrp_plan* pl, const spt_coo* x, unsigned flags,
                cudaStream_t st) {
   const uint32_t N = pl->N;
+  uint32_t order[SPT_MAX_ORDER];
+  order[0] = pl->mode;
+  for (uint32_t j = 0; j < pl->nm1; ++j) order[1 + j] = pl->lvl_mode[j];
+  // smallest k such that x's sort order without the modes order[0..k) is order[k..N)
+  uint32_t nkeys = N;
+  if (x->has_sort_order) {
+    for (uint32_t k = 0; k < N; ++k) {
+      uint32_t rest[SPT_MAX_ORDER], nr = 0;
+      for (uint32_t j = 0; j < N; ++j) {
+        const uint32_t m = static_cast<uint32_t>(x->sort_order[j]);
+        bool lead = false;
+        for (uint32_t i = 0; i < k; ++i) lead = lead || order[i] == m;
+        if (!lead) rest[nr++] = m;
+      }
+      bool ok = nr == N - k;
+      for (uint32_t j = 0; ok && j < nr; ++j) ok = rest[j] == order[k + j];
+      if (ok) {
+        nkeys = k;
+        break;
+      }
+    }
+  }
+  const PlanVariant v = plan_variant(pl->nm1, pl->CB);
+  const long avail = (long)plan_max_smem(ctx->device) - (long)v.fixed - 4096;  // static smem
+  uint32_t cap = avail > 0 ? static_cast<uint32_t>(avail / (pl->CB * 4)) : 0;
+  // Shared-memory hot rows measured no faster than L1 hits on the same
+  // rows (C1/C4/C5, DESIGN.md) and cost L1 capacity: off unless asked for.
+  cap = std::min<uint32_t>(cap, static_cast<uint32_t>(atoi(getenv("SPT_PLAN_HOT_MAX") ?: "0")));
+  // (An L2 evict_last tier for the next ~750K most-gathered rows, evict_first
+  // for the rest, measured no faster at C5 either: 23.1 vs 23.6 ms.)
+  bool ids_fit = true;  // kHot needs ids < 2^31
+  for (uint32_t j = 0; j < pl->nm1; ++j) ids_fit = ids_fit && pl->dims[pl->lvl_mode[j]] <= kHot;
+  if (!ids_fit || (flags & SPT_PLAN_NO_HOT)) cap = 0;
+  const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(
+      1, std::min<uint64_t>((pl->nblk * pl->CH + 255) / 256, (uint64_t)ctx->num_sms * 16)));
+
+  if (cap == 0) {
+    uint32_t* perm = nullptr;
+    int s = SPT_OK;
+    if (nkeys > 0 && x->nnz > 1) {
+      if (spt::tmp_alloc(ctx, &perm, x->nnz * sizeof(uint32_t), st) != cudaSuccess) {
+        cudaGetLastError();
+        return spt::set_error(SPT_ENOMEM, "mttkrp_plan: out of device memory (%zu bytes)",
+                              (size_t)x->nnz * 4);
+      }
+      s = spt::sort_tuples(ctx, x, order, perm, st, nkeys);
+    }
+    if (s == SPT_OK) {
+      TileSrc src{};
+      src.a[0] = x->idx[pl->mode];
+      for (uint32_t j = 0; j < pl->nm1; ++j) src.a[1 + j] = x->idx[pl->lvl_mode[j]];
+      src.a[pl->nm1 + 1] = reinterpret_cast<const uint32_t*>(x->val);
+      plan_tile_kernel<<<grid, 256, 0, st>>>(src, perm, static_cast<int>(pl->NA), pl->CH, x->nnz,
+                                             pl->nblk, pl->blk);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) s = spt::cuda_status(e, "plan_tile_kernel");
+      else ctx->launches++;
+    }
+    if (perm) cudaFreeAsync(perm, st);
+    return s;
+  }
+
   const size_t ab = align256((x->nnz + 4) * 4);
   char* soa = nullptr;
   if (spt::tmp_alloc(ctx, reinterpret_cast<void**>(&soa), ab * (N + 1), st) != cudaSuccess) {
@@ -742,36 +813,18 @@ int plan_build(spt_ctx* ctx, spt_mttkrp_plan* pl, const spt_coo* x, unsigned fla
   }
   c.val = reinterpret_cast<float*>(soa + N * ab);
   SPT_CUDA(cudaMemcpyAsync(c.val, x->val, x->nnz * 4, cudaMemcpyDeviceToDevice, st));
-  uint32_t order[SPT_MAX_ORDER];
-  order[0] = pl->mode;
-  for (uint32_t j = 0; j < pl->nm1; ++j) order[1 + j] = pl->lvl_mode[j];
-  bool same = x->has_sort_order != 0;
-  for (uint32_t j = 0; same && j < N; ++j) same = static_cast<uint32_t>(x->sort_order[j]) == order[j];
   int s = SPT_OK;
-  if (!same && x->nnz > 1) s = spt_sort_f32(ctx, &c, order, 0, st);
+  if (nkeys > 0 && x->nnz > 1) s = spt_sort_f32(ctx, &c, order, 0, st);
   uint32_t* lvl[SPT_MAX_ORDER - 1];
   for (uint32_t j = 0; j < pl->nm1; ++j) lvl[j] = c.idx[pl->lvl_mode[j]];
-  const PlanVariant v = plan_variant(pl->nm1, pl->CB);
-  const long avail = (long)plan_max_smem(ctx->device) - (long)v.fixed - 4096;  // static smem
-  uint32_t cap = avail > 0 ? static_cast<uint32_t>(avail / (pl->CB * 4)) : 0;
-  // Shared-memory hot rows measured no faster than L1 hits on the same
-  // rows (C1/C4/C5, DESIGN.md) and cost L1 capacity: off unless asked for.
-  cap = std::min<uint32_t>(cap, static_cast<uint32_t>(atoi(getenv("SPT_PLAN_HOT_MAX") ?: "0")));
-  // (An L2 evict_last tier for the next ~750K most-gathered rows, evict_first
-  // for the rest, measured no faster at C5 either: 23.1 vs 23.6 ms.)
-  bool ids_fit = true;  // kHot needs ids < 2^31
-  for (uint32_t j = 0; j < pl->nm1; ++j) ids_fit = ids_fit && pl->dims[pl->lvl_mode[j]] <= kHot;
-  if (!ids_fit || (flags & SPT_PLAN_NO_HOT)) cap = 0;
-  if (s == SPT_OK && cap > 0) s = plan_select_hot(ctx, pl, c.idx[pl->mode], lvl, cap, st);
+  if (s == SPT_OK) s = plan_select_hot(ctx, pl, c.idx[pl->mode], lvl, cap, st);
   if (s == SPT_OK) {
     TileSrc src{};
     src.a[0] = c.idx[pl->mode];
     for (uint32_t j = 0; j < pl->nm1; ++j) src.a[1 + j] = lvl[j];
     src.a[pl->nm1 + 1] = reinterpret_cast<const uint32_t*>(c.val);
-    const unsigned grid = static_cast<unsigned>(
-        std::min<uint64_t>((pl->nblk * pl->CH + 255) / 256, (uint64_t)ctx->num_sms * 16));
-    plan_tile_kernel<<<std::max(grid, 1u), 256, 0, st>>>(src, static_cast<int>(pl->NA), pl->CH,
-                                                         x->nnz, pl->nblk, pl->blk);
+    plan_tile_kernel<<<grid, 256, 0, st>>>(src, nullptr, static_cast<int>(pl->NA), pl->CH, x->nnz,
+                                           pl->nblk, pl->blk);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) s = spt::cuda_status(e, "plan_tile_kernel");
     else ctx->launches++;

@@ -255,9 +255,9 @@ size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 namespace spt {
 
 int sort_tuples(spt_ctx* ctx, const spt_coo* x, const uint32_t* mo, uint32_t* d_perm_out,
-                cudaStream_t st) {
+                cudaStream_t st, uint32_t nkeys) {
   const uint64_t n = x->nnz;
-  const uint32_t N = x->order;
+  const uint32_t N = std::min(x->order, nkeys);
   // Chunks from least significant mode (mo[N-1]) upward, each <= 64 bits.
   std::vector<PackSpec> chunks;
   std::vector<uint32_t> chunk_bits;
