@@ -94,7 +94,10 @@ __global__ void __launch_bounds__(256) hist_kernel(SrcDesc s, uint64_t n, Digits
   __shared__ uint32_t h[kMaxPasses * kBins];
   for (int j = threadIdx.x; j < dg.passes * kBins; j += blockDim.x) h[j] = 0;
   __syncthreads();
-  constexpr int U = 4;  // keys per thread and step: U loads per array in flight
+#ifndef SPT_RADIX_HIST_U
+#define SPT_RADIX_HIST_U 4
+#endif
+  constexpr int U = SPT_RADIX_HIST_U;  // keys per thread and step: U loads per array in flight
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * U;
   const unsigned lane = threadIdx.x & 31u;
   for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x * U; b < n; b += stride) {

@@ -84,9 +84,48 @@ def pack_keys(t, order: Sequence[int], dims: Optional[Sequence[int]] = None) -> 
     return key
 
 
+def _lower_bound_tuple(t, order: Sequence[int], tup: Sequence[int]) -> int:
+    """First entry of the sorted device tensor t whose tuple (in `order`
+    significance) is >= tup: one searchsorted pair per mode on the narrowing
+    range, nothing but a few scalars leaves the device."""
+    lo, hi = 0, int(t.indices[0].shape[0])
+    for d, v in zip(order, tup):
+        if lo == hi:
+            break
+        a = t.indices[d][lo:hi]
+        if v >= 1 << 31 or (a.dtype == torch.int32 and int(a[-1].item()) < 0):
+            raise OverflowError("ids >= 2^31 in an int32 device array: split on the host")
+        key = torch.tensor([v], dtype=a.dtype, device=a.device)
+        l = int(torch.searchsorted(a, key, right=False).item())
+        r = int(torch.searchsorted(a, key, right=True).item())
+        if l == r:
+            return lo + l
+        lo, hi = lo + l, lo + r
+    return lo
+
+
 def tew_shards(x, y, order: Sequence[int], world: int) -> list:
-    """Per-rank key-range shards of two sorted TEW operands, keys packed with
-    the common (per-mode max) dims so both share one layout."""
+    """Per-rank key-range shards of two sorted TEW operands: x cut at
+    equal-nnz positions, y cut at the same tuples, so matched tuples always
+    land on the same rank. Device tensors are searched in place (only the
+    world-1 splitter tuples come to the host); host tensors, and device ids
+    >= 2^31, go through packed u64 keys with the common (per-mode max) dims."""
+    if isinstance(x.indices[0], torch.Tensor) and x.indices[0].is_cuda:
+        try:
+            nx, ny = len(x.values), len(y.values)
+            cuts_x = [shard_range(nx, world, r)[0] for r in range(world)] + [nx]
+            cuts_y = [0]
+            for c in cuts_x[1:-1]:
+                if c >= nx:
+                    cuts_y.append(ny)
+                    continue
+                tup = [int(x.indices[d][c].item()) & 0xFFFFFFFF for d in order]
+                cuts_y.append(_lower_bound_tuple(y, order, tup))
+            cuts_y.append(ny)
+            return [((cuts_x[r], cuts_x[r + 1]), (cuts_y[r], cuts_y[r + 1]))
+                    for r in range(world)]
+        except OverflowError:
+            pass
     dims = [max(a, b) for a, b in zip(x.dims, y.dims)]
     return tew_key_ranges(pack_keys(x, order, dims), pack_keys(y, order, dims), world)
 

@@ -53,3 +53,19 @@ def test_mttkrp_multi_rejects_a_device_twice(mods):
     fs = [generate.uniform((d, 16), 4, 10 + k, 0.0, 1.0) for k, d in enumerate(x.dims)]
     with pytest.raises(_lib.InvalidArgument):
         parallel.mttkrp_multi(x, [fs, fs], 0, 16)
+
+
+def test_tew_shards_device_equals_host(mods):
+    """The key-range split of two TEW operands searched on the device (only
+    the splitter tuples leave it) equals the packed-key split on the host,
+    with unequal dims and with shared and unshared tuples."""
+    _lib, generate, ops, parallel = mods
+    x = generate.coo([400, 300, 50], 200_000, 21, [1.2, 0, 0], 0.5, 1.5, [2, 0, 1])
+    y = generate.coo([380, 310, 64], 150_000, 22, [0, 0, 0], 0.5, 1.5, [2, 0, 1])
+    hx, hy = x.to_host(), y.to_host()
+    for world in (1, 2, 3, 8):
+        dev = parallel.tew_shards(x, y, [2, 0, 1], world)
+        host = parallel.tew_shards(hx, hy, [2, 0, 1], world)
+        assert dev == host
+    # x against itself: every cut tuple exists in y, lower bound = same position
+    assert all(a == b for a, b in parallel.tew_shards(x, x, [2, 0, 1], 5))
