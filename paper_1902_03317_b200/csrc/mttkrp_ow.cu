@@ -71,6 +71,9 @@ __global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
   constexpr int C2 = 2 * V;    // float2 pairs per lane
   const unsigned lane = threadIdx.x & 31u, g = lane / G, q = lane % G;
   const uint32_t w = blockIdx.x * kOwWarps + (threadIdx.x >> 5);
+  // let the fold kernel's CTAs become resident now (they block in
+  // griddepcontrol.wait until this grid has finished and flushed its writes)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // equal shares cut at multiples of 4 entries: every array's piece of a share
   // starts 16-byte aligned (16-byte cp.async.cg, which also keeps the entry
   // stream out of L1 -- that is for the factor rows)
@@ -256,6 +259,9 @@ __global__ void ow_fold_kernel(const double* __restrict__ part, const uint32_t* 
                                uint32_t nslots, uint32_t R, float* __restrict__ out) {
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / R;
   const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) % R;
+  // launched with programmatic stream serialization: the grid is resident
+  // before the main kernel ends; wait for its writes here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (i >= nslots) return;
   const uint32_t tag = prow[i];
   if (tag == kNoRow || (tag & kContinues)) return;
@@ -372,9 +378,21 @@ int mttkrp_onewave(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors
   fn<<<grid, kOwThreads, smem, st>>>(p);
   SPT_LAUNCHED(ctx);
   const uint32_t threads = static_cast<uint32_t>(slots) * R;
-  ow_fold_kernel<<<(threads + 255) / 256, 256, 0, st>>>(p.part, p.prow,
-                                                        static_cast<uint32_t>(slots), R, d_out);
-  SPT_LAUNCHED(ctx);
+  // the fold's launch overlaps the main kernel's tail (programmatic dependent
+  // launch); it waits on griddepcontrol.wait before reading the slots
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((threads + 255) / 256);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  SPT_CUDA(cudaLaunchKernelEx(&cfg, ow_fold_kernel, static_cast<const double*>(p.part),
+                              static_cast<const uint32_t*>(p.prow),
+                              static_cast<uint32_t>(slots), R, d_out));
+  ctx->launches++;
   return SPT_OK;
 }
 
