@@ -44,15 +44,18 @@ struct OwParams {
   const float* ofac[SPT_MAX_ORDER - 1];
   const float* val;
   float* out;
-  uint32_t nnz, rows, R, nwarps;
+  uint32_t nnz, rows, R, nwarps, share_q, share_r;
   double* part;    // [2 * nwarps][R]
   uint32_t* prow;  // [2 * nwarps]
   unsigned long long* err;
 };
 
-__device__ __forceinline__ uint32_t share_cut(uint32_t nnz, uint32_t shares, uint32_t w) {
+// Share w starts at w*q + min(w, r) (q, r = nnz / shares, nnz % shares),
+// rounded down to a multiple of 4.
+__device__ __forceinline__ uint32_t share_cut(uint32_t nnz, uint32_t shares, uint32_t q,
+                                              uint32_t r, uint32_t w) {
   if (w >= shares) return nnz;
-  return static_cast<uint32_t>(static_cast<uint64_t>(nnz) * w / shares) & ~3u;
+  return (w * q + min(w, r)) & ~3u;
 }
 
 __device__ __forceinline__ void ow_zero_rows(float* out, uint32_t r0, uint32_t r1, uint32_t R,
@@ -77,7 +80,8 @@ __global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
   // equal shares cut at multiples of 4 entries: every array's piece of a share
   // starts 16-byte aligned (16-byte cp.async.cg, which also keeps the entry
   // stream out of L1 -- that is for the factor rows)
-  const uint32_t lo = share_cut(p.nnz, p.nwarps, w), hi = share_cut(p.nnz, p.nwarps, w + 1);
+  const uint32_t lo = share_cut(p.nnz, p.nwarps, p.share_q, p.share_r, w);
+  const uint32_t hi = share_cut(p.nnz, p.nwarps, p.share_q, p.share_r, w + 1);
   uint32_t* myrow = p.prow + 2 * w;
   double* mypart = p.part + static_cast<size_t>(2 * w) * p.R + q * 4 * V;
   if (lo >= hi) {
@@ -87,6 +91,7 @@ __global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
   const float* fq[NM1];
 #pragma unroll
   for (int j = 0; j < NM1; ++j) fq[j] = p.ofac[j] + q * 4 * V;
+  const uint32_t rb = p.R * 4;  // row bytes
 
   uint32_t cur = kNoRow;       // current row (warp-uniform)
   int flushed = 0;             // rows finished so far
@@ -192,8 +197,10 @@ __global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
         v[u] = ok ? __uint_as_float(sw[(NM1 + 1) * kOwChunk + i]) : 0.f;
 #pragma unroll
         for (int j = 0; j < NM1; ++j) {
+          // byte address = base + id * row bytes: one IMAD.WIDE
           const float4* row = reinterpret_cast<const float4*>(
-              fq[j] + static_cast<size_t>(ok ? sw[(1 + j) * kOwChunk + i] : 0u) * p.R);
+              reinterpret_cast<const char*>(fq[j]) +
+              static_cast<size_t>(ok ? sw[(1 + j) * kOwChunk + i] : 0u) * rb);
 #pragma unroll
           for (int k = 0; k < V; ++k)
             F[j][u][k] = ok ? __ldg(row + k) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -219,10 +226,12 @@ __global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
 #pragma unroll
           for (int c = 0; c < C2; ++c) ra[c].x += t[c].x, ra[c].y += t[c].y;
         } else {
-          // a row boundary (or the share's first entry) inside this step
-          for (int e = 0; e < EPW; ++e) {
+          // a row boundary (or the share's first entry) inside this step:
+          // one round per row present in the step, found by ballot
+          uint32_t todo = __ballot_sync(0xffffffffu, valid);  // lanes still to add
+          while (todo) {
+            const int e = (__ffs(todo) - 1) / G;  // first group not added yet
             const uint32_t re = __shfl_sync(0xffffffffu, r[u], e * G);
-            if (re == kNoRow) break;
             if (re != cur) {
               if (cur != kNoRow) {
                 if (re < cur && lane == 0)
@@ -235,10 +244,13 @@ __global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
               ow_zero_rows(p.out, gap, re, p.R, lane);
               cur = re;
             }
-            if (static_cast<int>(g) == e) {
+            // every group of this row in the step (they are consecutive)
+            const bool mine = valid && r[u] == cur && ((todo >> lane) & 1u);
+            if (mine) {
 #pragma unroll
               for (int c = 0; c < C2; ++c) ra[c].x += t[c].x, ra[c].y += t[c].y;
             }
+            todo &= ~__ballot_sync(0xffffffffu, mine);
           }
         }
       }
@@ -368,6 +380,8 @@ int mttkrp_onewave(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors
   p.rows = x->dims[mode];
   p.R = R;
   p.nwarps = grid * kOwWarps;
+  p.share_q = p.nnz / p.nwarps;
+  p.share_r = p.nnz % p.nwarps;
   p.err = ctx->d_err;
   const size_t slots = static_cast<size_t>(2) * p.nwarps;
   const size_t pbytes = ((slots * R * sizeof(double) + 255) / 256) * 256;
