@@ -360,10 +360,24 @@ int mttkrp_onewave(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors
   }
   if (!fn) return set_error(SPT_EINVAL, "mttkrp: no one-wave kernel for this shape");
   const size_t smem = static_cast<size_t>(kOwWarps) * (nm1 + 2) * kOwChunk * 4;
-  SPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
+  // attribute + occupancy once per (kernel, device): a 20 us op should not pay
+  // two runtime queries per call
+  struct Cached {
+    OwFn fn;
+    int device, per_sm;
+  };
+  static thread_local Cached cache[8] = {};
   int per_sm = 0;
-  SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kOwThreads, smem));
+  for (const Cached& c : cache)
+    if (c.fn == fn && c.device == ctx->device) per_sm = c.per_sm;
+  if (per_sm == 0) {
+    SPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    SPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kOwThreads, smem));
+    per_sm = std::max(per_sm, 1);
+    static thread_local int next = 0;
+    cache[next++ % 8] = Cached{fn, ctx->device, per_sm};
+  }
   const uint32_t grid = static_cast<uint32_t>(std::max(per_sm, 1) * ctx->num_sms);
   OwParams p{};
   p.out_idx = x->idx[mode];
