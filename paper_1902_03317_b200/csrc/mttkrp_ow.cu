@@ -1,4 +1,5 @@
-// One-wave segmented MTTKRP for small inputs (C1: 1M nonzeros, R = 16).
+// One-wave segmented MTTKRP for small and medium inputs (C1: 1M nonzeros,
+// R = 16; used up to 32M entries when rows average >= 16 entries).
 //
 // Reference: seq::mttkrp / par::mttkrp (P/src/kernels_seq.cpp:153-174,
 // P/src/kernel_detail.hpp:176-188), input sorted with the output mode leading.
@@ -20,9 +21,10 @@
 //     share holds a few rows), the step is replayed entry by entry and finished
 //     rows are reduced over the lane groups by a fixed shuffle tree;
 //   * rows strictly inside a warp's share are written once; its first and last
-//     row go to two fp64 partial slots (slot 0 flagged when the row continues
-//     the previous share's), and a second small kernel sums each row's run of
-//     slots in slot order. Rows without entries are zero-filled
+//     row go to two fp64 partial slots in shared memory (slot 0 flagged when
+//     the row continues the previous share's); the CTA folds its warps' slots
+//     into two global slots, and a second small kernel sums each row's run of
+//     CTA slots in slot order. Rows without entries are zero-filled
 //     by the warp whose share spans the gap. Deterministic: the split and both
 //     summation orders are fixed by (nnz, grid).
 #include <algorithm>
@@ -66,24 +68,23 @@ __device__ __forceinline__ void ow_zero_rows(float* out, uint32_t r0, uint32_t r
   for (size_t i = lane; i < n4; i += 32) __stcs(o + i, make_float4(0.f, 0.f, 0.f, 0.f));
 }
 
-// G lanes per factor row, V float4 slices (4V columns) per lane: R = 4 G V.
+// One warp's share. G lanes per factor row, V float4 slices (4V columns) per
+// lane: R = 4 G V. myrow[2] / myslots[2][R]: the share's first-row and
+// last-row partials (in shared memory; the CTA folds them afterwards); sw: the
+// warp's staging area.
 template <int NM1, int G, int V>
-__global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
+__device__ __forceinline__ void ow_share(const OwParams& p, uint32_t w, uint32_t* myrow,
+                                         double* myslots, uint32_t* sw) {
   constexpr int EPW = 32 / G;  // entries per warp step
   constexpr int U = kOwU / V;  // steps gathered at once
   constexpr int C2 = 2 * V;    // float2 pairs per lane
   const unsigned lane = threadIdx.x & 31u, g = lane / G, q = lane % G;
-  const uint32_t w = blockIdx.x * kOwWarps + (threadIdx.x >> 5);
-  // let the fold kernel's CTAs become resident now (they block in
-  // griddepcontrol.wait until this grid has finished and flushed its writes)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // equal shares cut at multiples of 4 entries: every array's piece of a share
   // starts 16-byte aligned (16-byte cp.async.cg, which also keeps the entry
   // stream out of L1 -- that is for the factor rows)
   const uint32_t lo = share_cut(p.nnz, p.nwarps, p.share_q, p.share_r, w);
   const uint32_t hi = share_cut(p.nnz, p.nwarps, p.share_q, p.share_r, w + 1);
-  uint32_t* myrow = p.prow + 2 * w;
-  double* mypart = p.part + static_cast<size_t>(2 * w) * p.R + q * 4 * V;
+  double* mypart = myslots + q * 4 * V;
   if (lo >= hi) {
     if (lane == 0) myrow[0] = myrow[1] = kNoRow;
     return;
@@ -148,8 +149,6 @@ __global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
   };
 
   // the share's entry words, staged per warp: [row | ids.. | val][kOwChunk]
-  extern __shared__ __align__(16) uint32_t ow_smem[];
-  uint32_t* sw = ow_smem + (threadIdx.x >> 5) * (NM1 + 2) * kOwChunk;
   const uint32_t sw_a = spt::smem_addr(sw);
   for (uint32_t c0 = lo; c0 < hi; c0 += kOwChunk) {
     const uint32_t n = min(static_cast<uint32_t>(kOwChunk), hi - c0);
@@ -262,52 +261,118 @@ __global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
   if (hi == p.nnz) ow_zero_rows(p.out, cur + 1, p.rows, p.R, lane);
 }
 
+// The kernel: every warp does its share, then the CTA folds its warps' 2 x 8
+// slots in shared memory: runs of equal rows are summed in slot order; the
+// CTA's first run (it may continue the previous CTA's last row: the flag of
+// its first slot is kept) and last run go to the CTA's two global slots, runs
+// in between are complete and go to the output. The fold kernel then only
+// sees 2 slots per CTA: a heavy row spanning most of the tensor is a run of a
+// few hundred CTA slots, not thousands of warp slots.
+template <int NM1, int G, int V>
+__global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
+  constexpr int S = 2 * kOwWarps;
+  extern __shared__ __align__(16) uint32_t ow_smem[];
+  const unsigned warp = threadIdx.x >> 5;
+  // let the fold kernel's CTAs become resident now (they block in
+  // griddepcontrol.wait until this grid has finished and flushed its writes)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  double* sval = reinterpret_cast<double*>(ow_smem + kOwWarps * (NM1 + 2) * kOwChunk);  // [S][R]
+  uint32_t* srow = reinterpret_cast<uint32_t*>(sval + static_cast<size_t>(S) * p.R);   // [S]
+  ow_share<NM1, G, V>(p, blockIdx.x * kOwWarps + warp, srow + 2 * warp,
+                      sval + static_cast<size_t>(2 * warp) * p.R,
+                      ow_smem + warp * (NM1 + 2) * kOwChunk);
+  uint32_t* grow = p.prow + 2 * blockIdx.x;
+  double* gpart = p.part + static_cast<size_t>(2 * blockIdx.x) * p.R;
+  if (threadIdx.x == 0) grow[0] = grow[1] = kNoRow;
+  __syncthreads();
+  for (uint32_t item = threadIdx.x; item < S * p.R; item += kOwThreads) {
+    const int i = static_cast<int>(item / p.R);
+    const uint32_t c = item % p.R;
+    const uint32_t tag = srow[i];
+    if (tag == kNoRow) continue;
+    const uint32_t row = tag & ~kContinues;
+    int j = i - 1;
+    while (j >= 0 && srow[j] == kNoRow) --j;
+    if (j >= 0 && (srow[j] & ~kContinues) == row) continue;  // not the run's first slot
+    double s = 0.0;
+    int k = i;
+    bool last_run = true;
+    for (; k < S; ++k) {
+      const uint32_t t = srow[k];
+      if (t == kNoRow) continue;
+      if ((t & ~kContinues) != row) {
+        last_run = false;
+        break;
+      }
+      s += sval[static_cast<size_t>(k) * p.R + c];
+    }
+    if (j < 0) {  // the CTA's first run: tag with its continuation flag
+      gpart[c] = s;
+      if (c == 0) grow[0] = tag;
+    } else if (last_run) {
+      gpart[p.R + c] = s;
+      if (c == 0) grow[1] = row;
+    } else {
+      p.out[static_cast<size_t>(row) * p.R + c] = static_cast<float>(s);
+    }
+  }
+}
+
 // Sum each row's run of partial slots in slot order. One thread per (slot,
 // column); the run's first slot -- a slot 1, or a slot 0 whose row does not
 // continue the previous share's -- does the work: its own part plus the slot 0
 // of the following shares for as long as they continue the row (a share whose
-// slot 1 is used ends the run: its last row is another one).
+// slot 1 is used ends the run: its last row is another one). The GL = min(R,
+// 32) lanes of a slot walk the run together: each reads the tags of one of the
+// next GL shares, ballots find where the run stops, then every lane adds its
+// column of the member slots in slot order -- a heavy row spanning hundreds of
+// shares costs a dozen round trips instead of one per four shares.
 __global__ void ow_fold_kernel(const double* __restrict__ part, const uint32_t* __restrict__ prow,
                                uint32_t nslots, uint32_t R, float* __restrict__ out) {
-  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / R;
-  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) % R;
+  const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t i = gt / R, c = gt % R;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t GL = R < 32u ? R : 32u;
+  const unsigned base = lane & ~(GL - 1u), l = lane - base;
+  const uint32_t gmask = GL == 32u ? 0xffffffffu : ((1u << GL) - 1u);
   // launched with programmatic stream serialization: the grid is resident
   // before the main kernel ends; wait for its writes here
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (i >= nslots) return;
-  const uint32_t tag = prow[i];
-  if (tag == kNoRow || (tag & kContinues)) return;
+  const uint32_t tag = i < nslots ? prow[i] : kNoRow;
+  const bool start = tag != kNoRow && !(tag & kContinues);
   const uint32_t row = tag;
-  double s = part[static_cast<size_t>(i) * R + c];
+  double s = start ? part[static_cast<size_t>(i) * R + c] : 0.0;
   // a slot 0 with its share's slot 1 in use is a complete run by itself
-  if ((i & 1u) || prow[i + 1] == kNoRow) {
-    constexpr int B = 4;  // following shares read per round trip
-    bool done = false;
-    for (uint32_t k0 = (i | 1u) + 1; k0 < nslots && !done; k0 += 2 * B) {
-      uint32_t t0[B], t1[B];
-      double v[B];
+  bool walk = start && ((i & 1u) || prow[i + 1] == kNoRow);
+  uint32_t k0 = (i | 1u) + 1;
+  while (__any_sync(0xffffffffu, walk)) {
+    // lane l of the slot's group looks at share l of the next GL
+    const uint32_t k = k0 + 2 * l;
+    const bool in = walk && k < nslots;
+    const uint32_t t0 = in ? prow[k] : 0u;  // 0 carries no flag: ends the run
+    const uint32_t t1 = in ? prow[k + 1] : 0u;
+    const bool empty = t0 == kNoRow && t1 == kNoRow;  // an empty share (nnz < shares)
+    const bool member = t0 == (row | kContinues);
+    const uint32_t bad_m = (__ballot_sync(0xffffffffu, !empty && !member) >> base) & gmask;
+    const uint32_t end_m = (__ballot_sync(0xffffffffu, member && t1 != kNoRow) >> base) & gmask;
+    const uint32_t mem_m = (__ballot_sync(0xffffffffu, member) >> base) & gmask;
+    const uint32_t first_bad = bad_m ? __ffs(bad_m) - 1 : GL;
+    const uint32_t first_end = end_m ? __ffs(end_m) - 1 : GL;
+    const uint32_t ntake = min(first_bad, first_end + 1);
+    if (walk) {
+      uint32_t take = mem_m & (ntake >= 32u ? 0xffffffffu : ((1u << ntake) - 1u));
+      // slot order; all of the round's loads in flight (absent ones add 0.0)
+      double v[32];
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const uint32_t k = k0 + 2 * b;
-        const bool in = k < nslots;
-        t0[b] = in ? prow[k] : 0u;  // 0 without the flag: ends the run
-        t1[b] = in ? prow[k + 1] : 0u;
-        v[b] = in ? part[static_cast<size_t>(k) * R + c] : 0.0;
-      }
+      for (int u = 0; u < 32; ++u)
+        v[u] = (take >> u) & 1u ? part[static_cast<size_t>(k0 + 2 * u) * R + c] : 0.0;
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        if (done) continue;
-        if (t0[b] == kNoRow && t1[b] == kNoRow) continue;  // an empty share (nnz < shares)
-        if (t0[b] != (row | kContinues)) {
-          done = true;
-          continue;
-        }
-        s += v[b];
-        if (t1[b] != kNoRow) done = true;
-      }
+      for (int u = 0; u < 32; ++u) s += v[u];
+      if (first_bad < GL || first_end < GL) walk = false;
+      k0 += 2 * GL;
     }
   }
-  out[static_cast<size_t>(row) * R + c] = static_cast<float>(s);
+  if (start) out[static_cast<size_t>(row) * R + c] = static_cast<float>(s);
 }
 
 using OwFn = void (*)(OwParams);
@@ -329,10 +394,19 @@ namespace spt {
 // 16-byte-aligned factors and output, at most kOwMaxNnz entries.
 bool mttkrp_onewave_ok(const spt_coo* x, uint64_t R, const float* const* d_factors, uint32_t mode,
                        const float* d_out) {
+  // Measured against the tiled kernels (tune/probe_c1_times.py, uniform rows):
+  // 16 vs 20 us at 0.5M, 21 vs 29 at 1M, 38 vs 61 at 3M, 94 vs 138 at 10M,
+  // 175 vs 250 at 20M entries (R = 16, 1000 rows); 701 vs 812 us with 20
+  // entries per row, but 1232 vs 1114 with 4: every row end costs a reduction
+  // over the lane groups, so short rows stay with the tiled kernels.
 #ifndef SPT_OW_MAX_NNZ
-#define SPT_OW_MAX_NNZ 3000000ull
+#define SPT_OW_MAX_NNZ 32000000ull
+#endif
+#ifndef SPT_OW_MIN_ROW
+#define SPT_OW_MIN_ROW 16ull
 #endif
   if (x->nnz == 0 || x->nnz > SPT_OW_MAX_NNZ) return false;
+  if (x->nnz < SPT_OW_MIN_ROW * x->dims[mode]) return false;
   if (x->order < 2 || x->order > 4) return false;
   if (x->dims[mode] >= kContinues) return false;  // the slot tag's top bit is a flag
   if (!(R == 8 || R == 16 || R == 32 || R == 64 || R == 128)) return false;
@@ -359,7 +433,8 @@ int mttkrp_onewave(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors
     case 128: fn = pick_ow<32, 1>(nm1); break;
   }
   if (!fn) return set_error(SPT_EINVAL, "mttkrp: no one-wave kernel for this shape");
-  const size_t smem = static_cast<size_t>(kOwWarps) * (nm1 + 2) * kOwChunk * 4;
+  const size_t smem = static_cast<size_t>(kOwWarps) * (nm1 + 2) * kOwChunk * 4 +
+                      static_cast<size_t>(2 * kOwWarps) * R * 8 + 2 * kOwWarps * 4;
   // attribute + occupancy once per (kernel, device): a 20 us op should not pay
   // two runtime queries per call
   struct Cached {
@@ -397,7 +472,7 @@ int mttkrp_onewave(spt_ctx* ctx, const spt_coo* x, const float* const* d_factors
   p.share_q = p.nnz / p.nwarps;
   p.share_r = p.nnz % p.nwarps;
   p.err = ctx->d_err;
-  const size_t slots = static_cast<size_t>(2) * p.nwarps;
+  const size_t slots = static_cast<size_t>(2) * grid;  // two per CTA
   const size_t pbytes = ((slots * R * sizeof(double) + 255) / 256) * 256;
   void* scratch;
   SPT_TRY(ctx_scratch(ctx, pbytes + slots * sizeof(uint32_t), &scratch));

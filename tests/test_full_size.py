@@ -152,7 +152,10 @@ def test_c4_mttkrp_full(lib, mode):
     ([200_000, 900, 800], 700_001, 32, [0, 0, 0]),          # ~3.5 entries per row, empty rows
     ([3, 50_000, 40_000], 1_200_000, 64, [0, 0, 0]),        # three rows spanning every share
     ([40_000, 600, 500, 30], 900_000, 8, [1.1, 0, 0, 0]),   # order 4, R = 8
-    ([1000, 1000], 3000, 128, [0, 0]),                      # fewer entries than shares x 4
+    ([1000, 1000], 3000, 128, [0, 0]),                      # short rows: the tiled kernel's case
+    ([50, 2000], 3000, 128, [0, 0]),                        # fewer entries than shares x 4
+    ([2000, 5000, 3000], 8_000_000, 16, [1.1, 0, 0]),       # a heavy row over hundreds of shares
+    ([300, 4000, 3000], 6_000_000, 64, [1.3, 0, 0]),        # the same with two warps per slot
 ])
 def test_mttkrp_onewave(lib, dims, nnz, R, zipf):
     """The one-wave small-input MTTKRP (default segmented path up to 3M

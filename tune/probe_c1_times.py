@@ -2,9 +2,11 @@
 import os, sys, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1902_03317_b200 import generate, ops, _lib
-x = generate.coo([1000] * 3, 1_000_000, 1, [0, 0, 0], 0, 1, [0, 1, 2])
-f = [generate.uniform((1000, 16), 1, k, 0, 1) for k in range(3)]
-out = torch.empty((1000, 16), device="cuda")
+nnz = int(os.environ.get("NNZ", 1_000_000)); R = int(os.environ.get("R", 16)); D = int(os.environ.get("D", 1000))
+Z = float(os.environ.get("ZIPF", 0))
+x = generate.coo([D, max(D, 3000), max(D, 3000)], nnz, 1, [Z, 0, 0], 0, 1, [0, 1, 2])
+f = [generate.uniform((d, R), 1, k, 0, 1) for k, d in enumerate(x.dims)]
+out = torch.empty((D, R), device="cuda")
 ctx = _lib.Context.get(0); lib = _lib.load(); st = torch.cuda.current_stream()
 strat = int(os.environ.get("STRAT", ops.MTTKRP_SEGMENTED))
 ts = []
@@ -14,4 +16,5 @@ for i in range(30):
     a.record(); ops.mttkrp(x, f, 0, strat, out=out, sync=False); b.record()
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b) * 1e3)
-print(" ".join(f"{t:.1f}" for t in ts))
+import statistics
+print(f"nnz {nnz} R {R} D {D} zipf {Z} strat {strat}: median {statistics.median(ts[3:]):.1f} us")
