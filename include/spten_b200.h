@@ -208,6 +208,11 @@ SPT_API int spt_mttkrp_plan_exec(spt_ctx* ctx, const spt_mttkrp_plan* plan,
  * rows per level served from shared memory. Any pointer may be NULL. */
 SPT_API int spt_mttkrp_plan_info(const spt_mttkrp_plan* plan, uint32_t* level_modes,
                                  uint32_t* hot_per_level, uint32_t* nhot);
+/* Waits for the stream that used the plan last (create or exec) and releases
+ * its arrays to the context's stream-ordered pool on that stream -- no
+ * device-wide synchronisation, so copies and kernels on other streams keep
+ * running. A plan executed on several streams must be idle on all but the last
+ * of them when it is destroyed; the context must outlive its plans. */
 SPT_API void spt_mttkrp_plan_destroy(spt_mttkrp_plan* plan);
 
 /* ---- multi-GPU MTTKRP (one process, one context per device) ---------------
