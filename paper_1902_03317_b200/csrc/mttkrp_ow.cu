@@ -33,7 +33,10 @@
 
 namespace {
 
-constexpr int kOwThreads = 256;
+#ifndef SPT_OW_THREADS
+#define SPT_OW_THREADS 384
+#endif
+constexpr int kOwThreads = SPT_OW_THREADS;
 constexpr int kOwWarps = kOwThreads / 32;
 constexpr int kOwU = 4;
 constexpr int kOwChunk = 288;  // entries of a share staged at a time (C1's share: 282)
@@ -269,7 +272,7 @@ __device__ __forceinline__ void ow_share(const OwParams& p, uint32_t w, uint32_t
 // sees 2 slots per CTA: a heavy row spanning most of the tensor is a run of a
 // few hundred CTA slots, not thousands of warp slots.
 template <int NM1, int G, int V>
-__global__ void __launch_bounds__(kOwThreads, 3) mttkrp_ow_kernel(OwParams p) {
+__global__ void __launch_bounds__(kOwThreads, 768 / kOwThreads) mttkrp_ow_kernel(OwParams p) {
   constexpr int S = 2 * kOwWarps;
   extern __shared__ __align__(16) uint32_t ow_smem[];
   const unsigned warp = threadIdx.x >> 5;
