@@ -832,6 +832,7 @@ class C4(Workload):
                 xs = base.clone()
                 ops.sort_lexicographic(xs, [mode] + [d for d in range(4) if d != mode])
                 self.xs.append(xs)
+        self.host_x = base.to_host()  # e2e: the caller's copy (draw order, unsorted)
         del base
         self.out = [torch.empty((d, self.R), dtype=torch.float32, device=f"cuda:{device}")
                     for d in self.dims]
@@ -854,6 +855,64 @@ class C4(Workload):
     def cpu_arrays(self):
         from paper_1902_03317_b200 import ops
         return _mode_sorted_sample_arrays(self, ops, 4)
+
+    # e2e through the public API from host buffers (the full workload)
+    E2E_PATH = ("ops.* -> C-ABI from pinned host buffers, every step: x (draw order, 2 GB) and "
+                "the four factors uploaded; per mode an MTTKRP plan built (a 67-bit key sort, the "
+                "preprocessing a host caller pays) and executed, its I x R result downloaded "
+                "while the next plan builds")
+
+    def e2e_host(self, device=0):
+        import torch
+        from paper_1902_03317_b200.coo import DeviceCOO
+        from paper_1902_03317_b200.staging import PinnedCOO, Pipeline
+        dev = torch.device("cuda", device)
+        n = self.nnz
+        hf = [f.cpu().pin_memory() for f in self.f]
+        for p_ in self.plans:
+            p_.close()
+        self.plans, self.xs, self.ops = [], [], []
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        host = {"pipe": Pipeline(dev), "px": PinnedCOO.from_host(self.host_x), "pf": hf}
+        host["dx"] = DeviceCOO(list(self.dims), [torch.empty(n, dtype=torch.int32, device=dev)
+                                                 for _ in self.dims],
+                               torch.empty(n, dtype=torch.float32, device=dev), None, True)
+        host["df"] = [torch.empty(tuple(f.shape), dtype=torch.float32, device=dev) for f in hf]
+        host["dout"] = self.out
+        host["out_m"] = [torch.empty((d, self.R), dtype=torch.float32).pin_memory()
+                         for d in self.dims]
+        return host
+
+    def e2e_step(self, host):
+        import torch
+        from paper_1902_03317_b200 import ops
+        from paper_1902_03317_b200.staging import Pipeline, chunk_bounds
+        pl = host["pipe"]
+        h2d = d2h = 0
+        pl.begin()
+        b = chunk_bounds(self.nnz, 4)
+        for lo, hi in zip(b[:-1], b[1:]):
+            h2d += host["px"].upload(host["dx"], lo, hi, pl.h2d)
+        ev_x = Pipeline.mark(pl.h2d)  # the plan builds start here
+        with torch.cuda.stream(pl.h2d):
+            for a, f in zip(host["df"], host["pf"]):
+                a.copy_(f, non_blocking=True)
+                h2d += f.numel() * 4
+        ev_f = Pipeline.mark(pl.h2d)
+        with torch.cuda.stream(pl.cmp):
+            pl.cmp.wait_event(ev_x)
+            for m in range(4):
+                plan = ops.mttkrp_plan(host["dx"], m, self.R)
+                pl.cmp.wait_event(ev_f)
+                ops.mttkrp(plan, host["df"], m, out=host["dout"][m], sync=False)
+                pl.d2h.wait_event(Pipeline.mark(pl.cmp))
+                with torch.cuda.stream(pl.d2h):
+                    host["out_m"][m].copy_(host["dout"][m], non_blocking=True)
+                d2h += host["out_m"][m].numel() * 4
+                plan.close()  # stream-ordered release: no device synchronisation
+        pl.end()
+        return h2d, d2h
 
 
 def _mode_sorted_sample_arrays(wl, ops, N):

@@ -101,3 +101,33 @@ def test_c5_e2e_small_matches_fp64():
     z = host["out_eq"].to_host()
     assert np.array_equal(z.values.view(np.uint32), (hx.values * hyv).view(np.uint32))
     assert all(np.array_equal(a, b) for a, b in zip(z.indices, hx.indices))
+
+
+def test_c4_e2e_small_matches_fp64():
+    """C4's host-buffer path (x in draw order uploaded, one plan per mode built
+    from the unsorted tensor and run, the I x R results downloaded) at 1/100
+    of the nnz."""
+    import bench
+    wl = bench.C4(20190210, 0, 0.01)
+    hx = wl.host_x
+    fs = [f.clone() for f in wl.f]
+    host = wl.e2e_host(0)
+    for _ in range(2):
+        for o in host["out_m"]:
+            o.fill_(np.nan)
+        h2d, d2h = wl.e2e_step(host)
+        torch.cuda.synchronize()
+    n = wl.nnz
+    assert h2d == n * 20 + sum(f.numel() * 4 for f in fs)
+    assert d2h == sum(o.numel() * 4 for o in host["out_m"])
+    idx = [torch.from_numpy(a.astype(np.int64)).cuda() for a in hx.indices]
+    val = torch.from_numpy(hx.values).cuda().to(torch.float64)
+    for m in range(4):
+        t = val[:, None].expand(-1, wl.R).clone()
+        for d in range(4):
+            if d != m:
+                t *= fs[d][idx[d]].to(torch.float64)
+        want = torch.zeros((wl.dims[m], wl.R), dtype=torch.float64, device="cuda")
+        want.index_add_(0, idx[m], t)
+        got = host["out_m"][m].cuda().to(torch.float64)
+        assert bool(((got - want).abs() <= 1e-5 * want.abs()).all()), m
