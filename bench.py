@@ -757,7 +757,9 @@ class C3(Workload):
             self.u.append(generate.uniform((self.dims[mode], R), seed, 300 + mode, -1.0, 1.0,
                                            device))
             max_nf = max(max_nf, fib.nfibs)
+        self.host_x = base.to_host()  # e2e: the caller's copy (draw order, unsorted)
         del base
+        self.max_nf = max_nf
         self.zv = DeviceCOO.empty([1, 1], max_nf, device)
         self.zm = DeviceCOO.empty([1, 1, 1], max_nf * R, device)
         for mode in range(3):
@@ -782,6 +784,80 @@ class C3(Workload):
         return {"workload": self.name, "baseline_config": "configs[2] (C3)", "dims": self.dims,
                 "nnz": self.nnz, "R": self.R, "nfibs": [f.nfibs for f in self.fib],
                 "mode0": "Zipf(1.1) over a seeded id permutation; modes 1,2 uniform"}
+
+    # e2e through the public API from host buffers (the full workload)
+    E2E_PATH = ("ops.* -> C-ABI from pinned host buffers, every step: x (draw order, 0.8 GB), "
+                "the three vectors and matrices uploaded; per mode x sorted mode-last and its "
+                "fiber index built on the device (the preprocessing a host caller pays), TTV and "
+                "TTM run and their full outputs (indices + values; TTM's is nfibs x R entries) "
+                "downloaded -- 24 GB down per step, which bounds it")
+
+    def e2e_host(self, device=0):
+        import torch
+        from paper_1902_03317_b200.coo import DeviceCOO
+        from paper_1902_03317_b200.staging import PinnedCOO, Pipeline
+        dev = torch.device("cuda", device)
+        n = self.nnz
+        host = {"pipe": Pipeline(dev), "px": PinnedCOO.from_host(self.host_x),
+                "pv": [v.cpu().pin_memory() for v in self.v],
+                "pu": [u.cpu().pin_memory() for u in self.u]}
+        self.xs, self.fib, self.ops = [], [], []
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+        def coo():
+            return DeviceCOO(list(self.dims), [torch.empty(n, dtype=torch.int32, device=dev)
+                                               for _ in self.dims],
+                             torch.empty(n, dtype=torch.float32, device=dev), None, True)
+        host["dx"], host["work"] = coo(), coo()
+        host["dv"] = [torch.empty_like(v, device=dev) for v in host["pv"]]
+        host["du"] = [torch.empty_like(u, device=dev) for u in host["pu"]]
+        host["out_v"] = PinnedCOO([1, 1], self.max_nf)
+        host["out_m"] = PinnedCOO([1, 1, 1], self.max_nf * self.R)
+        return host
+
+    def e2e_step(self, host):
+        import torch
+        from paper_1902_03317_b200 import ops
+        from paper_1902_03317_b200.coo import DeviceCOO
+        from paper_1902_03317_b200.staging import Pipeline, chunk_bounds
+        pl, R = host["pipe"], self.R
+        h2d = d2h = 0
+        pl.begin()
+        b = chunk_bounds(self.nnz, 4)
+        for lo, hi in zip(b[:-1], b[1:]):
+            h2d += host["px"].upload(host["dx"], lo, hi, pl.h2d)
+        with torch.cuda.stream(pl.h2d):
+            for d_, p_ in zip(host["dv"] + host["du"], host["pv"] + host["pu"]):
+                d_.copy_(p_, non_blocking=True)
+                h2d += p_.numel() * 4
+        ev_in = Pipeline.mark(pl.h2d)
+        with torch.cuda.stream(pl.cmp):
+            pl.cmp.wait_event(ev_in)
+            work = host["work"]
+            for m in range(3):
+                for a, s_ in zip(work.indices, host["dx"].indices):
+                    a.copy_(s_, non_blocking=True)
+                work.values.copy_(host["dx"].values, non_blocking=True)
+                work.sort_order = None
+                ops.sort_lexicographic(work, ops.mode_last_order(3, m), sync=False)
+                fib = ops.build_fiber_index(work, m)
+                nf = fib.nfibs
+                # the output buffers are shared by the modes: the previous
+                # download must have left them
+                pl.cmp.wait_event(Pipeline.mark(pl.d2h))
+                zv = ops.ttv(work, host["dv"][m], m, fib,
+                             out=DeviceCOO([1, 1], [a[:nf] for a in self.zv.indices[:2]],
+                                           self.zv.values[:nf]))
+                pl.d2h.wait_event(Pipeline.mark(pl.cmp))
+                d2h += host["out_v"].download(zv, pl.d2h)
+                zm = ops.ttm(work, host["du"][m], m, fib,
+                             out=DeviceCOO([1, 1, 1], [a[:nf * R] for a in self.zm.indices],
+                                           self.zm.values[:nf * R]))
+                pl.d2h.wait_event(Pipeline.mark(pl.cmp))
+                d2h += host["out_m"].download(zm, pl.d2h)
+        pl.end()
+        return h2d, d2h
 
     def cpu_arrays(self):
         # the first k entries of each mode-last sorted copy: whole fibers but

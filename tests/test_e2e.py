@@ -131,3 +131,26 @@ def test_c4_e2e_small_matches_fp64():
         want.index_add_(0, idx[m], t)
         got = host["out_m"][m].cuda().to(torch.float64)
         assert bool(((got - want).abs() <= 1e-5 * want.abs()).all()), m
+
+
+def test_c3_e2e_small_matches_device_ops():
+    """C3's host-buffer path (x in draw order uploaded, sorted mode-last and
+    indexed on the device per mode, TTV and TTM outputs downloaded) at 1/100
+    of the nnz: the last mode's downloaded outputs equal the ops run directly."""
+    import bench
+    from paper_1902_03317_b200 import ops
+    wl = bench.C3(20190210, 0, 0.01)
+    xs2, fib2 = wl.xs[2], wl.fib[2]
+    zv = ops.ttv(xs2, wl.v[2], 2, fib2)
+    zm = ops.ttm(xs2, wl.u[2], 2, fib2)
+    want_v, want_m = zv.to_host(), zm.to_host()
+    host = wl.e2e_host(0)
+    h2d, d2h = wl.e2e_step(host)
+    torch.cuda.synchronize()
+    got_v, got_m = host["out_v"].to_host(), host["out_m"].to_host()
+    nf = fib2.nfibs
+    assert all(np.array_equal(a[:nf], b) for a, b in zip(got_v.indices, want_v.indices))
+    assert np.array_equal(got_v.values[:nf].view(np.uint32), want_v.values.view(np.uint32))
+    assert all(np.array_equal(a[:nf * wl.R], b) for a, b in zip(got_m.indices, want_m.indices))
+    assert np.array_equal(got_m.values[:nf * wl.R].view(np.uint32), want_m.values.view(np.uint32))
+    assert h2d == wl.nnz * 16 + sum(v.numel() * 4 for v in host["pv"] + host["pu"])
