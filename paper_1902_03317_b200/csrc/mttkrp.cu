@@ -2095,11 +2095,13 @@ extern "C" int spt_mttkrp_f32(spt_ctx* ctx, const spt_coo* x, const float* const
   }
   if (strategy < SPT_MTTKRP_SEGMENTED || strategy > SPT_MTTKRP_SEGMENTED_WARP)
     return spt::set_error(SPT_EINVAL, "mttkrp: unknown strategy %d", strategy);
-  // Warp tiles win in the latency-bound small-problem regime (C1: 1M nnz,
-  // 29 vs 37 us); from ~2M nnz the persistent CTA-tile kernel wins (4M: 82 vs
-  // 94 us, C4 shape at 8M: 301 vs 528 us).
-  // Small inputs: one resident wave, a contiguous share per warp, no tile
-  // look-back (mttkrp_ow.cu; C1: ~2x the warp tiles).
+  // The rest (short rows, other ranks, unaligned operands): warp tiles win in
+  // the latency-bound small-problem regime (1M nnz: 29 vs 37 us); from ~2M nnz
+  // the persistent CTA-tile kernel wins (4M: 82 vs 94 us, C4 shape at 8M: 301
+  // vs 528 us).
+  // Inputs up to 32M entries whose rows average >= 16 entries: one resident
+  // wave, a contiguous share per warp, no tile look-back (mttkrp_ow.cu; C1 24
+  // vs 30 us, 10M entries 104 vs 138 us, 10M with Zipf(1.5) rows 114 vs 269).
   if (strategy == SPT_MTTKRP_SEGMENTED && spt::mttkrp_onewave_ok(x, R, d_factors, mode, d_out)) {
     SPT_TRY(spt::mttkrp_onewave(ctx, x, d_factors, mode, static_cast<uint32_t>(R), d_out, st));
     if (flags & SPT_FLAG_ASYNC) return SPT_OK;
