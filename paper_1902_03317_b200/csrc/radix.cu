@@ -207,9 +207,16 @@ __global__ void __launch_bounds__(kThreads, SPT_RADIX_MINB)
 
   const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint32_t bits = CB ? CB : bits_rt;
+  // Passes are chained by programmatic dependent launch: once every CTA of
+  // this pass has started, the next pass's CTAs may take the SMs this pass's
+  // last wave leaves idle; they take their ticket and clear their counters,
+  // then block in griddepcontrol.wait until this grid has completed and its
+  // writes are visible.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   for (int j = tid; j < WARPS * kBins / 2; j += kThreads)
     reinterpret_cast<uint4*>(pairs)[j] = make_uint4(0, 0, 0, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t tile_base = static_cast<uint64_t>(tile) * TILE;
@@ -454,9 +461,19 @@ int launch_pass(spt_ctx* ctx, const SrcDesc& s, const DstDesc& d, uint64_t n, ui
   SPT_TRY(ctx_status64(ctx, tiles * kBins, &status));
   uint32_t epoch;
   SPT_TRY(ctx_lookback(ctx, 0, 0, &epoch));
-  kern<<<static_cast<unsigned>(tiles), kThreads, smem, st>>>(s, d, n, shift, bits, base, status,
-                                                              epoch, ticket);
-  SPT_LAUNCHED(ctx);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(tiles));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  SPT_CUDA(cudaLaunchKernelEx(&cfg, kern, s, d, n, shift, bits, base,
+                              static_cast<unsigned long long*>(status), epoch, ticket));
+  ctx->launches++;
   return SPT_OK;
 }
 
