@@ -87,6 +87,8 @@ __device__ __forceinline__ int cmp_g(const MergeParams& p, uint64_t i, uint64_t 
 #endif
 template <int N, int G>
 __global__ void partition_g_kernel(MergeParams p, uint32_t* split) {
+  // the merge kernel's CTAs may become resident now (they wait for this grid)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / G;
   const unsigned lane = threadIdx.x & 31u, gl = lane % G;
   const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane - gl);
@@ -442,6 +444,10 @@ __global__ void __launch_bounds__(kPThreads, 2) merge64p_kernel(MergeParams p, u
     }
     spt::mbar_fence_init();
   }
+  // launched as a programmatic dependent of the partition kernel: the CTAs are
+  // resident and their barriers set up while it runs; its splits are read
+  // only after this wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   const uint64_t total = p.nx + p.ny;
   const unsigned lane = tid & 31u;
@@ -762,8 +768,18 @@ int launch64p_op(spt_ctx* ctx, MergeParams& p, cudaStream_t st) {
     per_sm = std::max(per_sm, 1);
   }
   const uint32_t nctas = std::min<uint32_t>(p.ntiles, (uint32_t)(per_sm * ctx->num_sms));
-  merge64p_kernel<N, OP><<<nctas, kPThreads, smem, st>>>(p, nctas);
-  SPT_LAUNCHED(ctx);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nctas);
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  SPT_CUDA(cudaLaunchKernelEx(&cfg, merge64p_kernel<N, OP>, p, nctas));
+  ctx->launches++;
   return SPT_OK;
 }
 
