@@ -90,6 +90,12 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (driver attach, several 100 ms) stalls CUDA
+            # calls of this process: let it deliver its first sample before the
+            # timed region begins; it keeps sampling every 100 ms through it
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 3.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
 
@@ -1524,6 +1530,7 @@ def main_ours(args, world, rank, local):
         gbs = by / (mean_ms / 1e3) / 1e9
         ops_out[op.name] = {"ms": round(mean_ms, 5),
                             "ms_median": round(statistics.median(op.times), 5),
+                            "ms_max": round(max(op.times), 5),
                             "alg_bytes": int(by), "GB_s": round(gbs, 1),
                             "frac": round(gbs / hbm, 4), "nnz_s": op.units / (mean_ms / 1e3),
                             "launches_per_call": op.launches / args.steps}
