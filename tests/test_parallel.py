@@ -194,3 +194,25 @@ def test_row_aligned_ranges_and_blocks():
         # the in-place tensor search (device arrays) gives the same cuts
         t = torch.from_numpy(rows.astype(np.int32))
         assert row_aligned_ranges(t, world) == rr and row_blocks(t, rr, n_rows) == bl
+
+
+def test_lower_bound_tuple_matches_packed_keys():
+    """The per-mode narrowing search used to cut y at x's splitter tuples
+    (device tensors in production; CPU tensors here) equals searchsorted on
+    packed keys, for present, absent, smallest and largest tuples."""
+    from types import SimpleNamespace
+    from paper_1902_03317_b200 import parallel
+    rng = np.random.default_rng(3)
+    dims = [40, 30, 20]
+    n = 5000
+    idx = np.stack([rng.integers(0, d, n) for d in dims])
+    order = [2, 0, 1]
+    key = (idx[2].astype(np.int64) * 40 + idx[0]) * 30 + idx[1]
+    perm = np.argsort(key, kind="stable")
+    idx, key = idx[:, perm], key[perm]
+    t = SimpleNamespace(indices=[torch.from_numpy(a.astype(np.int32)) for a in idx])
+    probes = [tuple(int(idx[d][i]) for d in order) for i in (0, 17, n // 2, n - 1)]
+    probes += [(0, 0, 0), (19, 39, 29), (7, 3, 29), (7, 4, 0)]
+    for tup in probes:
+        k = (tup[0] * 40 + tup[1]) * 30 + tup[2]
+        assert parallel._lower_bound_tuple(t, order, tup) == int(np.searchsorted(key, k, "left"))
