@@ -26,7 +26,10 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kIPT = 8;
+#ifndef SPT_MERGE_IPT
+#define SPT_MERGE_IPT 8
+#endif
+constexpr int kIPT = SPT_MERGE_IPT;
 constexpr int kTile = kThreads * kIPT;
 // Key arrays in shared memory get one pad word per 32 entries: the threads'
 // merge-path positions advance ~4 entries apart, which would otherwise fold
