@@ -98,13 +98,15 @@ __global__ void count_from_scan_kernel(const uint32_t* flags, const uint32_t* po
 // tiles. Sweep 1 counts the range's fiber heads, the CTA publishes the count
 // and gets its offset from one decoupled look-back over epoch-tagged 64-bit
 // count words (a per-tile look-back chain held 54% of the warps at the
-// barrier); sweep 2 re-reads the range (L2 hits: a range is ~100-200 KB),
-// scans each tile's head counts, compacts the head positions in shared memory
-// and writes them out coalesced. A tile is read as four warp-striped sweeps of
+// barrier); sweep 2 takes the head masks kept from sweep 1 (it re-reads the
+// index arrays, L2 hits, only past a range's first 8 tiles), scans each tile's
+// head counts, compacts the head positions in shared memory and writes them
+// out coalesced. A tile is read as four warp-striped sweeps of
 // 128-bit loads over each non-mode index array; a lane's first entry is
 // compared with the previous lane's last by shuffle. The last range appends
 // fptr[nfibs] = nnz.
 constexpr int kFibThreads = 256, kFibQuads = 4, kFibTile = kFibThreads * kFibQuads * 4;
+constexpr int kFibKeep = 8;  // tiles of a range whose head masks stay in registers
 
 template <bool VEC>
 __device__ __forceinline__ void fiber_tile_heads(const TupleCmp& t, uint64_t n, uint64_t tbase,
@@ -168,12 +170,26 @@ __global__ void __launch_bounds__(kFibThreads)
   const uint32_t tile_hi = min(tile_lo + tiles_per_cta, ntiles);
   uint32_t hd[kFibQuads];
 
-  // sweep 1: the range's head count
+  // sweep 1: the range's head count. The head masks of the range's first
+  // kFibKeep tiles (16 bits per thread and tile) stay in registers, so sweep 2
+  // re-reads the index arrays only for ranges longer than that.
   uint32_t mine = 0;
+  uint32_t keep[kFibKeep / 2];
+#pragma unroll
+  for (int k = 0; k < kFibKeep / 2; ++k) keep[k] = 0;
+#pragma unroll 1
   for (uint32_t tile = tile_lo; tile < tile_hi; ++tile) {
     fiber_tile_heads<VEC>(t, n, static_cast<uint64_t>(tile) * kFibTile, tid, lane, hd);
+    uint32_t m16 = 0;
 #pragma unroll
-    for (int q = 0; q < kFibQuads; ++q) mine += __popc(hd[q]);
+    for (int q = 0; q < kFibQuads; ++q) {
+      mine += __popc(hd[q]);
+      m16 |= hd[q] << (4 * q);
+    }
+    const uint32_t k = tile - tile_lo;
+#pragma unroll
+    for (int kk = 0; kk < kFibKeep; ++kk)
+      if (k == static_cast<uint32_t>(kk)) keep[kk / 2] |= m16 << (16 * (kk & 1));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
@@ -205,7 +221,17 @@ __global__ void __launch_bounds__(kFibThreads)
   // sweep 2: positions
   for (uint32_t tile = tile_lo; tile < tile_hi; ++tile) {
     const uint64_t tbase = static_cast<uint64_t>(tile) * kFibTile;
-    fiber_tile_heads<VEC>(t, n, tbase, tid, lane, hd);
+    const uint32_t k = tile - tile_lo;
+    if (k < kFibKeep) {
+      uint32_t m16 = 0;
+#pragma unroll
+      for (int kk = 0; kk < kFibKeep; ++kk)
+        if (k == static_cast<uint32_t>(kk)) m16 = (keep[kk / 2] >> (16 * (kk & 1))) & 0xffffu;
+#pragma unroll
+      for (int q = 0; q < kFibQuads; ++q) hd[q] = (m16 >> (4 * q)) & 0xfu;
+    } else {
+      fiber_tile_heads<VEC>(t, n, tbase, tid, lane, hd);
+    }
     uint32_t inc[kFibQuads], cnt[kFibQuads];
 #pragma unroll
     for (int q = 0; q < kFibQuads; ++q) {
