@@ -95,23 +95,26 @@ __global__ void count_from_scan_kernel(const uint32_t* flags, const uint32_t* po
 
 // build_fiber_index in one launch (P/src/tensor.cpp:92-120). The grid is a
 // few CTAs per SM; CTA r (ticket order) owns a contiguous range of 4096-entry
-// tiles. Sweep 1 counts the range's fiber heads, the CTA publishes the count
-// and gets its offset from one decoupled look-back over epoch-tagged 64-bit
-// count words (a per-tile look-back chain held 54% of the warps at the
-// barrier); sweep 2 takes the head masks kept from sweep 1 (it re-reads the
-// index arrays, L2 hits, only past a range's first 8 tiles), scans each tile's
-// head counts, compacts the head positions in shared memory and writes them
-// out coalesced. A tile is read as four warp-striped sweeps of
-// 128-bit loads over each non-mode index array; a lane's first entry is
-// compared with the previous lane's last by shuffle. The last range appends
-// fptr[nfibs] = nnz.
-constexpr int kFibThreads = 256, kFibQuads = 4, kFibTile = kFibThreads * kFibQuads * 4;
+// tiles, and inside a tile each of the 8 warps owns 512 consecutive entries
+// (four 128-entry quads read as 128-bit loads over each non-mode index array;
+// a lane's first entry is compared with the previous lane's last by shuffle).
+// Sweep 1 counts the fiber heads per (tile, warp) into shared memory -- the
+// head masks of the range's first 8 tiles stay in registers -- then the CTA
+// publishes its total, gets its offset from one decoupled look-back over
+// epoch-tagged 64-bit count words (a per-tile look-back chain held 54% of the
+// warps at the barrier) and scans the (tile, warp) counts once. Sweep 2 is
+// warp-local: every warp knows where its heads of every tile go, compacts
+// them in its own shared-memory slice and writes them out coalesced -- no CTA
+// barrier per tile (they were 43% of the stall samples). The last range
+// appends fptr[nfibs] = nnz.
+constexpr int kFibThreads = 256, kFibQuads = 4, kFibWarps = kFibThreads / 32;
+constexpr int kFibWarpEntries = kFibQuads * 128, kFibTile = kFibWarps * kFibWarpEntries;
 constexpr int kFibKeep = 8;  // tiles of a range whose head masks stay in registers
 
 template <bool VEC>
-__device__ __forceinline__ void fiber_tile_heads(const TupleCmp& t, uint64_t n, uint64_t tbase,
-                                                 unsigned tid, unsigned lane,
-                                                 uint32_t (&hd)[kFibQuads]) {
+__device__ __forceinline__ void fiber_tile_heads(const TupleCmp& t, uint64_t n, uint64_t wbase,
+                                                 unsigned lane, uint32_t (&hd)[kFibQuads]) {
+  // wbase: the warp's first entry of the tile; quad q, lane l: wbase + q*128 + l*4
 #pragma unroll
   for (int q = 0; q < kFibQuads; ++q) hd[q] = 0;
 #pragma unroll
@@ -121,7 +124,7 @@ __device__ __forceinline__ void fiber_tile_heads(const TupleCmp& t, uint64_t n, 
     uint32_t v[kFibQuads][4];
 #pragma unroll
     for (int q = 0; q < kFibQuads; ++q) {
-      const uint64_t e0 = tbase + q * (kFibThreads * 4) + tid * 4;
+      const uint64_t e0 = wbase + q * 128 + lane * 4;
       if (VEC && e0 + 4 <= n) {
         const uint4 u = __ldg(reinterpret_cast<const uint4*>(a + e0));
         v[q][0] = u.x, v[q][1] = u.y, v[q][2] = u.z, v[q][3] = u.w;
@@ -132,16 +135,23 @@ __device__ __forceinline__ void fiber_tile_heads(const TupleCmp& t, uint64_t n, 
     }
 #pragma unroll
     for (int q = 0; q < kFibQuads; ++q) {
-      const uint64_t e0 = tbase + q * (kFibThreads * 4) + tid * 4;
+      const uint64_t e0 = wbase + q * 128 + lane * 4;
       uint32_t prev = __shfl_up_sync(0xffffffffu, v[q][3], 1);
-      if (lane == 0) prev = (e0 > 0 && e0 < n) ? __ldg(a + e0 - 1) : ~v[q][0];
+      if (lane == 0) {
+        // the previous quad's last entry sits in lane 31 of the same warp
+        prev = q ? 0u : ((e0 > 0 && e0 < n) ? __ldg(a + e0 - 1) : ~v[q][0]);
+      }
+      if (q) {
+        const uint32_t last = __shfl_sync(0xffffffffu, v[q - 1][3], 31);
+        if (lane == 0) prev = last;
+      }
       hd[q] |= (v[q][0] != prev ? 1u : 0u) | (v[q][1] != v[q][0] ? 2u : 0u) |
                (v[q][2] != v[q][1] ? 4u : 0u) | (v[q][3] != v[q][2] ? 8u : 0u);
     }
   }
 #pragma unroll
   for (int q = 0; q < kFibQuads; ++q) {
-    const uint64_t e0 = tbase + q * (kFibThreads * 4) + tid * 4;
+    const uint64_t e0 = wbase + q * 128 + lane * 4;
     const uint32_t vq = e0 >= n ? 0u : (n - e0 < 4 ? static_cast<uint32_t>(n - e0) : 4u);
     if (e0 == 0 && vq) hd[q] |= 1u;  // entry 0 always starts a fiber
     hd[q] &= (1u << vq) - 1u;
@@ -153,11 +163,12 @@ __global__ void __launch_bounds__(kFibThreads)
     fiber_index_kernel(TupleCmp t, uint64_t n, uint32_t ntiles, uint32_t tiles_per_cta,
                        uint32_t* __restrict__ fptr, unsigned long long* status, uint32_t epoch,
                        unsigned long long* tile_ctr, unsigned long long* d_count) {
-  constexpr int WARPS = kFibThreads / 32;
-  __shared__ uint32_t s_rank;
+  constexpr int WARPS = kFibWarps;
+  __shared__ uint32_t s_rank, s_total;
   __shared__ unsigned long long s_base;
-  __shared__ uint32_t wsum[kFibQuads][WARPS];
-  __shared__ uint32_t out_s[kFibTile];
+  __shared__ uint32_t s_part[kFibThreads / 32];
+  __shared__ uint32_t out_s[kFibTile];            // a 512-word slice per warp
+  extern __shared__ uint32_t s_cnt[];             // [tiles_per_cta][WARPS] head counts
   const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   if (tid == 0) {
     const unsigned long long tk = atomicAdd(tile_ctr, 1ull);
@@ -168,37 +179,60 @@ __global__ void __launch_bounds__(kFibThreads)
   const uint32_t r = s_rank;
   const uint32_t tile_lo = min(r * tiles_per_cta, ntiles);
   const uint32_t tile_hi = min(tile_lo + tiles_per_cta, ntiles);
+  const uint32_t nt = tile_hi - tile_lo;
   uint32_t hd[kFibQuads];
 
-  // sweep 1: the range's head count. The head masks of the range's first
-  // kFibKeep tiles (16 bits per thread and tile) stay in registers, so sweep 2
-  // re-reads the index arrays only for ranges longer than that.
-  uint32_t mine = 0;
+  // sweep 1: head counts per (tile, warp); masks of the first kFibKeep tiles
+  // stay in registers (16 bits per thread and tile)
   uint32_t keep[kFibKeep / 2];
 #pragma unroll
   for (int k = 0; k < kFibKeep / 2; ++k) keep[k] = 0;
 #pragma unroll 1
-  for (uint32_t tile = tile_lo; tile < tile_hi; ++tile) {
-    fiber_tile_heads<VEC>(t, n, static_cast<uint64_t>(tile) * kFibTile, tid, lane, hd);
-    uint32_t m16 = 0;
+  for (uint32_t k = 0; k < nt; ++k) {
+    const uint64_t wbase =
+        static_cast<uint64_t>(tile_lo + k) * kFibTile + warp * kFibWarpEntries;
+    fiber_tile_heads<VEC>(t, n, wbase, lane, hd);
+    uint32_t m16 = 0, c = 0;
 #pragma unroll
     for (int q = 0; q < kFibQuads; ++q) {
-      mine += __popc(hd[q]);
+      c += __popc(hd[q]);
       m16 |= hd[q] << (4 * q);
     }
-    const uint32_t k = tile - tile_lo;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) s_cnt[k * WARPS + warp] = c;
 #pragma unroll
     for (int kk = 0; kk < kFibKeep; ++kk)
       if (k == static_cast<uint32_t>(kk)) keep[kk / 2] |= m16 << (16 * (kk & 1));
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-  if (lane == 0) wsum[0][warp] = mine;
   __syncthreads();
-  if (warp == 0) {
-    uint32_t range_total = 0;
+  // exclusive scan of the nt*WARPS counts (tile-major = entry order): a
+  // contiguous chunk per thread, then the chunks' sums over the CTA
+  const uint32_t M = nt * WARPS;
+  const uint32_t chunk = (M + kFibThreads - 1) / kFibThreads;
+  const uint32_t c_lo = min(tid * chunk, M), c_hi = min(c_lo + chunk, M);
+  uint32_t mine = 0;
+  for (uint32_t i = c_lo; i < c_hi; ++i) mine += s_cnt[i];
+  uint32_t inc = mine;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) range_total += wsum[0][w];
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_part[warp] = inc;
+  __syncthreads();
+  uint32_t pre = inc - mine, range_total = 0;
+#pragma unroll
+  for (int w = 0; w < kFibThreads / 32; ++w) {
+    if (w < static_cast<int>(warp)) pre += s_part[w];
+    range_total += s_part[w];
+  }
+  for (uint32_t i = c_lo; i < c_hi; ++i) {
+    const uint32_t v = s_cnt[i];
+    s_cnt[i] = pre;
+    pre += v;
+  }
+  if (warp == 0) {
     const unsigned long long ep = static_cast<unsigned long long>(epoch) << 34;
     if (lane == 0)
       spt::st_relaxed64(status + r, ep | ((r == 0 ? 2ull : 1ull) << 32) | range_total);
@@ -216,12 +250,14 @@ __global__ void __launch_bounds__(kFibThreads)
     }
   }
   __syncthreads();
-  unsigned long long base = s_base;
+  const unsigned long long base = s_base;
 
-  // sweep 2: positions
-  for (uint32_t tile = tile_lo; tile < tile_hi; ++tile) {
-    const uint64_t tbase = static_cast<uint64_t>(tile) * kFibTile;
-    const uint32_t k = tile - tile_lo;
+  // sweep 2, warp-local: the warp's heads of tile k go to fptr[base + s_cnt[k][warp] ...]
+  uint32_t* wout = out_s + warp * kFibWarpEntries;
+#pragma unroll 1
+  for (uint32_t k = 0; k < nt; ++k) {
+    const uint64_t wbase =
+        static_cast<uint64_t>(tile_lo + k) * kFibTile + warp * kFibWarpEntries;
     if (k < kFibKeep) {
       uint32_t m16 = 0;
 #pragma unroll
@@ -230,43 +266,31 @@ __global__ void __launch_bounds__(kFibThreads)
 #pragma unroll
       for (int q = 0; q < kFibQuads; ++q) hd[q] = (m16 >> (4 * q)) & 0xfu;
     } else {
-      fiber_tile_heads<VEC>(t, n, tbase, tid, lane, hd);
+      fiber_tile_heads<VEC>(t, n, wbase, lane, hd);
     }
-    uint32_t inc[kFibQuads], cnt[kFibQuads];
+    uint32_t run = 0;  // heads of the warp's earlier quads
 #pragma unroll
     for (int q = 0; q < kFibQuads; ++q) {
-      cnt[q] = __popc(hd[q]);
-      inc[q] = cnt[q];
+      const uint32_t c = __popc(hd[q]);
+      uint32_t in = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, inc[q], o);
-        if (lane >= o) inc[q] += u;
+        const uint32_t u = __shfl_up_sync(0xffffffffu, in, o);
+        if (lane >= o) in += u;
       }
-      if (lane == 31) wsum[q][warp] = inc[q];
-    }
-    __syncthreads();
-    uint32_t total = 0;
-#pragma unroll
-    for (int q = 0; q < kFibQuads; ++q) {
-      uint32_t pre = total;
-#pragma unroll
-      for (int w = 0; w < WARPS; ++w) {
-        if (w < static_cast<int>(warp)) pre += wsum[q][w];
-        total += wsum[q][w];
-      }
-      uint32_t pos = pre + inc[q] - cnt[q];
-      const uint32_t e0 = static_cast<uint32_t>(tbase) + q * (kFibThreads * 4) + tid * 4;
+      uint32_t pos = run + in - c;
+      const uint32_t e0 = static_cast<uint32_t>(wbase) + q * 128 + lane * 4;
       uint32_t h = hd[q];
       while (h) {
-        out_s[pos++] = e0 + (__ffs(h) - 1);
+        wout[pos++] = e0 + (__ffs(h) - 1);
         h &= h - 1;
       }
+      run += __shfl_sync(0xffffffffu, in, 31);
     }
-    __syncthreads();
-    uint32_t* dst = fptr + base;
-    for (uint32_t i = tid; i < total; i += kFibThreads) spt::st_stream(dst + i, out_s[i]);
-    base += total;
-    __syncthreads();  // out_s and wsum are reused by the next tile
+    __syncwarp();
+    uint32_t* dst = fptr + base + s_cnt[k * WARPS + warp];
+    for (uint32_t i = lane; i < run; i += 32) spt::st_stream(dst + i, wout[i]);
+    __syncwarp();  // the slice is reused by the next tile
   }
 }
 
@@ -485,7 +509,10 @@ int spt_fiber_index(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint32_t* d_f
       d_nfibs ? reinterpret_cast<unsigned long long*>(d_nfibs) : cnt64;
   if (n > 0) {
     const uint32_t ntiles = static_cast<uint32_t>((n + kFibTile - 1) / kFibTile);
-    const uint32_t grid = std::min<uint32_t>(ntiles, static_cast<uint32_t>(ctx->num_sms) * 5u);
+    // a few CTAs per SM; more when a range's (tile, warp) counts would not fit
+    // 24 KB of shared memory (ticket order keeps a larger grid safe)
+    const uint32_t grid = std::min<uint32_t>(
+        ntiles, std::max<uint32_t>(static_cast<uint32_t>(ctx->num_sms) * 5u, (ntiles + 767) / 768));
     const uint32_t tpc = (ntiles + grid - 1) / grid;
     unsigned long long* status;
     SPT_TRY(spt::ctx_status64(ctx, grid, &status));
@@ -493,12 +520,13 @@ int spt_fiber_index(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint32_t* d_f
     SPT_TRY(spt::ctx_lookback(ctx, 0, 0, &epoch));
     bool vec = true;
     for (int j = 0; j < t.n; ++j) vec = vec && spt::aligned16(t.idx[j]);
+    const size_t dsm = static_cast<size_t>(tpc) * kFibWarps * sizeof(uint32_t);  // <= 32 KB
     if (vec)
-      fiber_index_kernel<true><<<grid, kFibThreads, 0, st>>>(t, n, ntiles, tpc, d_fptr, status,
-                                                            epoch, ctx->d_tile_ctr, count_out);
+      fiber_index_kernel<true><<<grid, kFibThreads, dsm, st>>>(t, n, ntiles, tpc, d_fptr, status,
+                                                              epoch, ctx->d_tile_ctr, count_out);
     else
-      fiber_index_kernel<false><<<grid, kFibThreads, 0, st>>>(t, n, ntiles, tpc, d_fptr, status,
-                                                             epoch, ctx->d_tile_ctr, count_out);
+      fiber_index_kernel<false><<<grid, kFibThreads, dsm, st>>>(
+          t, n, ntiles, tpc, d_fptr, status, epoch, ctx->d_tile_ctr, count_out);
     SPT_LAUNCHED(ctx);
   } else {
     SPT_CUDA(cudaMemsetAsync(cnt32, 0, 4, st));
