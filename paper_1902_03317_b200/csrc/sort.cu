@@ -162,7 +162,8 @@ template <bool VEC>
 __global__ void __launch_bounds__(kFibThreads)
     fiber_index_kernel(TupleCmp t, uint64_t n, uint32_t ntiles, uint32_t tiles_per_cta,
                        uint32_t* __restrict__ fptr, unsigned long long* status, uint32_t epoch,
-                       unsigned long long* tile_ctr, unsigned long long* d_count) {
+                       unsigned long long* tile_ctr, unsigned long long* d_count,
+                       unsigned long long* h_count) {
   constexpr int WARPS = kFibWarps;
   __shared__ uint32_t s_rank, s_total;
   __shared__ unsigned long long s_base;
@@ -246,6 +247,10 @@ __global__ void __launch_bounds__(kFibThreads)
       if (r == gridDim.x - 1) {
         fptr[base + range_total] = static_cast<uint32_t>(n);
         if (d_count) *d_count = base + range_total;
+        if (h_count) {  // pinned host word (UVA): no copy, the caller only synchronises
+          *h_count = base + range_total;
+          __threadfence_system();
+        }
       }
     }
   }
@@ -520,13 +525,14 @@ int spt_fiber_index(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint32_t* d_f
     SPT_TRY(spt::ctx_lookback(ctx, 0, 0, &epoch));
     bool vec = true;
     for (int j = 0; j < t.n; ++j) vec = vec && spt::aligned16(t.idx[j]);
-    const size_t dsm = static_cast<size_t>(tpc) * kFibWarps * sizeof(uint32_t);  // <= 32 KB
+    const size_t dsm = static_cast<size_t>(tpc) * kFibWarps * sizeof(uint32_t);  // <= 24 KB
+    unsigned long long* hc = h_nfibs ? ctx->h_pinned : nullptr;
     if (vec)
-      fiber_index_kernel<true><<<grid, kFibThreads, dsm, st>>>(t, n, ntiles, tpc, d_fptr, status,
-                                                              epoch, ctx->d_tile_ctr, count_out);
+      fiber_index_kernel<true><<<grid, kFibThreads, dsm, st>>>(
+          t, n, ntiles, tpc, d_fptr, status, epoch, ctx->d_tile_ctr, count_out, hc);
     else
       fiber_index_kernel<false><<<grid, kFibThreads, dsm, st>>>(
-          t, n, ntiles, tpc, d_fptr, status, epoch, ctx->d_tile_ctr, count_out);
+          t, n, ntiles, tpc, d_fptr, status, epoch, ctx->d_tile_ctr, count_out, hc);
     SPT_LAUNCHED(ctx);
   } else {
     SPT_CUDA(cudaMemsetAsync(cnt32, 0, 4, st));
@@ -534,8 +540,10 @@ int spt_fiber_index(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint32_t* d_f
     SPT_LAUNCHED(ctx);
   }
   if (h_nfibs) {
-    SPT_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_nfibs ? (void*)d_nfibs : (void*)cnt64, 8,
-                             cudaMemcpyDeviceToHost, st));
+    if (n == 0)
+      SPT_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_nfibs ? (void*)d_nfibs : (void*)cnt64, 8,
+                               cudaMemcpyDeviceToHost, st));
+    // n > 0: the kernel's last range wrote the count into the pinned word itself
     SPT_CUDA(cudaStreamSynchronize(st));
     *h_nfibs = ctx->h_pinned[0];
   }
