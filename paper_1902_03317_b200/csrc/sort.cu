@@ -15,8 +15,6 @@
 // std::stable_sort produces, so the result is bit-identical to the reference,
 // duplicates included. Keys wider than 64 bits (C4: 67 bits, C5: 72 bits)
 // simply take a second chunk.
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -53,44 +51,11 @@ struct TupleCmp {
   int n;
 };
 
-// flag[m] = 1 iff entry m starts a new group of equal (selected-mode) tuples.
-__global__ void head_flags_kernel(TupleCmp t, uint32_t* flags, uint64_t n) {
-  uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (; m < n; m += stride) {
-    uint32_t f = (m == 0);
-    for (int j = 0; j < t.n && !f; ++j) f = t.idx[j][m] != t.idx[j][m - 1];
-    flags[m] = f;
-  }
-}
-
-// Coalesce: heads write the tuple and the sequential fp32 sum of their group
-// in storage order (acc = v[m]; acc += v[e] ...; P/src/tensor.cpp:79-88).
-__global__ void coalesce_write_kernel(TupleCmp t, const float* vals, const uint32_t* flags,
-                                      const uint32_t* pos, uint64_t n, TupleCmp out,
-                                      float* out_val) {
-  uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (; m < n; m += stride) {
-    if (!flags[m]) continue;
-    const uint32_t p = pos[m];
-    float acc = vals[m];
-    for (uint64_t e = m + 1; e < n && !flags[e]; ++e) acc += vals[e];
-    for (int j = 0; j < t.n; ++j) const_cast<uint32_t*>(out.idx[j])[p] = t.idx[j][m];
-    out_val[p] = acc;
-  }
-}
-
 __global__ void fptr_tail_kernel(uint32_t* fptr, const uint32_t* d_count32,
                                  unsigned long long* d_count64, uint64_t n) {
   const uint32_t nf = *d_count32;
   fptr[nf] = static_cast<uint32_t>(n);
   if (d_count64) *d_count64 = nf;
-}
-
-__global__ void count_from_scan_kernel(const uint32_t* flags, const uint32_t* pos, uint64_t n,
-                                       unsigned long long* out) {
-  *out = n ? (unsigned long long)pos[n - 1] + flags[n - 1] : 0ull;
 }
 
 // build_fiber_index in one launch (P/src/tensor.cpp:92-120). The grid is a
@@ -165,7 +130,7 @@ __global__ void __launch_bounds__(kFibThreads)
                        unsigned long long* tile_ctr, unsigned long long* d_count,
                        unsigned long long* h_count) {
   constexpr int WARPS = kFibWarps;
-  __shared__ uint32_t s_rank, s_total;
+  __shared__ uint32_t s_rank;
   __shared__ unsigned long long s_base;
   __shared__ uint32_t s_part[kFibThreads / 32];
   __shared__ uint32_t out_s[kFibTile];            // a 512-word slice per warp
@@ -296,6 +261,55 @@ __global__ void __launch_bounds__(kFibThreads)
     uint32_t* dst = fptr + base + s_cnt[k * WARPS + warp];
     for (uint32_t i = lane; i < run; i += 32) spt::st_stream(dst + i, wout[i]);
     __syncwarp();  // the slice is reused by the next tile
+  }
+}
+
+// Positions of the entries that start a new group of equal tuples over the
+// arrays of `t` (in order), then n as the sentinel; the count goes to *d_count
+// and, when h_count is given, into that pinned host word.
+int launch_heads(spt_ctx* ctx, const TupleCmp& t, uint64_t n, uint32_t* d_heads,
+                 unsigned long long* d_count, unsigned long long* h_count, cudaStream_t st) {
+  const uint32_t ntiles = static_cast<uint32_t>((n + kFibTile - 1) / kFibTile);
+  // a few CTAs per SM; more when a range's (tile, warp) counts would not fit
+  // 24 KB of shared memory (ticket order keeps a larger grid safe)
+  const uint32_t grid = std::min<uint32_t>(
+      ntiles, std::max<uint32_t>(static_cast<uint32_t>(ctx->num_sms) * 5u, (ntiles + 767) / 768));
+  const uint32_t tpc = (ntiles + grid - 1) / grid;
+  unsigned long long* status;
+  SPT_TRY(spt::ctx_status64(ctx, grid, &status));
+  uint32_t epoch;
+  SPT_TRY(spt::ctx_lookback(ctx, 0, 0, &epoch));
+  bool vec = true;
+  for (int j = 0; j < t.n; ++j) vec = vec && spt::aligned16(t.idx[j]);
+  const size_t dsm = static_cast<size_t>(tpc) * kFibWarps * sizeof(uint32_t);  // <= 24 KB
+  if (vec)
+    fiber_index_kernel<true><<<grid, kFibThreads, dsm, st>>>(
+        t, n, ntiles, tpc, d_heads, status, epoch, ctx->d_tile_ctr, d_count, h_count);
+  else
+    fiber_index_kernel<false><<<grid, kFibThreads, dsm, st>>>(
+        t, n, ntiles, tpc, d_heads, status, epoch, ctx->d_tile_ctr, d_count, h_count);
+  SPT_LAUNCHED(ctx);
+  return SPT_OK;
+}
+
+// Coalesce: output p is the tuple at heads[p] with the sequential fp32 sum of
+// its group in storage order (acc = v[m]; acc += v[e] ...; P/src/tensor.cpp:79-88
+// -- the order is the contract, so a group is one thread's chain).
+__global__ void coalesce_runs_kernel(TupleCmp t, const float* __restrict__ vals,
+                                     const uint32_t* __restrict__ heads,
+                                     const unsigned long long* __restrict__ count, TupleCmp out,
+                                     float* __restrict__ out_val) {
+  const uint64_t cnt = *count;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < cnt;
+       p += stride) {
+    const uint32_t m = heads[p], e = heads[p + 1];
+    float acc = vals[m];
+    for (uint32_t k = m + 1; k < e; ++k) acc += vals[k];
+#pragma unroll
+    for (int j = 0; j < SPT_MAX_ORDER; ++j)
+      if (j < t.n) const_cast<uint32_t*>(out.idx[j])[p] = t.idx[j][m];
+    out_val[p] = acc;
   }
 }
 
@@ -450,17 +464,13 @@ int spt_coalesce_f32(spt_ctx* ctx, const spt_coo* x, spt_coo* z, uint64_t* h_nnz
     if (d_nnz) SPT_CUDA(cudaMemsetAsync(d_nnz, 0, sizeof(uint64_t), st));
     return SPT_OK;
   }
-  size_t temp = 0;
-  SPT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                         static_cast<int64_t>(n), st));
-  const size_t fb = align_up(n * 4);
+  // group heads by the single-launch head-position kernel (the fiber index's,
+  // over all N index arrays), then one thread per output sums its group
   void* scratch;
-  SPT_TRY(spt::ctx_scratch(ctx, 2 * fb + align_up(temp) + 256, &scratch));
-  char* base = static_cast<char*>(scratch);
-  uint32_t* flags_d = reinterpret_cast<uint32_t*>(base);
-  uint32_t* pos = reinterpret_cast<uint32_t*>(base + fb);
-  void* tmp = base + 2 * fb;
-  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(base + 2 * fb + align_up(temp));
+  SPT_TRY(spt::ctx_scratch(ctx, 256 + align_up((n + 1) * 4), &scratch));
+  unsigned long long* cnt = static_cast<unsigned long long*>(scratch);
+  uint32_t* heads = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + 256);
+  unsigned long long* count_out = d_nnz ? reinterpret_cast<unsigned long long*>(d_nnz) : cnt;
   TupleCmp t{};
   TupleCmp o{};
   for (uint32_t d = 0; d < x->order; ++d) {
@@ -468,20 +478,10 @@ int spt_coalesce_f32(spt_ctx* ctx, const spt_coo* x, spt_coo* z, uint64_t* h_nnz
     o.idx[d] = z->idx[d];
   }
   t.n = o.n = static_cast<int>(x->order);
-  const unsigned g = grid_of(ctx, n);
-  head_flags_kernel<<<g, 256, 0, st>>>(t, flags_d, n);
-  SPT_LAUNCHED(ctx);
-  SPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, temp, flags_d, pos, static_cast<int64_t>(n), st));
-  ctx->launches += 2;
-  coalesce_write_kernel<<<g, 256, 0, st>>>(t, x->val, flags_d, pos, n, o, z->val);
-  SPT_LAUNCHED(ctx);
-  count_from_scan_kernel<<<1, 1, 0, st>>>(flags_d, pos, n,
-                                          d_nnz ? reinterpret_cast<unsigned long long*>(d_nnz)
-                                                : cnt);
+  SPT_TRY(launch_heads(ctx, t, n, heads, count_out, h_nnz ? ctx->h_pinned : nullptr, st));
+  coalesce_runs_kernel<<<grid_of(ctx, n), 256, 0, st>>>(t, x->val, heads, count_out, o, z->val);
   SPT_LAUNCHED(ctx);
   if (h_nnz) {
-    SPT_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_nnz ? (void*)d_nnz : (void*)cnt, 8,
-                             cudaMemcpyDeviceToHost, st));
     SPT_CUDA(cudaStreamSynchronize(st));
     *h_nnz = ctx->h_pinned[0];
     z->nnz = *h_nnz;
@@ -513,27 +513,7 @@ int spt_fiber_index(spt_ctx* ctx, const spt_coo* x, uint32_t mode, uint32_t* d_f
   unsigned long long* count_out =
       d_nfibs ? reinterpret_cast<unsigned long long*>(d_nfibs) : cnt64;
   if (n > 0) {
-    const uint32_t ntiles = static_cast<uint32_t>((n + kFibTile - 1) / kFibTile);
-    // a few CTAs per SM; more when a range's (tile, warp) counts would not fit
-    // 24 KB of shared memory (ticket order keeps a larger grid safe)
-    const uint32_t grid = std::min<uint32_t>(
-        ntiles, std::max<uint32_t>(static_cast<uint32_t>(ctx->num_sms) * 5u, (ntiles + 767) / 768));
-    const uint32_t tpc = (ntiles + grid - 1) / grid;
-    unsigned long long* status;
-    SPT_TRY(spt::ctx_status64(ctx, grid, &status));
-    uint32_t epoch;
-    SPT_TRY(spt::ctx_lookback(ctx, 0, 0, &epoch));
-    bool vec = true;
-    for (int j = 0; j < t.n; ++j) vec = vec && spt::aligned16(t.idx[j]);
-    const size_t dsm = static_cast<size_t>(tpc) * kFibWarps * sizeof(uint32_t);  // <= 24 KB
-    unsigned long long* hc = h_nfibs ? ctx->h_pinned : nullptr;
-    if (vec)
-      fiber_index_kernel<true><<<grid, kFibThreads, dsm, st>>>(
-          t, n, ntiles, tpc, d_fptr, status, epoch, ctx->d_tile_ctr, count_out, hc);
-    else
-      fiber_index_kernel<false><<<grid, kFibThreads, dsm, st>>>(
-          t, n, ntiles, tpc, d_fptr, status, epoch, ctx->d_tile_ctr, count_out, hc);
-    SPT_LAUNCHED(ctx);
+    SPT_TRY(launch_heads(ctx, t, n, d_fptr, count_out, h_nfibs ? ctx->h_pinned : nullptr, st));
   } else {
     SPT_CUDA(cudaMemsetAsync(cnt32, 0, 4, st));
     fptr_tail_kernel<<<1, 1, 0, st>>>(d_fptr, cnt32, count_out, n);
