@@ -57,3 +57,41 @@ def test_ttv_ttm_tew_protocols_deterministic(lib):
         z = ops.tew(a, b, ops.ADD)
         return [z.indices[0], z.indices[2], z.values]
     _same_every_run(merge)
+
+
+def test_sort_fiber_coalesce_onewave_deterministic(lib):
+    """The round-2 kernels with cross-block protocols: the radix passes
+    (tickets, per-bin look-back, passes chained by dependent launch), the
+    head-position kernel behind build_fiber_index and coalesce (tickets, one
+    look-back per CTA), the one-wave MTTKRP (CTA slots + dependent fold kernel)."""
+    generate, ops = lib
+    src = generate.coo([3000, 2000, 1500], 3_000_000, 6, [1.1, 0, 0], -1.0, 1.0)
+
+    def sort_it():
+        w = src.clone()
+        ops.sort_lexicographic(w, [2, 0, 1])
+        return [w.indices[0], w.indices[1], w.indices[2], w.values]
+    _same_every_run(sort_it)
+    wide = generate.coo([2_000_000, 500_000, 100_000, 1000], 1_500_000, 7, [1.2, 0, 0, 0], 0.0, 1.0)
+
+    def sort_wide():
+        w = wide.clone()
+        ops.sort_lexicographic(w, [3, 1, 0, 2])  # 67-bit key: two chunks, permutation payload
+        return [w.indices[3], w.indices[0], w.values]
+    _same_every_run(sort_wide)
+    t = src.clone()
+    ops.sort_lexicographic(t, ops.mode_last_order(3, 1))
+    _same_every_run(lambda: [ops.build_fiber_index(t, 1).fptr])
+    # duplicates for coalesce: fold the last mode onto 4 values
+    d = src.clone()
+    d.indices[2].remainder_(4)
+    d.dims = [3000, 2000, 4]
+    ops.sort_lexicographic(d, [0, 1, 2])
+
+    def coalesce():
+        z = ops.coalesce(d)
+        return [z.indices[0], z.indices[1], z.indices[2], z.values]
+    _same_every_run(coalesce)
+    x = generate.coo([4000, 900, 800], 6_000_000, 8, [1.3, 0, 0], 0.0, 1.0, [0, 1, 2])
+    fs = [generate.uniform((dd, 16), 8, 20 + k, 0.0, 1.0) for k, dd in enumerate(x.dims)]
+    _same_every_run(lambda: [ops.mttkrp(x, fs, 0, ops.MTTKRP_SEGMENTED)])
